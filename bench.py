@@ -1,0 +1,410 @@
+#!/usr/bin/env python3
+"""Benchmark driver (graft contract): one JSON line on rank 0.
+
+Default workload (N = 1 and under torchrun for N > 1): BASELINE.json config 3,
+``sum(x + x.T)`` on a 40000 x 40000 fp64 array in 2000 x 2000 chunks,
+round-robin row-major block ownership over N B200s, weak in
+nothing: the array is fixed, so ``scaling`` is "strong".
+
+* ``value``  : wall time per step (ms, max over ranks, CUDA events on the
+  launching stream) with x resident in HBM: fused transpose-add-reduce kernel
+  (partner tiles of other GPUs read over NVLink inside the kernel), block-sum
+  gather, final fsum on the host.
+* ``e2e``    : the same step through the public harness API with x in pinned
+  HOST memory: H2D of this rank's x blocks, kernel, D2H of the result.
+* ``roofline``: the fused kernel's algorithmic bytes / its event-timed
+  duration against MEASURED_PEAKS.json (HBM) or the measured 770 GB/s peer
+  copy (NVLink), whichever bounds it.
+* ``cpu_baseline``: the oracle (oracle/liboracle.so) on a bounded sample of
+  block pairs with x resident in host memory, all host threads.
+
+``--impl reference`` times the CPU restatement of the path (the reference has
+no operator code) on the same config; under torchrun only
+rank 0 runs it.  Other workloads: ``--workload key_merge|p2p``.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, HERE)
+
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+# -- environment ------------------------------------------------------------------------------
+
+
+def load_peaks() -> dict:
+    path = os.path.join(HERE, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            peaks = json.load(fh)
+        peaks["_source"] = "measured (MEASURED_PEAKS.json)"
+        return peaks
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+        self._reader = None
+
+    def start(self) -> None:
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._reader = threading.Thread(target=self._pump, daemon=True)
+        self._reader.start()
+
+    def _pump(self) -> None:
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self._reader:
+            self._reader.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+class Dist:
+    """Rank/world plumbing over torch.distributed (NCCL) when launched by torchrun."""
+
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.torch = None
+        self.gloo = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            torch.cuda.set_device(self.local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
+            self.gloo = dist.new_group(backend="gloo")
+            self.torch = torch
+            self.dist = dist
+
+    def barrier(self) -> None:
+        if self.world > 1:
+            self.dist.barrier(group=self.gloo)
+
+    def allgather_bytes(self, blob: bytes) -> list[bytes]:
+        if self.world == 1:
+            return [blob]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, blob, group=self.gloo)
+        return out
+
+    def max(self, value: float) -> float:
+        if self.world == 1:
+            return value
+        t = self.torch.tensor([value], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.gloo)
+        return float(t.item())
+
+    def sum(self, value: float) -> float:
+        if self.world == 1:
+            return value
+        t = self.torch.tensor([value], dtype=self.torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.gloo)
+        return float(t.item())
+
+    def close(self) -> None:
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def emit(line: dict) -> None:
+    print(json.dumps(line), flush=True)
+
+
+# -- transpose_sum -------------------------------------------------------------------------------
+
+
+def ts_cpu_sample(n: int, b: int, pairs: int, threads: int) -> dict:
+    """Oracle (C restatement) on `pairs` output blocks with x resident in host memory."""
+    import numpy as np
+
+    import oracle
+
+    nb = n // b
+    rng = np.random.default_rng(7)
+    ids = rng.choice(nb * nb, size=min(pairs, nb * nb), replace=False)
+    a_blocks, bt_blocks, y_blocks = [], [], []
+    for g in ids:
+        i, j = divmod(int(g), nb)
+        a_blocks.append(oracle.gen_block_c(n, i * b, j * b, b))
+        bt_blocks.append(oracle.gen_block_c(n, j * b, i * b, b))
+        y_blocks.append(np.empty((b, b)))
+    t0 = time.perf_counter()
+    oracle.transpose_sum_resident_c(a_blocks, bt_blocks, y_blocks, threads)
+    dt = time.perf_counter() - t0
+    per_block = dt / len(ids)
+    return {"seconds": dt, "blocks": len(ids), "per_block_s": per_block, "full_ms": per_block * nb * nb * 1e3}
+
+
+def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
+    from paper_2101_08878_b200 import native
+    from paper_2101_08878_b200.harness.transpose_sum import TransposeSum
+
+    n, b = args.n, args.block
+    device = dist.local_rank
+    native.set_device(device)
+    ts = TransposeSum(n, b, rank=dist.rank, world=dist.world, device=device,
+                      exchange=dist.allgather_bytes).setup()
+    stream = ts.stream
+    e0, e1 = native.Event(), native.Event()
+
+    def step():
+        return ts.step()
+
+    # warm-up (also the parity check against the oracle on sampled blocks)
+    for _ in range(args.warmup):
+        res = step()
+    checksum = res.checksum
+
+    # -- timed region: K full steps (kernel + gather + fsum) --
+    sampler = ClockSampler(device)
+    dist.barrier()
+    stream.synchronize()
+    sampler.start()
+    t_wall = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    e1.record(stream)
+    e1.synchronize()
+    wall_ms = (time.perf_counter() - t_wall) * 1e3 / args.steps
+    step_ms_local = max(e0.elapsed_ms(e1) / args.steps, wall_ms)
+    dist.barrier()
+    clocks = sampler.stop()
+    step_ms = dist.max(step_ms_local)
+    if res.checksum != checksum:
+        raise RuntimeError("checksum changed between steps")
+
+    # -- kernel-only timing for the roofline (same stream, K back-to-back launches) --
+    dist.barrier()
+    stream.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        ts.launch()
+    e1.record(stream)
+    e1.synchronize()
+    kernel_ms = dist.max(e0.elapsed_ms(e1) / args.steps)
+
+    alg = ts.algorithmic_bytes()
+    hbm_bytes = alg["hbm"]
+    nvl_bytes = alg["nvlink"]
+    hbm_peak = float(peaks["hbm_gbs"])
+    t_hbm = hbm_bytes / (hbm_peak * 1e9)
+    t_nvl = nvl_bytes / (NVLINK_PEER_GBS * 1e9)
+    if t_nvl > t_hbm:
+        roof = {"bound": "nvlink", "achieved": nvl_bytes / (kernel_ms * 1e-3) / 1e9, "peak": NVLINK_PEER_GBS,
+                "unit": "GB/s", "peak_source": "measured peer copy, B200_PROFILING.md"}
+    else:
+        roof = {"bound": "hbm", "achieved": hbm_bytes / (kernel_ms * 1e-3) / 1e9, "peak": hbm_peak,
+                "unit": "GB/s", "peak_source": peaks["_source"]}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = args.traffic
+    roof["kernel"] = "ts_kernel (transpose_sum.cu)"
+    roof["kernel_ms"] = kernel_ms
+    roof["algorithmic_bytes_per_launch"] = {"hbm": hbm_bytes, "nvlink": nvl_bytes}
+    roof["t_roof_ms"] = max(t_hbm, t_nvl) * 1e3
+
+    # -- e2e: x from pinned host memory through the public harness API --
+    e2e = None
+    if not args.skip_e2e:
+        pool = len(ts.owned) * ts.block_bytes
+        host = native.PinnedHostBuffer(pool)
+        native.memcpy(host.ptr, ts.x.ptr, pool, stream)  # snapshot x to host once (untimed)
+        stream.synchronize()
+        e2e_steps = max(1, min(args.steps, 3))
+        dist.barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            native.memcpy(ts.x.ptr, host.ptr, pool, stream)
+            r = ts.step()
+        e1.record(stream)
+        e1.synchronize()
+        e2e_ms = max(e0.elapsed_ms(e1), (time.perf_counter() - t0) * 1e3) / e2e_steps
+        e2e_ms = dist.max(e2e_ms)
+        if r.checksum != checksum:
+            raise RuntimeError("e2e checksum differs from the resident-input checksum")
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(dist.sum(pool)),
+               "d2h_bytes_per_step": int(dist.sum(len(ts.owned) * 8)), "steps": e2e_steps}
+        host.free()
+
+    # -- parity (outside timing): sampled block sums vs the oracle --
+    parity = None
+    cpu = None
+    if dist.rank == 0:
+        import oracle
+
+        sample = sorted(res.block_sums)[:: max(1, len(res.block_sums) // 8)][:8]
+        ref = oracle.transpose_sum_blocks_c(n, b, sample, threads=os.cpu_count() or 1)
+        worst = max(abs(res.block_sums[g] - r) / abs(r) for g, r in zip(sample, ref))
+        parity = {"sampled_blocks": len(sample), "max_rel_err": worst, "tolerance": 1e-12,
+                  "ok": worst <= 1e-12}
+        if not args.skip_cpu:
+            threads = len(os.sched_getaffinity(0))
+            cpu_s = ts_cpu_sample(n, b, args.cpu_pairs, threads)
+            cpu = {"value": cpu_s["full_ms"], "unit": "ms", "cores": threads, "kind": "port",
+                   "sample": f"oracle C restatement, {cpu_s['blocks']} of {ts.nb ** 2} output blocks "
+                             f"(x resident in host RAM), {cpu_s['seconds']:.2f} s, extrapolated to the "
+                             f"full {n}^2 array"}
+    ts.close()
+    if dist.rank != 0:
+        return None
+    launches = args.steps * native.lib().m4d_ts_launches_per_run()
+    return {
+        "metric": f"x+x.T sum wall time ({n}^2 fp64, {b}^2 chunks)",
+        "value": step_ms,
+        "unit": "ms",
+        "n_gpus": dist.world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": step_ms,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
+        "config": {"workload": "transpose_sum", "dims": n, "block": b, "workers": dist.world,
+                   "ownership": "round-robin row-major (SPEC.md:447)",
+                   "l2": "inputs (25.6 GB x+y) far larger than the 126 MB L2; no flush needed",
+                   "checksum": checksum},
+        "gpu_launches": launches,
+        "roofline": roof,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "parity": parity,
+        "clocks": clocks,
+        "wall_ms_per_step": wall_ms,
+    }
+
+
+def reference_transpose_sum(args) -> dict:
+    threads = len(os.sched_getaffinity(0))
+    per_step = []
+    for _ in range(args.warmup):
+        ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads)
+    for _ in range(args.steps):
+        per_step.append(ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads))
+    value = statistics.mean(s["full_ms"] for s in per_step)
+    nb = args.n // args.block
+    sample = (f"oracle C restatement (the reference has no operator code), {per_step[0]['blocks']} of "
+              f"{nb * nb} output blocks per step with x resident in host RAM, extrapolated to the full array")
+    return {
+        "impl": "reference",
+        "metric": f"x+x.T sum wall time ({args.n}^2 fp64, {args.block}^2 chunks)",
+        "value": value,
+        "unit": "ms",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": value,
+        "higher_is_better": False,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
+        "config": {"workload": "transpose_sum", "dims": args.n, "block": args.block},
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# -- main -------------------------------------------------------------------------------------------
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["transpose_sum"], default="transpose_sum")
+    ap.add_argument("--n", type=int, default=40000)
+    ap.add_argument("--block", type=int, default=2000)
+    ap.add_argument("--cpu-pairs", type=int, default=48, help="output blocks in the CPU baseline sample")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="dram bytes per launch from an ncu --set full capture (reported as roofline.traffic)")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("bench: W >= 3 warm-up steps required; raising to 3", file=sys.stderr)
+        args.warmup = 3
+
+    if args.impl == "reference":
+        if int(os.environ.get("RANK", "0")) != 0:
+            return 0
+        emit(reference_transpose_sum(args))
+        return 0
+
+    dist = Dist()
+    peaks = load_peaks()
+    try:
+        line = bench_transpose_sum(args, dist, peaks)
+    finally:
+        dist.close()
+    if line is not None:
+        emit(line)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,138 @@
+/*
+ * m4d.h — C ABI of libm4d.so, the B200-native data path behind the
+ * `commshim` drop-in package (paper_2101_08878_b200).
+ *
+ * Plain pointers, sizes and integer status codes only: no torch types cross
+ * this boundary.  Every function returns an `m4d_status` (0 = success); the
+ * message of the most recent failure on the calling thread is available from
+ * m4d_last_error().  Status codes map 1:1 onto the reference exception
+ * hierarchy (pkg/src/commshim/errors.py:6-89); see M4D_ERR_* below.
+ *
+ * Sections
+ *   1. status codes / library info
+ *   2. device helpers (streams, events, memory, IPC export/import)
+ *   3. transport (replaces pkg/src/commshim/transport/base.py:199-306
+ *      Transport.post_send/post_recv/test/progress/cancel/purge_channel,
+ *      selected by transport_init(kind="nvlink"), transport/__init__.py:42-76)
+ *   4. transpose_sum kernels
+ *   5. key_merge kernels
+ *
+ * Threading: a context (m4d_ctx) belongs to one executor thread
+ * (reference base.py:9-11); the library starts no host threads.
+ */
+#ifndef M4D_H
+#define M4D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------------ */
+/* 1. status codes                                                          */
+/* ------------------------------------------------------------------------ */
+
+typedef int m4d_status;
+
+enum {
+    M4D_OK = 0,
+    M4D_ERR_CONFIGURATION = 1,  /* errors.ConfigurationError            */
+    M4D_ERR_STARTUP = 2,        /* errors.StartupError(rank)            */
+    M4D_ERR_USAGE = 3,          /* errors.UsageError                    */
+    M4D_ERR_CHANNEL = 4,        /* errors.ChannelError                  */
+    M4D_ERR_COUNT_OVERFLOW = 5, /* errors.CountOverflowError            */
+    M4D_ERR_TRANSFER = 6,       /* errors.TransferError(bytes_moved)    */
+    M4D_ERR_TRUNCATION = 7,     /* errors.TruncationError               */
+    M4D_ERR_CANCELLED = 8,      /* errors.CancelledTransferError        */
+    M4D_ERR_PROTOCOL = 9,       /* errors.ProtocolError                 */
+    M4D_ERR_CLOSED = 10,        /* errors.CommClosedError               */
+    M4D_ERR_BUSY = 11,          /* errors.BusyError                     */
+    M4D_ERR_CUDA = 12,          /* CUDA runtime failure (TransferError) */
+    M4D_ERR_NOMEM = 13,         /* host allocation failure              */
+    M4D_ERR_CAPACITY = 14       /* output buffer too small; retry with the reported size */
+};
+
+/* Copies the last failure message of this thread (NUL-terminated). */
+size_t m4d_last_error(char* buf, size_t n);
+/* Library ABI version: (major << 16) | minor. */
+int m4d_version(void);
+/* Number of visible CUDA devices (0 on a host without a driver; never fails). */
+int m4d_device_count(void);
+
+/* ------------------------------------------------------------------------ */
+/* 2. device helpers                                                        */
+/* ------------------------------------------------------------------------ */
+
+m4d_status m4d_set_device(int device);
+m4d_status m4d_stream_create(int device, void** stream_out);  /* non-blocking stream */
+m4d_status m4d_stream_destroy(void* stream);
+m4d_status m4d_stream_sync(void* stream);
+m4d_status m4d_device_sync(int device);
+/* Event timing on a given stream (the stream the kernel is launched on). */
+m4d_status m4d_event_create(void** ev_out);
+m4d_status m4d_event_destroy(void* ev);
+m4d_status m4d_event_record(void* ev, void* stream);
+m4d_status m4d_event_sync(void* ev);
+m4d_status m4d_event_elapsed_ms(void* start, void* stop, float* ms_out);
+m4d_status m4d_malloc(int device, size_t nbytes, void** ptr_out);
+m4d_status m4d_free(void* ptr);
+m4d_status m4d_host_alloc(size_t nbytes, void** ptr_out);   /* pinned */
+m4d_status m4d_host_free(void* ptr);
+m4d_status m4d_memcpy(void* dst, const void* src, size_t nbytes, void* stream); /* async, any direction */
+m4d_status m4d_memset(void* dst, int value, size_t nbytes, void* stream);
+/* Legacy CUDA IPC: 64-byte handle of the allocation containing `ptr`;
+ * `offset_out` is ptr - allocation base. */
+m4d_status m4d_ipc_export(const void* ptr, uint8_t handle_out[64], uint64_t* offset_out);
+m4d_status m4d_ipc_import(int device, const uint8_t handle[64], void** base_out);
+m4d_status m4d_ipc_close(void* base);
+/* Enables peer access between two devices in this process (same-process multi-rank mode). */
+m4d_status m4d_enable_peer(int device, int peer_device);
+
+/* ------------------------------------------------------------------------ */
+/* 4. transpose_sum (K3/K4)                                                 */
+/* ------------------------------------------------------------------------ */
+
+/* x[r, c] = (splitmix64(seed ^ (r * n + c)) >> 11) * 2^-53 for the b x b block
+ * whose top-left global element is (row0, col0); dst is row-major b*b. */
+m4d_status m4d_fill_block_f64(double* dst, int64_t n, int64_t row0, int64_t col0,
+                              int64_t b, uint64_t seed, void* stream);
+
+/* One output block y(i,j) = x(i,j) + x(j,i)^T of a chunked square array.
+ *   a  : x(i,j), local, row-major b*b
+ *   bt : x(j,i), local OR a peer-mapped pointer (read over NVLink, no staging)
+ *   y  : y(i,j) output, local
+ *   y2 : y(j,i) output when it is also owned here (pairs the two outputs so
+ *        x is read once), else NULL.  For a diagonal block (i == j) pass
+ *        a == bt, y2 == NULL and diag = 1.
+ * slot_y / slot_y2 index the per-block sum array handed to m4d_ts_run. */
+typedef struct m4d_ts_task {
+    const double* a;
+    const double* bt;
+    double* y;
+    double* y2;
+    int32_t slot_y;
+    int32_t slot_y2;
+    int32_t diag;
+    int32_t reserved;
+} m4d_ts_task;
+
+typedef struct m4d_ts_plan m4d_ts_plan;
+
+m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks,
+                              int64_t block, int nslots, m4d_ts_plan** plan_out);
+/* Launches the fused transpose-add-reduce kernel (one launch).  Writes
+ * block_sums[nslots] (device, fp64, deterministic fixed-order reduction of
+ * each output block) and *total (device, sequential sum of block_sums in slot
+ * order; may be NULL). */
+m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void* stream);
+m4d_status m4d_ts_plan_destroy(m4d_ts_plan* plan);
+/* Number of kernel launches one m4d_ts_run issues (for gpu_launches accounting). */
+int m4d_ts_launches_per_run(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* M4D_H */

@@ -1,0 +1,200 @@
+// Device plumbing exported through the C ABI: errors, streams, events,
+// allocation and legacy CUDA IPC (export/import of allocations so a peer
+// process on another B200 can read or write them over NVLink).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "m4d_internal.h"
+
+namespace m4d {
+
+static thread_local char g_last_error[512];
+
+int fail(int code, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_last_error, sizeof g_last_error, fmt, ap);
+    va_end(ap);
+    return code;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point, so the
+// library never links libcuda directly (it must load on GPU-less hosts).
+typedef CUresult (*PFN_getAddressRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+static PFN_getAddressRange address_range_fn() {
+    static PFN_getAddressRange fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_getAddressRange>(p);
+    });
+    return fn;
+}
+
+}  // namespace m4d
+
+using namespace m4d;
+
+extern "C" {
+
+size_t m4d_last_error(char* buf, size_t n) {
+    size_t len = strlen(g_last_error);
+    if (buf && n) {
+        size_t c = len < n - 1 ? len : n - 1;
+        memcpy(buf, g_last_error, c);
+        buf[c] = 0;
+    }
+    return len;
+}
+
+int m4d_version(void) { return (1 << 16) | 0; }
+
+int m4d_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+m4d_status m4d_set_device(int device) {
+    M4D_CUDA_TRY(cudaSetDevice(device));
+    return M4D_OK;
+}
+
+m4d_status m4d_stream_create(int device, void** stream_out) {
+    M4D_CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t s;
+    M4D_CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    *stream_out = s;
+    return M4D_OK;
+}
+
+m4d_status m4d_stream_destroy(void* stream) {
+    M4D_CUDA_TRY(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+    return M4D_OK;
+}
+
+m4d_status m4d_stream_sync(void* stream) {
+    M4D_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return M4D_OK;
+}
+
+m4d_status m4d_device_sync(int device) {
+    M4D_CUDA_TRY(cudaSetDevice(device));
+    M4D_CUDA_TRY(cudaDeviceSynchronize());
+    return M4D_OK;
+}
+
+m4d_status m4d_event_create(void** ev_out) {
+    cudaEvent_t e;
+    M4D_CUDA_TRY(cudaEventCreate(&e));
+    *ev_out = e;
+    return M4D_OK;
+}
+
+m4d_status m4d_event_destroy(void* ev) {
+    M4D_CUDA_TRY(cudaEventDestroy(static_cast<cudaEvent_t>(ev)));
+    return M4D_OK;
+}
+
+m4d_status m4d_event_record(void* ev, void* stream) {
+    M4D_CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(ev), static_cast<cudaStream_t>(stream)));
+    return M4D_OK;
+}
+
+m4d_status m4d_event_sync(void* ev) {
+    M4D_CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(ev)));
+    return M4D_OK;
+}
+
+m4d_status m4d_event_elapsed_ms(void* start, void* stop, float* ms_out) {
+    M4D_CUDA_TRY(cudaEventElapsedTime(ms_out, static_cast<cudaEvent_t>(start),
+                                      static_cast<cudaEvent_t>(stop)));
+    return M4D_OK;
+}
+
+m4d_status m4d_malloc(int device, size_t nbytes, void** ptr_out) {
+    M4D_CUDA_TRY(cudaSetDevice(device));
+    M4D_CUDA_TRY(cudaMalloc(ptr_out, nbytes ? nbytes : 1));
+    return M4D_OK;
+}
+
+m4d_status m4d_free(void* ptr) {
+    M4D_CUDA_TRY(cudaFree(ptr));
+    return M4D_OK;
+}
+
+m4d_status m4d_host_alloc(size_t nbytes, void** ptr_out) {
+    M4D_CUDA_TRY(cudaHostAlloc(ptr_out, nbytes ? nbytes : 1, cudaHostAllocPortable));
+    return M4D_OK;
+}
+
+m4d_status m4d_host_free(void* ptr) {
+    M4D_CUDA_TRY(cudaFreeHost(ptr));
+    return M4D_OK;
+}
+
+m4d_status m4d_memcpy(void* dst, const void* src, size_t nbytes, void* stream) {
+    if (!nbytes) return M4D_OK;
+    M4D_CUDA_TRY(cudaMemcpyAsync(dst, src, nbytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+    return M4D_OK;
+}
+
+m4d_status m4d_memset(void* dst, int value, size_t nbytes, void* stream) {
+    if (!nbytes) return M4D_OK;
+    M4D_CUDA_TRY(cudaMemsetAsync(dst, value, nbytes, static_cast<cudaStream_t>(stream)));
+    return M4D_OK;
+}
+
+m4d_status m4d_ipc_export(const void* ptr, uint8_t handle_out[64], uint64_t* offset_out) {
+    PFN_getAddressRange range = address_range_fn();
+    if (!range) return fail(M4D_ERR_CUDA, "cuMemGetAddressRange entry point unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+        return fail(M4D_ERR_USAGE, "pointer %p is not a device allocation", ptr);
+    cudaIpcMemHandle_t h;
+    M4D_CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle_out, &h, 64);
+    *offset_out = reinterpret_cast<uint64_t>(ptr) - static_cast<uint64_t>(base);
+    return M4D_OK;
+}
+
+m4d_status m4d_ipc_import(int device, const uint8_t handle[64], void** base_out) {
+    M4D_CUDA_TRY(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, 64);
+    M4D_CUDA_TRY(cudaIpcOpenMemHandle(base_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return M4D_OK;
+}
+
+m4d_status m4d_ipc_close(void* base) {
+    M4D_CUDA_TRY(cudaIpcCloseMemHandle(base));
+    return M4D_OK;
+}
+
+m4d_status m4d_enable_peer(int device, int peer_device) {
+    if (device == peer_device) return M4D_OK;
+    int ok = 0;
+    M4D_CUDA_TRY(cudaDeviceCanAccessPeer(&ok, device, peer_device));
+    if (!ok) return fail(M4D_ERR_CONFIGURATION, "device %d cannot access peer %d", device, peer_device);
+    M4D_CUDA_TRY(cudaSetDevice(device));
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return M4D_OK;
+    }
+    M4D_CUDA_TRY(e);
+    return M4D_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,35 @@
+// Internal helpers shared by the libm4d translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include "m4d.h"
+
+namespace m4d {
+
+// Records a formatted message for m4d_last_error() and returns `code`.
+int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+
+inline int cuda_fail(cudaError_t err, const char* what) {
+    return fail(M4D_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
+}
+
+}  // namespace m4d
+
+#define M4D_CUDA_TRY(expr)                                         \
+    do {                                                           \
+        cudaError_t m4d_err__ = (expr);                            \
+        if (m4d_err__ != cudaSuccess) return m4d::cuda_fail(m4d_err__, #expr); \
+    } while (0)
+
+// splitmix64 finaliser with the golden-ratio increment (Steele et al. 2014);
+// the generator of BASELINE.md §3 / SURVEY.md §8(d).
+__host__ __device__ __forceinline__ uint64_t m4d_splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
