@@ -296,8 +296,8 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
         sample = sorted(res.block_sums)[:: max(1, len(res.block_sums) // 8)][:8]
         ref = oracle.transpose_sum_blocks_c(n, b, sample, threads=os.cpu_count() or 1)
         worst = max(abs(res.block_sums[g] - r) / abs(r) for g, r in zip(sample, ref))
-        parity = {"sampled_blocks": len(sample), "max_rel_err": worst, "tolerance": 1e-12,
-                  "ok": worst <= 1e-12}
+        parity = {"sampled_blocks": len(sample), "max_rel_err": float(worst), "tolerance": 1e-12,
+                  "ok": bool(worst <= 1e-12)}
         if not args.skip_cpu:
             threads = len(os.sched_getaffinity(0))
             cpu_s = ts_cpu_sample(n, b, args.cpu_pairs, threads)

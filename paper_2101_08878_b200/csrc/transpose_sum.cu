@@ -21,19 +21,32 @@
 // pattern), and the last block folds the block sums, so one launch per step.
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
 #include "m4d_internal.h"
+#include "ptx.cuh"
 
 namespace {
 
 constexpr int kTile = 64;
-constexpr int kPitch = kTile + 1;
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerWarp = kTile / kWarps;  // 8
-constexpr size_t kSmemBytes = 2ull * kTile * kPitch * sizeof(double);
+
+// v1 (LDG) path: padded pitch 65 -> conflict-free 64-bit column reads.
+constexpr int kPitchLdg = kTile + 1;
+constexpr size_t kSmemLdg = 2ull * kTile * kPitchLdg * sizeof(double);
+
+// v2 (TMA bulk) path: rows must be 16-byte aligned -> pitch 66 (2-way conflicts
+// on the transposed read, far below the smem bandwidth budget).
+constexpr int kPitchTma = kTile + 2;
+constexpr int kStages = 3;
+constexpr int kTmaThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
+constexpr size_t kTileBytesTma = static_cast<size_t>(kTile) * kPitchTma * sizeof(double);
+constexpr size_t kSmemTma = kStages * 2 * kTileBytesTma;
 
 struct TsParams {
     const m4d_ts_task* tasks;
@@ -41,12 +54,20 @@ struct TsParams {
     int ntasks;
     int T;                    // tiles per block edge
     int64_t b;                // block edge (elements)
+    int64_t items;            // total tile items
     int nslots;
     double* tile_sums;        // [nslots][T*T]
     unsigned* block_done;     // [nslots]
     unsigned* all_done;       // [1]
+    unsigned long long* work; // [1] dynamic item cursor (TMA path)
+    unsigned* exits;          // [1] CTAs done (TMA path)
     double* block_sums;       // [nslots]
     double* total;            // [1] or null
+};
+
+struct Item {
+    int task;
+    int tr, tc;
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -63,71 +84,36 @@ __device__ __forceinline__ double warp_fold(const double* v, int n, int lane) {
     return warp_sum(s);
 }
 
-__global__ void __launch_bounds__(kThreads, 3) ts_kernel(TsParams p) {
-    extern __shared__ double smem[];
-    double* sA = smem;                   // sA[r][c] = x(i,j)[R0+r][C0+c]
-    double* sB = smem + kTile * kPitch;  // sB[r][c] = x(j,i)[C0+r][R0+c]
-    __shared__ double part[2][kWarps];
-    __shared__ int finished[2];
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const int64_t item = blockIdx.x;
-
-    // Locate the task owning this item (prefix offsets, binary search).
+__device__ __forceinline__ Item decode_item(const TsParams& p, int64_t item) {
     int lo = 0, hi = p.ntasks - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
         if (p.item_off[mid] <= item) lo = mid; else hi = mid - 1;
     }
-    const m4d_ts_task task = p.tasks[lo];
+    Item it;
+    it.task = lo;
     int64_t local = item - p.item_off[lo];
     const int T = p.T;
-    int tr, tc;
-    if (task.diag) {  // upper triangle of the tile grid, row by row
-        tr = 0;
+    if (p.tasks[lo].diag) {  // upper triangle of the tile grid, row by row
+        int tr = 0;
         while (local >= T - tr) { local -= T - tr; ++tr; }
-        tc = tr + static_cast<int>(local);
+        it.tr = tr;
+        it.tc = tr + static_cast<int>(local);
     } else {
-        tr = static_cast<int>(local / T);
-        tc = static_cast<int>(local % T);
+        it.tr = static_cast<int>(local / T);
+        it.tc = static_cast<int>(local % T);
     }
-    const bool second = task.diag ? (tr != tc) : (task.y2 != nullptr);
-    double* const y2 = task.diag ? task.y : task.y2;
-    const int slot2 = task.diag ? task.slot_y : task.slot_y2;
+    return it;
+}
 
-    const int64_t b = p.b;
-    const int64_t R0 = static_cast<int64_t>(tr) * kTile;
-    const int64_t C0 = static_cast<int64_t>(tc) * kTile;
-
-    // Phase 1: stage both x tiles (coalesced rows, streaming loads).
-#pragma unroll
-    for (int k = 0; k < kRowsPerWarp; ++k) {
-        const int r = warp * kRowsPerWarp + k;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int c = lane + 32 * h;
-            double av = 0.0;
-            if (R0 + r < b && C0 + c < b) av = __ldcs(task.a + (R0 + r) * b + (C0 + c));
-            sA[r * kPitch + c] = av;
-        }
-    }
-#pragma unroll
-    for (int k = 0; k < kRowsPerWarp; ++k) {
-        const int r = warp * kRowsPerWarp + k;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int c = lane + 32 * h;
-            double bv = 0.0;
-            if (C0 + r < b && R0 + c < b) bv = __ldcs(task.bt + (C0 + r) * b + (R0 + c));
-            sB[r * kPitch + c] = bv;
-        }
-    }
-    __syncthreads();
-
-    // Phase 2: y(i,j)[R0+r][C0+c] = sA[r][c] + sB[c][r];
-    //          y(j,i)[C0+r][R0+c] = sB[r][c] + sA[c][r]   (paired / diagonal).
-    double s1 = 0.0, s2 = 0.0;
+// y(i,j)[R0+r][C0+c] = sA[r][c] + sB[c][r];  y(j,i)[C0+r][R0+c] = sB[r][c] + sA[c][r].
+// Thread (warp w, lane l) owns rows w*8..w*8+7, columns l and l+32 of both
+// output tiles and accumulates them in that fixed order (the determinism
+// contract: identical per-tile sums for paired and single computation).
+template <int PITCH>
+__device__ __forceinline__ void transpose_add_tile(const double* sA, const double* sB, double* y, double* y2,
+                                                   bool second, int64_t b, int64_t R0, int64_t C0, int warp,
+                                                   int lane, double& s1, double& s2) {
 #pragma unroll
     for (int k = 0; k < kRowsPerWarp; ++k) {
         const int r = warp * kRowsPerWarp + k;
@@ -135,17 +121,210 @@ __global__ void __launch_bounds__(kThreads, 3) ts_kernel(TsParams p) {
         for (int h = 0; h < 2; ++h) {
             const int c = lane + 32 * h;
             if (R0 + r < b && C0 + c < b) {
-                const double v = sA[r * kPitch + c] + sB[c * kPitch + r];
-                __stcs(task.y + (R0 + r) * b + (C0 + c), v);
+                const double v = sA[r * PITCH + c] + sB[c * PITCH + r];
+                __stcs(y + (R0 + r) * b + (C0 + c), v);
                 s1 += v;
             }
             if (second && C0 + r < b && R0 + c < b) {
-                const double w = sB[r * kPitch + c] + sA[c * kPitch + r];
+                const double w = sB[r * PITCH + c] + sA[c * PITCH + r];
                 __stcs(y2 + (C0 + r) * b + (R0 + c), w);
                 s2 += w;
             }
         }
     }
+}
+
+// Records one item's tile sums; the CTA that completes an output block folds
+// its tile sums, and the one completing the last block folds the block sums.
+// Called by all 32 lanes of one warp after t1/t2 are final.
+__device__ __forceinline__ void finish_item(const TsParams& p, const m4d_ts_task& task, int tr, int tc,
+                                            bool second, int slot2, double t1, double t2, int lane) {
+    const int T = p.T;
+    const int tiles = T * T;
+    int fin0 = -1, fin1 = -1;
+    if (lane == 0) {
+        p.tile_sums[static_cast<int64_t>(task.slot_y) * tiles + tr * T + tc] = t1;
+        if (second) p.tile_sums[static_cast<int64_t>(slot2) * tiles + tc * T + tr] = t2;
+        __threadfence();
+        if (second && slot2 == task.slot_y) {
+            if (atomicAdd(p.block_done + task.slot_y, 2u) + 2u == static_cast<unsigned>(tiles)) fin0 = task.slot_y;
+        } else {
+            if (atomicAdd(p.block_done + task.slot_y, 1u) + 1u == static_cast<unsigned>(tiles)) fin0 = task.slot_y;
+            if (second && atomicAdd(p.block_done + slot2, 1u) + 1u == static_cast<unsigned>(tiles)) fin1 = slot2;
+        }
+        __threadfence();
+    }
+    fin0 = __shfl_sync(0xffffffffu, fin0, 0);
+    fin1 = __shfl_sync(0xffffffffu, fin1, 0);
+    for (int f = 0; f < 2; ++f) {
+        const int slot = f ? fin1 : fin0;
+        if (slot < 0) continue;
+        const double bs = warp_fold(p.tile_sums + static_cast<int64_t>(slot) * tiles, tiles, lane);
+        int last = 0;
+        if (lane == 0) {
+            p.block_sums[slot] = bs;
+            p.block_done[slot] = 0;  // re-arm for the next run
+            __threadfence();
+            last = atomicAdd(p.all_done, 1u) + 1u == static_cast<unsigned>(p.nslots);
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {  // this CTA completed the last block
+            __threadfence();
+            const double tot = warp_fold(p.block_sums, p.nslots, lane);
+            if (lane == 0) {
+                if (p.total) *p.total = tot;
+                *p.all_done = 0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// v2: persistent, warp-specialised, TMA-fed.  One CTA per SM; a producer warp
+// claims items from a global cursor and streams both x tiles of each item into
+// a 3-stage shared-memory ring with cp.async.bulk row copies (mbarrier
+// complete_tx); 8 consumer warps transpose-add-store and reduce.  Two tile
+// pairs stay in flight while the third is consumed.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kTmaThreads, 1) ts_kernel_tma(TsParams p) {
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) uint64_t full_bar[kStages];
+    __shared__ __align__(8) uint64_t empty_bar[kStages];
+    __shared__ int4 stage_info[kStages];
+    __shared__ double part[kStages][2][kWarps];
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            m4d::ptx::mbar_init(&full_bar[s], 1);
+            m4d::ptx::mbar_init(&empty_bar[s], kWarps);
+        }
+        m4d::ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    const int64_t b = p.b;
+    if (warp == kWarps) {
+        // ---------------- producer warp ----------------
+        for (int k = 0;; ++k) {
+            const int s = k % kStages;
+            const uint32_t ph = (k / kStages) & 1;
+            m4d::ptx::mbar_wait(&empty_bar[s], ph ^ 1);
+            unsigned long long item = 0;
+            if (lane == 0) item = atomicAdd(p.work, 1ull);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= static_cast<unsigned long long>(p.items)) {
+                if (lane == 0) {
+                    stage_info[s] = make_int4(-1, 0, 0, 0);
+                    m4d::ptx::mbar_arrive(&full_bar[s]);
+                }
+                break;
+            }
+            const Item it = decode_item(p, static_cast<int64_t>(item));
+            const m4d_ts_task& task = p.tasks[it.task];
+            const int64_t R0 = static_cast<int64_t>(it.tr) * kTile;
+            const int64_t C0 = static_cast<int64_t>(it.tc) * kTile;
+            const int64_t rows_a = (b - R0 < kTile ? b - R0 : (int64_t)kTile), cols_a = (b - C0 < kTile ? b - C0 : (int64_t)kTile);
+            const int64_t rows_b = cols_a, cols_b = rows_a;  // B tile = x(j,i) rows C0.., cols R0..
+            const uint32_t bytes = static_cast<uint32_t>((rows_a * cols_a + rows_b * cols_b) * sizeof(double));
+            double* sA = smem + static_cast<size_t>(s) * 2 * kTile * kPitchTma;
+            double* sB = sA + kTile * kPitchTma;
+            if (lane == 0) {
+                stage_info[s] = make_int4(it.task, it.tr, it.tc, 1);
+                m4d::ptx::mbar_arrive_expect_tx(&full_bar[s], bytes);
+            }
+            __syncwarp();
+            for (int r = lane; r < rows_a; r += 32)
+                m4d::ptx::bulk_g2s(sA + r * kPitchTma, task.a + (R0 + r) * b + C0,
+                                   static_cast<uint32_t>(cols_a * sizeof(double)), &full_bar[s]);
+            for (int r = lane; r < rows_b; r += 32)
+                m4d::ptx::bulk_g2s(sB + r * kPitchTma, task.bt + (C0 + r) * b + R0,
+                                   static_cast<uint32_t>(cols_b * sizeof(double)), &full_bar[s]);
+        }
+    } else {
+        // ---------------- consumer warps ----------------
+        for (int k = 0;; ++k) {
+            const int s = k % kStages;
+            const uint32_t ph = (k / kStages) & 1;
+            m4d::ptx::mbar_wait(&full_bar[s], ph);
+            const int4 info = stage_info[s];
+            if (info.w < 0) break;
+            const m4d_ts_task task = p.tasks[info.x];
+            const int tr = info.y, tc = info.z;
+            const bool second = task.diag ? (tr != tc) : (task.y2 != nullptr);
+            double* const y2 = task.diag ? task.y : task.y2;
+            const int slot2 = task.diag ? task.slot_y : task.slot_y2;
+            const double* sA = smem + static_cast<size_t>(s) * 2 * kTile * kPitchTma;
+            const double* sB = sA + kTile * kPitchTma;
+            double s1 = 0.0, s2 = 0.0;
+            transpose_add_tile<kPitchTma>(sA, sB, task.y, y2, second, b, static_cast<int64_t>(tr) * kTile,
+                                          static_cast<int64_t>(tc) * kTile, warp, lane, s1, s2);
+            __syncwarp();
+            if (lane == 0) m4d::ptx::mbar_arrive(&empty_bar[s]);  // this warp is done with the stage
+            s1 = warp_sum(s1);
+            s2 = warp_sum(s2);
+            if (lane == 0) {
+                part[s][0][warp] = s1;
+                part[s][1][warp] = s2;
+            }
+            m4d::ptx::named_barrier(1, kThreads);
+            if (warp == 0) {
+                double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+                for (int w = 0; w < kWarps; ++w) { t1 += part[s][0][w]; t2 += part[s][1][w]; }
+                finish_item(p, task, tr, tc, second, slot2, t1, t2, lane);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(p.exits, 1u) + 1u == gridDim.x) {  // last CTA out re-arms the cursor
+            *p.work = 0;
+            *p.exits = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// v1: one CTA per tile item, LDG-staged (fallback for odd block edges or
+// pointers that are not 16-byte aligned, which TMA rows cannot express).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads, 3) ts_kernel_ldg(TsParams p) {
+    extern __shared__ double smem[];
+    double* sA = smem;
+    double* sB = smem + kTile * kPitchLdg;
+    __shared__ double part[2][kWarps];
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const Item it = decode_item(p, blockIdx.x);
+    const m4d_ts_task task = p.tasks[it.task];
+    const int tr = it.tr, tc = it.tc;
+    const bool second = task.diag ? (tr != tc) : (task.y2 != nullptr);
+    double* const y2 = task.diag ? task.y : task.y2;
+    const int slot2 = task.diag ? task.slot_y : task.slot_y2;
+    const int64_t b = p.b;
+    const int64_t R0 = static_cast<int64_t>(tr) * kTile;
+    const int64_t C0 = static_cast<int64_t>(tc) * kTile;
+
+#pragma unroll
+    for (int k = 0; k < kRowsPerWarp; ++k) {
+        const int r = warp * kRowsPerWarp + k;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int c = lane + 32 * h;
+            double av = 0.0, bv = 0.0;
+            if (R0 + r < b && C0 + c < b) av = __ldcs(task.a + (R0 + r) * b + (C0 + c));
+            if (C0 + r < b && R0 + c < b) bv = __ldcs(task.bt + (C0 + r) * b + (R0 + c));
+            sA[r * kPitchLdg + c] = av;
+            sB[r * kPitchLdg + c] = bv;
+        }
+    }
+    __syncthreads();
+    double s1 = 0.0, s2 = 0.0;
+    transpose_add_tile<kPitchLdg>(sA, sB, task.y, y2, second, b, R0, C0, warp, lane, s1, s2);
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     if (lane == 0) {
@@ -153,50 +332,11 @@ __global__ void __launch_bounds__(kThreads, 3) ts_kernel(TsParams p) {
         part[1][warp] = s2;
     }
     __syncthreads();
-
-    const int tiles = T * T;
-    if (threadIdx.x == 0) {
+    if (warp == 0) {
         double t1 = 0.0, t2 = 0.0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) { t1 += part[0][w]; t2 += part[1][w]; }
-        p.tile_sums[static_cast<int64_t>(task.slot_y) * tiles + tr * T + tc] = t1;
-        if (second) p.tile_sums[static_cast<int64_t>(slot2) * tiles + tc * T + tr] = t2;
-        __threadfence();
-        finished[0] = finished[1] = -1;
-        if (second && slot2 == task.slot_y) {
-            if (atomicAdd(p.block_done + task.slot_y, 2u) + 2u == static_cast<unsigned>(tiles))
-                finished[0] = task.slot_y;
-        } else {
-            if (atomicAdd(p.block_done + task.slot_y, 1u) + 1u == static_cast<unsigned>(tiles))
-                finished[0] = task.slot_y;
-            if (second && atomicAdd(p.block_done + slot2, 1u) + 1u == static_cast<unsigned>(tiles))
-                finished[1] = slot2;
-        }
-        __threadfence();
-    }
-    __syncthreads();
-
-    if (warp == 0) {
-        for (int f = 0; f < 2; ++f) {
-            const int slot = finished[f];
-            if (slot < 0) continue;
-            const double bs = warp_fold(p.tile_sums + static_cast<int64_t>(slot) * tiles, tiles, lane);
-            if (lane == 0) {
-                p.block_sums[slot] = bs;
-                p.block_done[slot] = 0;  // re-arm for the next run
-                __threadfence();
-                finished[f] = (atomicAdd(p.all_done, 1u) + 1u == static_cast<unsigned>(p.nslots)) ? -2 : -1;
-            }
-            __syncwarp();
-            if (finished[f] == -2) {  // this CTA completed the last block
-                __threadfence();
-                const double tot = warp_fold(p.block_sums, p.nslots, lane);
-                if (lane == 0) {
-                    if (p.total) *p.total = tot;
-                    *p.all_done = 0;
-                }
-            }
-        }
+        finish_item(p, task, tr, tc, second, slot2, t1, t2, lane);
     }
 }
 
@@ -224,7 +364,10 @@ struct m4d_ts_plan {
     m4d_ts_task* d_tasks = nullptr;
     int64_t* d_off = nullptr;
     double* d_tile_sums = nullptr;
-    unsigned* d_counters = nullptr;  // nslots block counters + 1 global counter
+    unsigned* d_counters = nullptr;  // nslots block counters, all_done, exits
+    unsigned long long* d_work = nullptr;
+    bool tma = false;                // TMA-fed persistent kernel usable
+    int sms = 148;
 };
 
 using m4d::fail;
@@ -312,14 +455,26 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks, 
         return cleanup(m4d::cuda_fail(e, "plan offsets"));
     if ((e = cudaMalloc(&plan->d_tile_sums, sizeof(double) * std::max<int64_t>(1, tiles * nslots))) !=
             cudaSuccess ||
-        (e = cudaMalloc(&plan->d_counters, sizeof(unsigned) * (nslots + 1))) != cudaSuccess ||
-        (e = cudaMemset(plan->d_counters, 0, sizeof(unsigned) * (nslots + 1))) != cudaSuccess)
+        (e = cudaMalloc(&plan->d_counters, sizeof(unsigned) * (nslots + 2))) != cudaSuccess ||
+        (e = cudaMemset(plan->d_counters, 0, sizeof(unsigned) * (nslots + 2))) != cudaSuccess ||
+        (e = cudaMalloc(&plan->d_work, sizeof(unsigned long long))) != cudaSuccess ||
+        (e = cudaMemset(plan->d_work, 0, sizeof(unsigned long long))) != cudaSuccess)
         return cleanup(m4d::cuda_fail(e, "plan scratch"));
-    if ((e = cudaFuncSetAttribute(ts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes))) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(ts_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) !=
-            cudaSuccess)
-        return cleanup(m4d::cuda_fail(e, "ts_kernel attributes"));
+    if ((e = cudaFuncSetAttribute(ts_kernel_ldg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemLdg))) != cudaSuccess ||
+        (e = cudaFuncSetAttribute(ts_kernel_ldg, cudaFuncAttributePreferredSharedMemoryCarveout, 100)) !=
+            cudaSuccess ||
+        (e = cudaFuncSetAttribute(ts_kernel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemTma))) != cudaSuccess)
+        return cleanup(m4d::cuda_fail(e, "ts kernel attributes"));
+    if ((e = cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
+        return cleanup(m4d::cuda_fail(e, "SM count"));
+    // TMA rows need 16-byte aligned row starts and sizes: even block edge and
+    // 16-byte aligned block bases.  M4D_TS_FORCE_LDG=1 selects the v1 kernel.
+    plan->tma = (block % 2 == 0) && !getenv("M4D_TS_FORCE_LDG");
+    for (int t = 0; t < ntasks && plan->tma; ++t)
+        if ((reinterpret_cast<uintptr_t>(tasks[t].a) | reinterpret_cast<uintptr_t>(tasks[t].bt)) & 15)
+            plan->tma = false;
     *plan_out = plan;
     return M4D_OK;
 }
@@ -339,12 +494,20 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
     p.T = plan->T;
     p.b = plan->b;
     p.nslots = plan->nslots;
+    p.items = plan->items;
     p.tile_sums = plan->d_tile_sums;
     p.block_done = plan->d_counters;
     p.all_done = plan->d_counters + plan->nslots;
+    p.exits = plan->d_counters + plan->nslots + 1;
+    p.work = plan->d_work;
     p.block_sums = block_sums;
     p.total = total;
-    ts_kernel<<<static_cast<unsigned>(plan->items), kThreads, kSmemBytes, s>>>(p);
+    if (plan->tma) {
+        const int64_t grid = std::min<int64_t>(plan->sms, plan->items);
+        ts_kernel_tma<<<static_cast<unsigned>(grid), kTmaThreads, kSmemTma, s>>>(p);
+    } else {
+        ts_kernel_ldg<<<static_cast<unsigned>(plan->items), kThreads, kSmemLdg, s>>>(p);
+    }
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }
@@ -355,6 +518,7 @@ m4d_status m4d_ts_plan_destroy(m4d_ts_plan* plan) {
     cudaFree(plan->d_off);
     cudaFree(plan->d_tile_sums);
     cudaFree(plan->d_counters);
+    cudaFree(plan->d_work);
     delete plan;
     return M4D_OK;
 }

@@ -16,6 +16,16 @@ pytestmark = pytest.mark.gpu
 REL_TOL = 1e-12  # fp64 sum tolerance stated by north_star
 
 
+@pytest.fixture(params=["tma", "ldg"])
+def kernel_path(request, monkeypatch):
+    """Both kernels: the TMA-fed persistent one and the LDG fallback."""
+    if request.param == "ldg":
+        monkeypatch.setenv("M4D_TS_FORCE_LDG", "1")
+    else:
+        monkeypatch.delenv("M4D_TS_FORCE_LDG", raising=False)
+    return request.param
+
+
 def run_world(n, b, world, seed=oracle.SEED_X):
     from paper_2101_08878_b200.harness.transpose_sum import TransposeSum
 
@@ -37,7 +47,7 @@ def y_block(ranks, g):
 
 
 @pytest.mark.parametrize("n,b", [(256, 64), (300, 100), (4096, 1024), (130, 65), (2000, 2000), (96, 1)])
-def test_single_gpu_matches_oracle_bit_exact(cuda, n, b):
+def test_single_gpu_matches_oracle_bit_exact(cuda, kernel_path, n, b):
     ranks, sums, total = run_world(n, b, 1)
     nb = n // b
     want_sums, want_total = oracle.transpose_sum_checksum(n, b, threads=8)
@@ -63,7 +73,7 @@ def test_numpy_restatement_agrees_at_small_size(cuda):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4, 5])
-def test_checksum_independent_of_worker_count(cuda, world):
+def test_checksum_independent_of_worker_count(cuda, kernel_path, world):
     n, b = 1024, 128
     _, sums1, total1 = run_world(n, b, 1)
     ranks, sums_w, total_w = run_world(n, b, world)
