@@ -128,6 +128,8 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks,
  * order; may be NULL). */
 m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void* stream);
 m4d_status m4d_ts_plan_destroy(m4d_ts_plan* plan);
+/* 1 when the plan runs the TMA-fed persistent kernel, 0 for the LDG fallback. */
+int m4d_ts_plan_uses_tma(const m4d_ts_plan* plan);
 /* Number of kernel launches one m4d_ts_run issues (for gpu_launches accounting). */
 int m4d_ts_launches_per_run(void);
 

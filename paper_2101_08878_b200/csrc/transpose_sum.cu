@@ -3,27 +3,40 @@
 // generator of BASELINE.md §3.
 //
 // Work decomposition.  Every output block y(i,j) = x(i,j) + x(j,i)^T is cut
-// into 64x64 fp64 tiles.  One CTA (256 threads) handles one tile item:
+// into 64x64 fp64 tiles; one *item* is one tile position:
 //   * paired item  : y(i,j) tile (tr,tc) AND y(j,i) tile (tc,tr).  Both x tiles
 //                    are staged once in shared memory, so x is read exactly
 //                    once for both outputs (16 B of HBM per output element).
 //   * single item  : y(i,j) tile only; the x(j,i) tile may live on a peer B200
 //                    and is read straight over NVLink through its IPC mapping.
 //   * diagonal     : y(i,i) tiles (tr,tc) and (tc,tr) of the same block.
-// Global access is one 256 B coalesced row segment per warp instruction
-// (8 B per lane, streaming .cs hints); the transposed read comes out of a
-// padded shared tile (pitch 65 doubles -> conflict-free 64-bit column reads).
+//
+// Main kernel (ts_kernel_tma): persistent, one CTA per SM, warp-specialised.
+// A producer warp claims items from a global cursor and streams both x tiles
+// into a 3-stage shared-memory ring with tiled TMA loads (2-D tensor maps over
+// each block pool, 128-byte swizzle, 4 boxes of 64x16 fp64 per tile, mbarrier
+// complete_tx); 8 consumer warps transpose-add, store y with coalesced 256 B
+// row segments and reduce.  Two tile pairs are in flight while a third is
+// consumed.  The swizzle keeps the transposed shared-memory read at <= 2-way
+// bank conflicts without padding.
+//
+// Fallback (ts_kernel_ldg): one CTA per item, LDG-staged, padded shared
+// tiles; used when the block edge is odd or the pointers cannot be described
+// by tensor maps.
 //
 // Reduction.  Each tile's sum is accumulated in a fixed thread/element order
 // that does not depend on whether the tile was computed paired or single, so
-// per-block sums are bit-identical for any worker count.  The last CTA to
-// finish a block folds its tile sums in fixed order (threadfence-reduction
-// pattern), and the last block folds the block sums, so one launch per step.
+// per-block sums are bit-identical for any worker count and either kernel.
+// The CTA that completes a block folds its tile sums in fixed order
+// (threadfence-reduction pattern), and the one completing the last block folds
+// the block sums, so a step is exactly one launch.
+#include <cuda.h>
 #include <cuda_runtime.h>
-
 #include <stdlib.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "m4d_internal.h"
@@ -36,20 +49,27 @@ constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kRowsPerWarp = kTile / kWarps;  // 8
 
-// v1 (LDG) path: padded pitch 65 -> conflict-free 64-bit column reads.
+// LDG path: padded pitch 65 -> conflict-free 64-bit column reads.
 constexpr int kPitchLdg = kTile + 1;
 constexpr size_t kSmemLdg = 2ull * kTile * kPitchLdg * sizeof(double);
 
-// v2 (TMA bulk) path: rows must be 16-byte aligned -> pitch 66 (2-way conflicts
-// on the transposed read, far below the smem bandwidth budget).
-constexpr int kPitchTma = kTile + 2;
+// TMA path: a tile is 4 swizzled boxes of 64 rows x 16 fp64 (128 B rows).
+constexpr int kBoxCols = 16;
+constexpr int kBoxes = kTile / kBoxCols;
+constexpr uint32_t kBoxBytes = kTile * kBoxCols * sizeof(double);  // 8 KB
+constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;                // 32 KB
 constexpr int kStages = 3;
 constexpr int kTmaThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
-constexpr size_t kTileBytesTma = static_cast<size_t>(kTile) * kPitchTma * sizeof(double);
-constexpr size_t kSmemTma = kStages * 2 * kTileBytesTma;
+constexpr size_t kSmemTma = kStages * 2ull * kTileBytes + 1024;  // + alignment slack
+constexpr int kMaxMaps = 16;
+
+struct TsMaps {
+    CUtensorMap m[kMaxMaps];
+};
 
 struct TsParams {
     const m4d_ts_task* tasks;
+    const int4* refs;         // per task: (map of a, slot of a, map of bt, slot of bt)
     const int64_t* item_off;  // ntasks + 1 prefix offsets of tile items
     int ntasks;
     int T;                    // tiles per block edge
@@ -106,12 +126,29 @@ __device__ __forceinline__ Item decode_item(const TsParams& p, int64_t item) {
     return it;
 }
 
-// y(i,j)[R0+r][C0+c] = sA[r][c] + sB[c][r];  y(j,i)[C0+r][R0+c] = sB[r][c] + sA[c][r].
+// Shared-tile addressing.  Padded: row-major with pitch 65.  Swizzled: the
+// TMA 128-byte swizzle of 4 boxes (16-byte chunk index XOR row % 8).
+struct PaddedTile {
+    const double* base;
+    __device__ __forceinline__ double operator()(int r, int c) const { return base[r * kPitchLdg + c]; }
+};
+
+struct SwizzledTile {
+    const unsigned char* base;
+    __device__ __forceinline__ double operator()(int r, int c) const {
+        const int box = c >> 4, cc = c & 15;
+        const uint32_t off = box * kBoxBytes + r * 128 + ((((cc >> 1) ^ (r & 7))) << 4) + ((cc & 1) << 3);
+        return *reinterpret_cast<const double*>(base + off);
+    }
+};
+
+// y(i,j)[R0+r][C0+c] = A(r,c) + B(c,r);  y(j,i)[C0+r][R0+c] = B(r,c) + A(c,r),
+// where A is the x(i,j) tile and B the x(j,i) tile (rows C0.., cols R0..).
 // Thread (warp w, lane l) owns rows w*8..w*8+7, columns l and l+32 of both
 // output tiles and accumulates them in that fixed order (the determinism
 // contract: identical per-tile sums for paired and single computation).
-template <int PITCH>
-__device__ __forceinline__ void transpose_add_tile(const double* sA, const double* sB, double* y, double* y2,
+template <typename Tile>
+__device__ __forceinline__ void transpose_add_tile(const Tile& A, const Tile& B, double* y, double* y2,
                                                    bool second, int64_t b, int64_t R0, int64_t C0, int warp,
                                                    int lane, double& s1, double& s2) {
 #pragma unroll
@@ -121,12 +158,12 @@ __device__ __forceinline__ void transpose_add_tile(const double* sA, const doubl
         for (int h = 0; h < 2; ++h) {
             const int c = lane + 32 * h;
             if (R0 + r < b && C0 + c < b) {
-                const double v = sA[r * PITCH + c] + sB[c * PITCH + r];
+                const double v = A(r, c) + B(c, r);
                 __stcs(y + (R0 + r) * b + (C0 + c), v);
                 s1 += v;
             }
             if (second && C0 + r < b && R0 + c < b) {
-                const double w = sB[r * PITCH + c] + sA[c * PITCH + r];
+                const double w = B(r, c) + A(c, r);
                 __stcs(y2 + (C0 + r) * b + (R0 + c), w);
                 s2 += w;
             }
@@ -179,19 +216,16 @@ __device__ __forceinline__ void finish_item(const TsParams& p, const m4d_ts_task
     }
 }
 
-// ---------------------------------------------------------------------------
-// v2: persistent, warp-specialised, TMA-fed.  One CTA per SM; a producer warp
-// claims items from a global cursor and streams both x tiles of each item into
-// a 3-stage shared-memory ring with cp.async.bulk row copies (mbarrier
-// complete_tx); 8 consumer warps transpose-add-store and reduce.  Two tile
-// pairs stay in flight while the third is consumed.
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kTmaThreads, 1) ts_kernel_tma(TsParams p) {
-    extern __shared__ __align__(128) double smem[];
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    ts_kernel_tma(const TsParams p, const __grid_constant__ TsMaps maps) {
+    extern __shared__ unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full_bar[kStages];
     __shared__ __align__(8) uint64_t empty_bar[kStages];
     __shared__ int4 stage_info[kStages];
     __shared__ double part[kStages][2][kWarps];
+    // 128-byte swizzled boxes need 1024-byte aligned destinations.
+    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                                           ~static_cast<uintptr_t>(1023));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -216,31 +250,32 @@ __global__ void __launch_bounds__(kTmaThreads, 1) ts_kernel_tma(TsParams p) {
             item = __shfl_sync(0xffffffffu, item, 0);
             if (item >= static_cast<unsigned long long>(p.items)) {
                 if (lane == 0) {
-                    stage_info[s] = make_int4(-1, 0, 0, 0);
+                    stage_info[s] = make_int4(0, 0, 0, -1);  // sentinel: no more items
+                    __threadfence_block();  // order the stage_info store before the arrive
                     m4d::ptx::mbar_arrive(&full_bar[s]);
                 }
                 break;
             }
-            const Item it = decode_item(p, static_cast<int64_t>(item));
-            const m4d_ts_task& task = p.tasks[it.task];
-            const int64_t R0 = static_cast<int64_t>(it.tr) * kTile;
-            const int64_t C0 = static_cast<int64_t>(it.tc) * kTile;
-            const int64_t rows_a = (b - R0 < kTile ? b - R0 : (int64_t)kTile), cols_a = (b - C0 < kTile ? b - C0 : (int64_t)kTile);
-            const int64_t rows_b = cols_a, cols_b = rows_a;  // B tile = x(j,i) rows C0.., cols R0..
-            const uint32_t bytes = static_cast<uint32_t>((rows_a * cols_a + rows_b * cols_b) * sizeof(double));
-            double* sA = smem + static_cast<size_t>(s) * 2 * kTile * kPitchTma;
-            double* sB = sA + kTile * kPitchTma;
             if (lane == 0) {
+                const Item it = decode_item(p, static_cast<int64_t>(item));
+                const int4 ref = p.refs[it.task];
+                const int R0 = it.tr * kTile, C0 = it.tc * kTile;
+                unsigned char* sA = smem + static_cast<size_t>(s) * 2 * kTileBytes;
+                unsigned char* sB = sA + kTileBytes;
                 stage_info[s] = make_int4(it.task, it.tr, it.tc, 1);
-                m4d::ptx::mbar_arrive_expect_tx(&full_bar[s], bytes);
+                __threadfence_block();  // publish stage_info before the phase can complete
+                m4d::ptx::mbar_arrive_expect_tx(&full_bar[s], 2 * kTileBytes);
+                const void* ma = &maps.m[ref.x];
+                const void* mb = &maps.m[ref.z];
+                const int rowa = ref.y * static_cast<int>(b) + R0;  // x(i,j): rows R0.., cols C0..
+                const int rowb = ref.w * static_cast<int>(b) + C0;  // x(j,i): rows C0.., cols R0..
+#pragma unroll
+                for (int q = 0; q < kBoxes; ++q) {
+                    m4d::ptx::tma_load_2d(sA + q * kBoxBytes, ma, C0 + q * kBoxCols, rowa, &full_bar[s]);
+                    m4d::ptx::tma_load_2d(sB + q * kBoxBytes, mb, R0 + q * kBoxCols, rowb, &full_bar[s]);
+                }
             }
             __syncwarp();
-            for (int r = lane; r < rows_a; r += 32)
-                m4d::ptx::bulk_g2s(sA + r * kPitchTma, task.a + (R0 + r) * b + C0,
-                                   static_cast<uint32_t>(cols_a * sizeof(double)), &full_bar[s]);
-            for (int r = lane; r < rows_b; r += 32)
-                m4d::ptx::bulk_g2s(sB + r * kPitchTma, task.bt + (C0 + r) * b + R0,
-                                   static_cast<uint32_t>(cols_b * sizeof(double)), &full_bar[s]);
         }
     } else {
         // ---------------- consumer warps ----------------
@@ -255,11 +290,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1) ts_kernel_tma(TsParams p) {
             const bool second = task.diag ? (tr != tc) : (task.y2 != nullptr);
             double* const y2 = task.diag ? task.y : task.y2;
             const int slot2 = task.diag ? task.slot_y : task.slot_y2;
-            const double* sA = smem + static_cast<size_t>(s) * 2 * kTile * kPitchTma;
-            const double* sB = sA + kTile * kPitchTma;
+            const SwizzledTile A{smem + static_cast<size_t>(s) * 2 * kTileBytes};
+            const SwizzledTile B{A.base + kTileBytes};
             double s1 = 0.0, s2 = 0.0;
-            transpose_add_tile<kPitchTma>(sA, sB, task.y, y2, second, b, static_cast<int64_t>(tr) * kTile,
-                                          static_cast<int64_t>(tc) * kTile, warp, lane, s1, s2);
+            transpose_add_tile(A, B, task.y, y2, second, b, static_cast<int64_t>(tr) * kTile,
+                               static_cast<int64_t>(tc) * kTile, warp, lane, s1, s2);
             __syncwarp();
             if (lane == 0) m4d::ptx::mbar_arrive(&empty_bar[s]);  // this warp is done with the stage
             s1 = warp_sum(s1);
@@ -287,14 +322,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1) ts_kernel_tma(TsParams p) {
     }
 }
 
-// ---------------------------------------------------------------------------
-// v1: one CTA per tile item, LDG-staged (fallback for odd block edges or
-// pointers that are not 16-byte aligned, which TMA rows cannot express).
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads, 3) ts_kernel_ldg(TsParams p) {
-    extern __shared__ double smem[];
-    double* sA = smem;
-    double* sB = smem + kTile * kPitchLdg;
+__global__ void __launch_bounds__(kThreads, 3) ts_kernel_ldg(const TsParams p) {
+    extern __shared__ double smem_ldg[];
+    double* sA = smem_ldg;
+    double* sB = smem_ldg + kTile * kPitchLdg;
     __shared__ double part[2][kWarps];
 
     const int warp = threadIdx.x >> 5;
@@ -324,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 3) ts_kernel_ldg(TsParams p) {
     }
     __syncthreads();
     double s1 = 0.0, s2 = 0.0;
-    transpose_add_tile<kPitchLdg>(sA, sB, task.y, y2, second, b, R0, C0, warp, lane, s1, s2);
+    transpose_add_tile(PaddedTile{sA}, PaddedTile{sB}, task.y, y2, second, b, R0, C0, warp, lane, s1, s2);
     s1 = warp_sum(s1);
     s2 = warp_sum(s2);
     if (lane == 0) {
@@ -352,6 +383,77 @@ __global__ void fill_block_kernel(double* dst, int64_t n, int64_t row0, int64_t 
     }
 }
 
+typedef CUresult (*PFN_encodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled encode_tiled_fn() {
+    static PFN_encodeTiled fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_encodeTiled>(ptr);
+    });
+    return fn;
+}
+
+// Groups the x-block pointers of the tasks into pools (a base plus whole
+// blocks) and encodes one 2-D tensor map per pool: rows = slot * b + row,
+// cols = col, 128-byte swizzled 64x16 boxes.  Returns false when the tasks
+// cannot be expressed that way (the LDG kernel is used instead).
+bool build_maps(const m4d_ts_task* tasks, int ntasks, int64_t b, TsMaps* maps, std::vector<int4>* refs) {
+    if (b % 2 || b > 0x7fffffff / 2) return false;
+    PFN_encodeTiled encode = encode_tiled_fn();
+    if (!encode) return false;
+    const uint64_t block_bytes = static_cast<uint64_t>(b) * b * sizeof(double);
+    std::vector<uintptr_t> ptrs;
+    for (int t = 0; t < ntasks; ++t) {
+        ptrs.push_back(reinterpret_cast<uintptr_t>(tasks[t].a));
+        ptrs.push_back(reinterpret_cast<uintptr_t>(tasks[t].bt));
+    }
+    std::sort(ptrs.begin(), ptrs.end());
+    ptrs.erase(std::unique(ptrs.begin(), ptrs.end()), ptrs.end());
+    std::vector<uintptr_t> bases;
+    std::vector<uint64_t> slots;  // max slot + 1 per base
+    std::map<uintptr_t, std::pair<int, int>> where;
+    for (uintptr_t p : ptrs) {
+        if (p & 15) return false;
+        int found = -1;
+        for (size_t k = 0; k < bases.size(); ++k)
+            if ((p - bases[k]) % block_bytes == 0) { found = static_cast<int>(k); break; }
+        if (found < 0) {
+            if (bases.size() == kMaxMaps) return false;
+            bases.push_back(p);
+            slots.push_back(0);
+            found = static_cast<int>(bases.size()) - 1;
+        }
+        const uint64_t slot = (p - bases[found]) / block_bytes;
+        if ((slot + 1) * b > 0x7fffffffull) return false;
+        slots[found] = std::max<uint64_t>(slots[found], slot + 1);
+        where[p] = {found, static_cast<int>(slot)};
+    }
+    for (size_t k = 0; k < bases.size(); ++k) {
+        cuuint64_t dims[2] = {static_cast<cuuint64_t>(b), static_cast<cuuint64_t>(slots[k] * b)};
+        cuuint64_t strides[1] = {static_cast<cuuint64_t>(b) * sizeof(double)};
+        cuuint32_t box[2] = {kBoxCols, kTile};
+        cuuint32_t estr[2] = {1, 1};
+        if (encode(&maps->m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, reinterpret_cast<void*>(bases[k]), dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+    }
+    refs->resize(ntasks);
+    for (int t = 0; t < ntasks; ++t) {
+        auto a = where[reinterpret_cast<uintptr_t>(tasks[t].a)];
+        auto bt = where[reinterpret_cast<uintptr_t>(tasks[t].bt)];
+        (*refs)[t] = make_int4(a.first, a.second, bt.first, bt.second);
+    }
+    return true;
+}
+
 }  // namespace
 
 struct m4d_ts_plan {
@@ -362,12 +464,14 @@ struct m4d_ts_plan {
     int nslots = 0;
     int64_t items = 0;
     m4d_ts_task* d_tasks = nullptr;
+    int4* d_refs = nullptr;
     int64_t* d_off = nullptr;
     double* d_tile_sums = nullptr;
     unsigned* d_counters = nullptr;  // nslots block counters, all_done, exits
     unsigned long long* d_work = nullptr;
     bool tma = false;                // TMA-fed persistent kernel usable
     int sms = 148;
+    TsMaps maps;
 };
 
 using m4d::fail;
@@ -443,11 +547,19 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks, 
     };
     cudaError_t e;
     if ((e = cudaSetDevice(device)) != cudaSuccess) return cleanup(m4d::cuda_fail(e, "cudaSetDevice"));
+    std::vector<int4> refs;
+    // M4D_TS_FORCE_LDG=1 selects the fallback kernel (tests cover both).
+    plan->tma = !getenv("M4D_TS_FORCE_LDG") && ntasks > 0 && build_maps(tasks, ntasks, block, &plan->maps, &refs);
     if (ntasks) {
         if ((e = cudaMalloc(&plan->d_tasks, sizeof(m4d_ts_task) * ntasks)) != cudaSuccess ||
             (e = cudaMemcpy(plan->d_tasks, tasks, sizeof(m4d_ts_task) * ntasks, cudaMemcpyHostToDevice)) !=
                 cudaSuccess)
             return cleanup(m4d::cuda_fail(e, "plan tasks"));
+        if (plan->tma &&
+            ((e = cudaMalloc(&plan->d_refs, sizeof(int4) * ntasks)) != cudaSuccess ||
+             (e = cudaMemcpy(plan->d_refs, refs.data(), sizeof(int4) * ntasks, cudaMemcpyHostToDevice)) !=
+                 cudaSuccess))
+            return cleanup(m4d::cuda_fail(e, "plan tensor refs"));
     }
     if ((e = cudaMalloc(&plan->d_off, sizeof(int64_t) * (ntasks + 1))) != cudaSuccess ||
         (e = cudaMemcpy(plan->d_off, off.data(), sizeof(int64_t) * (ntasks + 1), cudaMemcpyHostToDevice)) !=
@@ -469,12 +581,6 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks, 
         return cleanup(m4d::cuda_fail(e, "ts kernel attributes"));
     if ((e = cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
         return cleanup(m4d::cuda_fail(e, "SM count"));
-    // TMA rows need 16-byte aligned row starts and sizes: even block edge and
-    // 16-byte aligned block bases.  M4D_TS_FORCE_LDG=1 selects the v1 kernel.
-    plan->tma = (block % 2 == 0) && !getenv("M4D_TS_FORCE_LDG");
-    for (int t = 0; t < ntasks && plan->tma; ++t)
-        if ((reinterpret_cast<uintptr_t>(tasks[t].a) | reinterpret_cast<uintptr_t>(tasks[t].bt)) & 15)
-            plan->tma = false;
     *plan_out = plan;
     return M4D_OK;
 }
@@ -489,6 +595,7 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
     if (!block_sums) return fail(M4D_ERR_USAGE, "block_sums must not be NULL");
     TsParams p;
     p.tasks = plan->d_tasks;
+    p.refs = plan->d_refs;
     p.item_off = plan->d_off;
     p.ntasks = plan->ntasks;
     p.T = plan->T;
@@ -504,7 +611,7 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
     p.total = total;
     if (plan->tma) {
         const int64_t grid = std::min<int64_t>(plan->sms, plan->items);
-        ts_kernel_tma<<<static_cast<unsigned>(grid), kTmaThreads, kSmemTma, s>>>(p);
+        ts_kernel_tma<<<static_cast<unsigned>(grid), kTmaThreads, kSmemTma, s>>>(p, plan->maps);
     } else {
         ts_kernel_ldg<<<static_cast<unsigned>(plan->items), kThreads, kSmemLdg, s>>>(p);
     }
@@ -512,9 +619,12 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
     return M4D_OK;
 }
 
+int m4d_ts_plan_uses_tma(const m4d_ts_plan* plan) { return plan && plan->tma ? 1 : 0; }
+
 m4d_status m4d_ts_plan_destroy(m4d_ts_plan* plan) {
     if (!plan) return M4D_OK;
     cudaFree(plan->d_tasks);
+    cudaFree(plan->d_refs);
     cudaFree(plan->d_off);
     cudaFree(plan->d_tile_sums);
     cudaFree(plan->d_counters);

@@ -30,6 +30,12 @@ def run_world(n, b, world, seed=oracle.SEED_X):
     from paper_2101_08878_b200.harness.transpose_sum import TransposeSum
 
     ranks = TransposeSum.local_world(n, b, world, seed=seed)
+    import os
+    from paper_2101_08878_b200 import native
+
+    want_tma = not os.environ.get("M4D_TS_FORCE_LDG") and b % 2 == 0
+    for r in ranks:
+        assert native.lib().m4d_ts_plan_uses_tma(r._plan) == int(want_tma)
     merged = {}
     for r in ranks:
         r.launch()
