@@ -16,8 +16,9 @@
 // into a 3-stage shared-memory ring with tiled TMA loads (2-D tensor maps over
 // each block pool, 128-byte swizzle, 4 boxes of 64x16 fp64 per tile, mbarrier
 // complete_tx); 8 consumer warps transpose-add, store y with coalesced 256 B
-// row segments and reduce.  Two tile pairs are in flight while a third is
-// consumed.  The swizzle keeps the transposed shared-memory read at <= 2-way
+// row segments and reduce per warp; an epilogue warp folds the warp partials
+// and runs the block-completion bookkeeping off the critical path.  Two tile
+// pairs are in flight while a third is consumed.  The swizzle keeps the transposed shared-memory read at <= 2-way
 // bank conflicts without padding.
 //
 // Fallback (ts_kernel_ldg): one CTA per item, LDG-staged, padded shared
@@ -59,7 +60,7 @@ constexpr int kBoxes = kTile / kBoxCols;
 constexpr uint32_t kBoxBytes = kTile * kBoxCols * sizeof(double);  // 8 KB
 constexpr uint32_t kTileBytes = kBoxes * kBoxBytes;                // 32 KB
 constexpr int kStages = 3;
-constexpr int kTmaThreads = kThreads + 32;  // 8 consumer warps + 1 producer warp
+constexpr int kTmaThreads = kThreads + 64;  // 8 consumer warps + producer warp + epilogue warp
 constexpr size_t kSmemTma = kStages * 2ull * kTileBytes + 1024;  // + alignment slack
 constexpr int kMaxMaps = 16;
 
@@ -219,9 +220,12 @@ __device__ __forceinline__ void finish_item(const TsParams& p, const m4d_ts_task
 __global__ void __launch_bounds__(kTmaThreads, 1)
     ts_kernel_tma(const TsParams p, const __grid_constant__ TsMaps maps) {
     extern __shared__ unsigned char smem_raw[];
-    __shared__ __align__(8) uint64_t full_bar[kStages];
-    __shared__ __align__(8) uint64_t empty_bar[kStages];
+    __shared__ __align__(8) uint64_t full_bar[kStages];   // producer -> consumers (TMA bytes landed)
+    __shared__ __align__(8) uint64_t empty_bar[kStages];  // consumers -> producer (tiles read)
+    __shared__ __align__(8) uint64_t sum_full[kStages];   // consumers -> epilogue (partials written)
+    __shared__ __align__(8) uint64_t sum_empty[kStages];  // epilogue -> consumers (partials read)
     __shared__ int4 stage_info[kStages];
+    __shared__ int4 sum_info[kStages];
     __shared__ double part[kStages][2][kWarps];
     // 128-byte swizzled boxes need 1024-byte aligned destinations.
     unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -233,6 +237,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             m4d::ptx::mbar_init(&full_bar[s], 1);
             m4d::ptx::mbar_init(&empty_bar[s], kWarps);
+            m4d::ptx::mbar_init(&sum_full[s], kWarps);
+            m4d::ptx::mbar_init(&sum_empty[s], 1);
         }
         m4d::ptx::fence_mbar_init();
     }
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 
     const int64_t b = p.b;
     if (warp == kWarps) {
-        // ---------------- producer warp ----------------
+        // ---------------- producer warp: claim items, issue TMA ----------------
         for (int k = 0;; ++k) {
             const int s = k % kStages;
             const uint32_t ph = (k / kStages) & 1;
@@ -277,39 +283,55 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             }
             __syncwarp();
         }
+    } else if (warp == kWarps + 1) {
+        // ---------------- epilogue warp: tile sums, block completion ----------------
+        for (int k = 0;; ++k) {
+            const int s = k % kStages;
+            const uint32_t ph = (k / kStages) & 1;
+            m4d::ptx::mbar_wait(&sum_full[s], ph);
+            const int4 info = sum_info[s];
+            double t1 = 0.0, t2 = 0.0;
+#pragma unroll
+            for (int w = 0; w < kWarps; ++w) { t1 += part[s][0][w]; t2 += part[s][1][w]; }
+            __syncwarp();
+            if (lane == 0) m4d::ptx::mbar_arrive(&sum_empty[s]);
+            if (info.w < 0) break;
+            const m4d_ts_task task = p.tasks[info.x];
+            const bool second = task.diag ? (info.y != info.z) : (task.y2 != nullptr);
+            const int slot2 = task.diag ? task.slot_y : task.slot_y2;
+            finish_item(p, task, info.y, info.z, second, slot2, t1, t2, lane);
+        }
     } else {
-        // ---------------- consumer warps ----------------
+        // ---------------- consumer warps: transpose-add-store ----------------
         for (int k = 0;; ++k) {
             const int s = k % kStages;
             const uint32_t ph = (k / kStages) & 1;
             m4d::ptx::mbar_wait(&full_bar[s], ph);
             const int4 info = stage_info[s];
-            if (info.w < 0) break;
-            const m4d_ts_task task = p.tasks[info.x];
-            const int tr = info.y, tc = info.z;
-            const bool second = task.diag ? (tr != tc) : (task.y2 != nullptr);
-            double* const y2 = task.diag ? task.y : task.y2;
-            const int slot2 = task.diag ? task.slot_y : task.slot_y2;
-            const SwizzledTile A{smem + static_cast<size_t>(s) * 2 * kTileBytes};
-            const SwizzledTile B{A.base + kTileBytes};
             double s1 = 0.0, s2 = 0.0;
-            transpose_add_tile(A, B, task.y, y2, second, b, static_cast<int64_t>(tr) * kTile,
-                               static_cast<int64_t>(tc) * kTile, warp, lane, s1, s2);
+            if (info.w >= 0) {
+                const m4d_ts_task task = p.tasks[info.x];
+                const int tr = info.y, tc = info.z;
+                const bool second = task.diag ? (tr != tc) : (task.y2 != nullptr);
+                double* const y2 = task.diag ? task.y : task.y2;
+                const SwizzledTile A{smem + static_cast<size_t>(s) * 2 * kTileBytes};
+                const SwizzledTile B{A.base + kTileBytes};
+                transpose_add_tile(A, B, task.y, y2, second, b, static_cast<int64_t>(tr) * kTile,
+                                   static_cast<int64_t>(tc) * kTile, warp, lane, s1, s2);
+            }
             __syncwarp();
-            if (lane == 0) m4d::ptx::mbar_arrive(&empty_bar[s]);  // this warp is done with the stage
+            if (lane == 0) m4d::ptx::mbar_arrive(&empty_bar[s]);  // tiles of this stage consumed
             s1 = warp_sum(s1);
             s2 = warp_sum(s2);
+            m4d::ptx::mbar_wait(&sum_empty[s], ph ^ 1);  // epilogue has read this slot's partials
             if (lane == 0) {
                 part[s][0][warp] = s1;
                 part[s][1][warp] = s2;
+                if (warp == 0) sum_info[s] = info;
+                __threadfence_block();
+                m4d::ptx::mbar_arrive(&sum_full[s]);
             }
-            m4d::ptx::named_barrier(1, kThreads);
-            if (warp == 0) {
-                double t1 = 0.0, t2 = 0.0;
-#pragma unroll
-                for (int w = 0; w < kWarps; ++w) { t1 += part[s][0][w]; t2 += part[s][1][w]; }
-                finish_item(p, task, tr, tc, second, slot2, t1, t2, lane);
-            }
+            if (info.w < 0) break;
         }
     }
     __syncthreads();
