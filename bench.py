@@ -173,8 +173,9 @@ def emit(line: dict) -> None:
 # -- transpose_sum -------------------------------------------------------------------------------
 
 
-def ts_cpu_sample(n: int, b: int, pairs: int, threads: int) -> dict:
-    """Oracle (C restatement) on `pairs` output blocks with x resident in host memory."""
+def ts_cpu_sample(n: int, b: int, pairs: int, threads: int, min_seconds: float = 10.0) -> dict:
+    """Oracle (C restatement) on `pairs` output blocks with x resident in host memory,
+    repeated until at least `min_seconds` of CPU work has been timed."""
     import numpy as np
 
     import oracle
@@ -188,11 +189,18 @@ def ts_cpu_sample(n: int, b: int, pairs: int, threads: int) -> dict:
         a_blocks.append(oracle.gen_block_c(n, i * b, j * b, b))
         bt_blocks.append(oracle.gen_block_c(n, j * b, i * b, b))
         y_blocks.append(np.empty((b, b)))
+    oracle.transpose_sum_resident_c(a_blocks, bt_blocks, y_blocks, threads)  # first touch of y (untimed)
+    done = 0
     t0 = time.perf_counter()
-    oracle.transpose_sum_resident_c(a_blocks, bt_blocks, y_blocks, threads)
-    dt = time.perf_counter() - t0
-    per_block = dt / len(ids)
-    return {"seconds": dt, "blocks": len(ids), "per_block_s": per_block, "full_ms": per_block * nb * nb * 1e3}
+    while True:
+        oracle.transpose_sum_resident_c(a_blocks, bt_blocks, y_blocks, threads)
+        done += len(ids)
+        dt = time.perf_counter() - t0
+        if dt >= min_seconds:
+            break
+    per_block = dt / done
+    return {"seconds": dt, "blocks": len(ids), "passes": done // len(ids), "per_block_s": per_block,
+            "full_ms": per_block * nb * nb * 1e3}
 
 
 def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
@@ -300,15 +308,16 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
                   "ok": bool(worst <= 1e-12)}
         if not args.skip_cpu:
             threads = len(os.sched_getaffinity(0))
-            cpu_s = ts_cpu_sample(n, b, args.cpu_pairs, threads)
+            cpu_s = ts_cpu_sample(n, b, args.cpu_pairs, threads, min_seconds=min(10.0, args.cpu_seconds))
             cpu = {"value": cpu_s["full_ms"], "unit": "ms", "cores": threads, "kind": "port",
-                   "sample": f"oracle C restatement, {cpu_s['blocks']} of {ts.nb ** 2} output blocks "
-                             f"(x resident in host RAM), {cpu_s['seconds']:.2f} s, extrapolated to the "
-                             f"full {n}^2 array"}
+                   "sample": f"oracle C restatement, {cpu_s['blocks']} of {ts.nb ** 2} output blocks x "
+                             f"{cpu_s['passes']} passes (x resident in host RAM), {cpu_s['seconds']:.1f} s, "
+                             f"extrapolated to the full {n}^2 array"}
+    launches_per_step = native.lib().m4d_ts_launches_per_run(ts._plan)
     ts.close()
     if dist.rank != 0:
         return None
-    launches = args.steps * native.lib().m4d_ts_launches_per_run()
+    launches = args.steps * launches_per_step
     return {
         "metric": f"x+x.T sum wall time ({n}^2 fp64, {b}^2 chunks)",
         "value": step_ms,
@@ -339,10 +348,11 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
 def reference_transpose_sum(args) -> dict:
     threads = len(os.sched_getaffinity(0))
     per_step = []
-    for _ in range(args.warmup):
-        ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads)
+    budget = max(2.0, args.cpu_seconds / max(1, args.steps))
+    for _ in range(min(args.warmup, 1)):
+        ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads, min_seconds=1.0)
     for _ in range(args.steps):
-        per_step.append(ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads))
+        per_step.append(ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads, min_seconds=budget))
     value = statistics.mean(s["full_ms"] for s in per_step)
     nb = args.n // args.block
     sample = (f"oracle C restatement (the reference has no operator code), {per_step[0]['blocks']} of "
@@ -380,6 +390,7 @@ def main(argv=None) -> int:
     ap.add_argument("--n", type=int, default=40000)
     ap.add_argument("--block", type=int, default=2000)
     ap.add_argument("--cpu-pairs", type=int, default=48, help="output blocks in the CPU baseline sample")
+    ap.add_argument("--cpu-seconds", type=float, default=30.0, help="CPU-baseline time budget (whole run)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--traffic", type=float, default=None,

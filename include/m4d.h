@@ -122,7 +122,8 @@ typedef struct m4d_ts_plan m4d_ts_plan;
 
 m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks,
                               int64_t block, int nslots, m4d_ts_plan** plan_out);
-/* Launches the fused transpose-add-reduce kernel (one launch).  Writes
+/* Launches the fused transpose-add-reduce kernel (plus a tiny fold launch on
+ * the TMA path; see m4d_ts_launches_per_run).  Writes
  * block_sums[nslots] (device, fp64, deterministic fixed-order reduction of
  * each output block) and *total (device, sequential sum of block_sums in slot
  * order; may be NULL). */
@@ -130,8 +131,8 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
 m4d_status m4d_ts_plan_destroy(m4d_ts_plan* plan);
 /* 1 when the plan runs the TMA-fed persistent kernel, 0 for the LDG fallback. */
 int m4d_ts_plan_uses_tma(const m4d_ts_plan* plan);
-/* Number of kernel launches one m4d_ts_run issues (for gpu_launches accounting). */
-int m4d_ts_launches_per_run(void);
+/* Number of kernel launches one m4d_ts_run of this plan issues (gpu_launches accounting). */
+int m4d_ts_launches_per_run(const m4d_ts_plan* plan);
 
 #ifdef __cplusplus
 }

@@ -102,7 +102,7 @@ SIGNATURES: dict[str, tuple] = {
     ),
     "m4d_ts_run": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p]),
     "m4d_ts_plan_destroy": (ctypes.c_int, [_c_void_p]),
-    "m4d_ts_launches_per_run": (ctypes.c_int, []),
+    "m4d_ts_launches_per_run": (ctypes.c_int, [_c_void_p]),
     "m4d_ts_plan_uses_tma": (ctypes.c_int, [_c_void_p]),
 }
 

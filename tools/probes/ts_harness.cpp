@@ -32,7 +32,16 @@ int main(int argc, char** argv) {
         }
     m4d_ts_plan* plan;
     if (m4d_ts_plan_create(0, tasks.data(), (int)tasks.size(), b, nb * nb, &plan)) { char e[512]; m4d_last_error(e, 512); printf("plan: %s\n", e); return 1; }
-    for (int rep = 0; rep < 3; ++rep) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int rep = 0; rep < 3; ++rep) m4d_ts_run(plan, sums, sums + nb * nb, st);
+    cudaEventRecord(e0, (cudaStream_t)st);
+    for (int rep = 0; rep < 10; ++rep) m4d_ts_run(plan, sums, sums + nb * nb, st);
+    cudaEventRecord(e1, (cudaStream_t)st);
+    cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    printf("avg %.3f ms per run  (%.1f GB/s algorithmic)\n", ms / 10, 16.0 * n * (double)n / (ms / 10 * 1e-3) / 1e9);
+    for (int rep = 0; rep < 1; ++rep) {
         int rc = m4d_ts_run(plan, sums, sums + nb * nb, st);
         printf("run %d rc %d\n", rep, rc); fflush(stdout);
         int waited = 0;
