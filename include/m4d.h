@@ -91,6 +91,79 @@ m4d_status m4d_ipc_close(void* base);
 m4d_status m4d_enable_peer(int device, int peer_device);
 
 /* ------------------------------------------------------------------------ */
+/* 3. transport                                                             */
+/* ------------------------------------------------------------------------ */
+/* Replaces the reference Transport contract (pkg/src/commshim/transport/
+ * base.py:199-306): exact (channel, peer, tag) FIFO matching, non-blocking
+ * posts, cooperative progress.  One context per rank; all ranks of a world
+ * share `session` and live on one node (shared-memory rings carry control
+ * and host payloads, CUDA-IPC rendezvous carries device payloads over
+ * NVLink).  Python binding: paper_2101_08878_b200/transport/nvlink.py. */
+
+typedef struct m4d_transport m4d_transport;
+
+typedef struct m4d_transport_config {
+    int32_t world;            /* world size (transport_init world_size)            */
+    int32_t rank;             /* this rank (transport_init self_rank)              */
+    int32_t device;           /* CUDA ordinal, or -1 for a host-only context       */
+    int32_t reserved;
+    uint64_t ring_bytes;      /* per ordered pair ring, multiple of 4096, >= 64 KiB */
+    double connect_timeout;   /* seconds to wait for every peer (StartupError)     */
+    const char* session;      /* shared-memory namespace of the world              */
+} m4d_transport_config;
+
+/* A finished request.  status: M4D_OK, or the M4D_ERR_* code of the
+ * failure (TRUNCATION, CANCELLED, TRANSFER, CLOSED, CUDA); status -1 in an
+ * immediate-completion slot means "still pending". */
+typedef struct m4d_completion {
+    uint64_t req_id;
+    int32_t status;
+    int32_t kind;             /* 0 send, 1 recv */
+    uint64_t bytes;           /* bytes moved (TransferRequest.bytes_moved) */
+} m4d_completion;
+
+typedef struct m4d_transport_stats {
+    uint64_t sends_completed, recvs_completed, bytes_sent, bytes_received;
+    uint64_t eager_bytes;       /* host payload bytes written into rings         */
+    uint64_t nvlink_bytes;      /* device payload bytes pulled peer-to-peer      */
+    uint64_t rendezvous_pulls;
+    uint64_t unexpected_messages;
+} m4d_transport_stats;
+
+/* transport_init: publishes this rank and maps the peers that are already up
+ * (the rest are mapped lazily by progress, like the reference socket mesh,
+ * tcp.py:173-254).  ConfigurationError for a rank collision or disagreeing
+ * settings. */
+m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** out);
+/* SocketTransport.wait_ready (tcp.py:163-171): block until every peer is
+ * mapped; StartupError naming the first unreachable rank after `timeout` s. */
+m4d_status m4d_transport_wait_ready(m4d_transport* t, double timeout);
+int m4d_transport_mesh_ready(const m4d_transport* t);
+/* Transport.post_send (base.py:267-269).  `on_device` = 1 when ptr is device
+ * memory (rendezvous over NVLink); host payloads are sent eagerly.  When the
+ * request finishes inside the call, *now receives its completion (status
+ * != -1) and it is not reported again by m4d_transport_progress. */
+m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer, uint32_t tag,
+                                   const void* ptr, uint64_t len, int domain, int on_device,
+                                   uint64_t req_id, m4d_completion* now);
+/* Transport.post_recv (base.py:271-273); same conventions. */
+m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer, uint32_t tag,
+                                   void* ptr, uint64_t cap, int domain, int on_device,
+                                   uint64_t req_id, m4d_completion* now);
+/* Transport.progress (sim.py:144-159, tcp.py:334-344): drains rings, flushes
+ * queued sends, polls device copies; writes up to `max` completions and
+ * returns how many. */
+int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max);
+int m4d_transport_pending_completions(const m4d_transport* t);
+/* Transport.cancel: *cancelled = 1 when the request was still unmatched. */
+m4d_status m4d_transport_cancel(m4d_transport* t, uint64_t req_id, int* cancelled);
+/* Transport.purge_channel (sim.py:171-180): drop unmatched state of a channel id. */
+m4d_status m4d_transport_purge_channel(m4d_transport* t, uint32_t channel);
+int m4d_transport_peer_alive(const m4d_transport* t, int peer);
+m4d_status m4d_transport_stats_get(const m4d_transport* t, m4d_transport_stats* out);
+m4d_status m4d_transport_close(m4d_transport* t);
+
+/* ------------------------------------------------------------------------ */
 /* 4. transpose_sum (K3/K4)                                                 */
 /* ------------------------------------------------------------------------ */
 

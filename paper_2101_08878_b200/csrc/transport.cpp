@@ -1,0 +1,1073 @@
+// libm4d transport: the B200 replacement of the reference Transport
+// (pkg/src/commshim/transport/base.py:199-306; sim.py / tcp.py behaviour).
+//
+// One process per GPU (or several ranks in one process for tests).  Every
+// rank publishes a POSIX shared-memory segment holding one single-producer /
+// single-consumer byte ring per sending peer; the peers map it.  All traffic
+// from rank s to rank r goes through ring (s -> r) in post order, so per-key
+// FIFO across every protocol follows from ring order, and matching happens at
+// the receiver exactly on (channel, source, tag) with no wildcards.
+//
+// Protocols, chosen per post:
+//   * host payload  -> EAGER: the bytes are copied into the ring (fragments
+//     of <= frag_bytes) and the send completes as soon as the last fragment
+//     is in; an unmatched message is buffered at the receiver.
+//   * device payload -> RENDEZVOUS over NVLink: the sender publishes an RTS
+//     carrying the CUDA-IPC handle (+ offset) of the allocation; the matching
+//     receiver maps it once (cached) and pulls the bytes device-to-device
+//     with a copy-engine cudaMemcpyAsync on its own stream, then answers FIN.
+//     Device bytes never touch host memory (device_aware = True).
+// Truncation fails the receive and, for rendezvous, the send too (the
+// reference simulated-fabric semantics, sim.py:115-122).  No host threads:
+// everything advances inside m4d_transport_progress (cooperative progress,
+// PAPER.md:82).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <errno.h>
+#include <fcntl.h>
+#include <signal.h>
+#include <string.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <time.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <deque>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "m4d_internal.h"
+
+using m4d::fail;
+
+namespace {
+
+constexpr uint32_t kSegMagic = 0x4D344453;  // "M4DS"
+constexpr uint32_t kSegVersion = 1;
+constexpr uint64_t kHeaderBytes = 4096;
+constexpr int kStateInit = 0, kStateReady = 1, kStateClosed = 2;
+
+double now_s() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + ts.tv_nsec * 1e-9;
+}
+
+struct alignas(64) RingCtl {
+    std::atomic<uint64_t> tail;  // bytes ever produced (producer writes)
+    char pad0[56];
+    std::atomic<uint64_t> head;  // bytes ever consumed (consumer writes)
+    char pad1[56];
+};
+
+struct SegHeader {
+    uint32_t magic;
+    uint32_t version;
+    int32_t world;
+    int32_t rank;
+    int32_t pid;
+    int32_t device;
+    std::atomic<int32_t> state;
+    int32_t reserved;
+    uint64_t ring_bytes;
+    uint64_t ring_stride;
+};
+
+enum Kind : uint16_t { kPad = 0, kMsg = 1, kCont = 2, kRts = 3, kFin = 4, kBye = 5 };
+
+struct RecHdr {
+    uint32_t bytes;  // whole record, 8-byte multiple
+    uint16_t kind;
+    uint16_t flags;
+};
+
+struct MsgRec {  // first (or only) fragment of an eager message; payload follows
+    RecHdr h;
+    uint32_t channel, tag;
+    uint64_t total;
+    uint32_t frag;
+    uint32_t domain;
+};
+
+struct ContRec {  // continuation fragment; payload follows
+    RecHdr h;
+    uint32_t frag;
+    uint32_t reserved;
+};
+
+struct RtsRec {
+    RecHdr h;
+    uint32_t channel, tag;
+    uint64_t len;
+    uint64_t send_id;
+    uint64_t src_ptr;  // sender-process pointer (used when both ranks share a process)
+    uint64_t offset;   // ptr - allocation base
+    int32_t pid;
+    int32_t device;
+    uint8_t handle[64];
+};
+
+struct FinRec {
+    RecHdr h;
+    int32_t status;
+    uint32_t reserved;
+    uint64_t send_id;
+    uint64_t bytes;
+};
+
+inline uint64_t align8(uint64_t n) { return (n + 7) & ~7ull; }
+
+struct Ring {
+    RingCtl* ctl = nullptr;
+    uint8_t* data = nullptr;
+    uint64_t cap = 0;
+    uint64_t cursor = 0;  // producer: cached tail / consumer: cached head
+
+    uint64_t free_bytes() const { return cap - (cursor - ctl->head.load(std::memory_order_acquire)); }
+
+    // Producer side: room for a record of `bytes` (plus wrap padding)?  Returns
+    // the write pointer or nullptr; commit() publishes it.
+    uint8_t* reserve(uint64_t bytes) {
+        uint64_t pos = cursor % cap;
+        uint64_t head = ctl->head.load(std::memory_order_acquire);
+        uint64_t used = cursor - head;
+        if (pos + bytes > cap) {  // would wrap: pad to the end first
+            uint64_t pad = cap - pos;
+            if (used + pad + bytes > cap) return nullptr;
+            RecHdr* p = reinterpret_cast<RecHdr*>(data + pos);
+            p->bytes = static_cast<uint32_t>(pad);
+            p->kind = kPad;
+            p->flags = 0;
+            cursor += pad;
+            ctl->tail.store(cursor, std::memory_order_release);
+            pos = 0;
+            used += pad;
+        }
+        if (used + bytes > cap) return nullptr;
+        return data + pos;
+    }
+
+    void commit(uint64_t bytes) {
+        cursor += bytes;
+        ctl->tail.store(cursor, std::memory_order_release);
+    }
+};
+
+enum ReqKind { kSend = 0, kRecv = 1 };
+
+struct Req {
+    uint64_t id;
+    int kind;
+    uint32_t channel, tag;
+    int peer;
+    uint8_t* ptr;
+    uint64_t len;
+    int domain;
+    bool device;        // pointer is device memory (send: rendezvous; recv: H2D / D2D target)
+    // send progress
+    uint64_t sent = 0;
+    bool started = false;
+    RtsRec rts;
+    // queue membership
+    bool in_posted = false;
+    bool in_outq = false;
+};
+
+struct Unexpected {
+    bool rts = false;
+    RtsRec rec;               // rendezvous descriptor
+    std::vector<uint8_t> data;  // eager payload so far
+    uint64_t total = 0;
+    bool complete = false;
+};
+
+// Where the fragments of the eager message currently arriving from a peer go.
+struct Inbound {
+    bool active = false;
+    Req* recv = nullptr;                  // matched receive, or
+    std::shared_ptr<Unexpected> buf;      // buffered unexpected message, or neither: discard
+    uint64_t total = 0, got = 0;
+};
+
+struct Copy {
+    Req* recv;
+    int peer;
+    uint64_t send_id;
+    uint64_t bytes;
+    cudaEvent_t ev;
+};
+
+inline uint64_t ckey(uint32_t channel, uint32_t tag) { return (static_cast<uint64_t>(channel) << 32) | tag; }
+
+struct Peer {
+    SegHeader* seg = nullptr;  // peer's segment (we produce into ring me->peer inside it)
+    size_t seg_len = 0;
+    Ring out;                  // ring in the peer's segment, we are the producer
+    Ring in;                   // ring in our segment, the peer produces
+    int pid = 0;
+    bool dead = false;
+    bool said_bye = false;
+    std::deque<Req*> outq;     // sends not yet fully in the ring, post order
+    std::deque<FinRec> fins;   // control records waiting for ring space
+    std::unordered_map<uint64_t, std::deque<Req*>> posted;
+    std::unordered_map<uint64_t, std::deque<std::shared_ptr<Unexpected>>> unexpected;
+    Inbound inbound;
+};
+
+}  // namespace
+
+struct m4d_transport {
+    int world = 1, rank = 0, device = -1;
+    uint64_t ring_bytes = 0, frag_bytes = 0;
+    std::string session;
+    std::string seg_name;
+    SegHeader* me = nullptr;
+    size_t me_len = 0;
+    std::vector<Peer> peers;
+    std::unordered_map<uint64_t, std::unique_ptr<Req>> reqs;  // live requests by id
+    std::unordered_map<uint64_t, Req*> awaiting_fin;           // rendezvous sends by id
+    std::vector<Copy> copies;
+    std::vector<cudaEvent_t> spare_events;
+    std::vector<m4d_completion> done;
+    std::map<std::string, void*> ipc_maps;                      // handle bytes -> mapped base
+    cudaStream_t stream = nullptr;
+    double last_liveness = 0.0;
+    double last_map_attempt = 0.0;
+    int unmapped = 0;
+    m4d_transport_stats stats{};
+};
+
+namespace {
+
+std::string seg_name_for(const std::string& session, int rank) { return "/m4d_" + session + "_" + std::to_string(rank); }
+
+bool pid_alive(int pid) { return pid > 0 && (kill(pid, 0) == 0 || errno != ESRCH); }
+
+uint64_t ring_stride(uint64_t ring_bytes) { return (sizeof(RingCtl) + ring_bytes + 4095) & ~4095ull; }
+
+Ring ring_in(SegHeader* seg, int src) {
+    Ring r;
+    uint8_t* base = reinterpret_cast<uint8_t*>(seg) + kHeaderBytes + seg->ring_stride * static_cast<uint64_t>(src);
+    r.ctl = reinterpret_cast<RingCtl*>(base);
+    r.data = base + sizeof(RingCtl);
+    r.cap = seg->ring_bytes;
+    return r;
+}
+
+void complete(m4d_transport* t, Req* r, int status, uint64_t bytes) {
+    m4d_completion c;
+    c.req_id = r->id;
+    c.status = status;
+    c.kind = r->kind;
+    c.bytes = bytes;
+    t->done.push_back(c);
+    if (status == M4D_OK) {
+        if (r->kind == kSend) {
+            t->stats.sends_completed++;
+            t->stats.bytes_sent += bytes;
+        } else {
+            t->stats.recvs_completed++;
+            t->stats.bytes_received += bytes;
+        }
+    }
+    t->reqs.erase(r->id);  // frees r
+}
+
+int copy_in(m4d_transport* t, Req* r, uint64_t at, const void* src, uint64_t n) {
+    if (!n) return M4D_OK;
+    if (r->device) {
+        cudaError_t e = cudaMemcpy(r->ptr + at, src, n, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return m4d::cuda_fail(e, "eager host->device delivery");
+    } else {
+        memcpy(r->ptr + at, src, n);
+    }
+    return M4D_OK;
+}
+
+void queue_fin(m4d_transport* t, int peer, uint64_t send_id, int status, uint64_t bytes) {
+    FinRec f{};
+    f.h.bytes = sizeof(FinRec);
+    f.h.kind = kFin;
+    f.status = status;
+    f.send_id = send_id;
+    f.bytes = bytes;
+    t->peers[peer].fins.push_back(f);
+}
+
+void* map_peer_allocation(m4d_transport* t, const RtsRec& rts, int* status) {
+    *status = M4D_OK;
+    if (rts.pid == static_cast<int32_t>(getpid())) return reinterpret_cast<void*>(rts.src_ptr);
+    std::string key(reinterpret_cast<const char*>(rts.handle), 64);
+    auto it = t->ipc_maps.find(key);
+    if (it != t->ipc_maps.end()) return static_cast<uint8_t*>(it->second) + rts.offset;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, rts.handle, 64);
+    void* base = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        *status = m4d::cuda_fail(e, "cudaIpcOpenMemHandle (rendezvous source)");
+        return nullptr;
+    }
+    t->ipc_maps[key] = base;
+    return static_cast<uint8_t*>(base) + rts.offset;
+}
+
+// Matched rendezvous: pull the peer's bytes device-to-device (or D2H for a
+// host receive buffer), complete on the event.
+void start_pull(m4d_transport* t, int peer, Req* r, const RtsRec& rts) {
+    if (rts.len > r->len) {
+        queue_fin(t, peer, rts.send_id, M4D_ERR_TRUNCATION, 0);
+        fail(M4D_ERR_TRUNCATION, "incoming %llu bytes exceed posted buffer of %llu",
+             (unsigned long long)rts.len, (unsigned long long)r->len);
+        complete(t, r, M4D_ERR_TRUNCATION, 0);
+        return;
+    }
+    if (rts.len == 0) {
+        queue_fin(t, peer, rts.send_id, M4D_OK, 0);
+        complete(t, r, M4D_OK, 0);
+        return;
+    }
+    int st;
+    void* src = map_peer_allocation(t, rts, &st);
+    cudaError_t e = cudaSuccess;
+    cudaEvent_t ev = nullptr;
+    if (src) {
+        if (!t->spare_events.empty()) {
+            ev = t->spare_events.back();
+            t->spare_events.pop_back();
+        } else {
+            e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(r->ptr, src, rts.len, cudaMemcpyDefault, t->stream);
+        if (e == cudaSuccess) e = cudaEventRecord(ev, t->stream);
+        if (e != cudaSuccess) st = m4d::cuda_fail(e, "rendezvous pull");
+    }
+    if (st != M4D_OK) {
+        if (ev) t->spare_events.push_back(ev);
+        queue_fin(t, peer, rts.send_id, M4D_ERR_TRANSFER, 0);
+        complete(t, r, M4D_ERR_CUDA, 0);
+        return;
+    }
+    t->copies.push_back(Copy{r, peer, rts.send_id, rts.len, ev});
+    t->stats.rendezvous_pulls++;
+    t->stats.nvlink_bytes += rts.len;
+}
+
+// A receive meets a buffered unexpected message.
+void deliver_unexpected(m4d_transport* t, int peer, Req* r, std::shared_ptr<Unexpected> u) {
+    if (u->rts) {
+        start_pull(t, peer, r, u->rec);
+        return;
+    }
+    Inbound& in = t->peers[peer].inbound;
+    const bool arriving = in.active && in.buf == u;
+    if (u->total > r->len) {
+        fail(M4D_ERR_TRUNCATION, "incoming %llu bytes exceed posted buffer of %llu",
+             (unsigned long long)u->total, (unsigned long long)r->len);
+        if (arriving) in.buf.reset();  // remaining fragments are discarded
+        complete(t, r, M4D_ERR_TRUNCATION, 0);
+        return;
+    }
+    int st = copy_in(t, r, 0, u->data.data(), u->data.size());
+    if (st != M4D_OK) {
+        complete(t, r, st, 0);
+        return;
+    }
+    if (arriving) {  // the rest streams straight into the receive buffer
+        in.buf.reset();
+        in.recv = r;
+        return;
+    }
+    complete(t, r, M4D_OK, u->total);
+}
+
+void fail_peer(m4d_transport* t, int peer, int status, const char* why) {
+    Peer& p = t->peers[peer];
+    if (p.dead) return;
+    p.dead = true;
+    fail(status, "rank %d %s", peer, why);
+    std::vector<Req*> victims;
+    for (auto& kv : p.posted)
+        for (Req* r : kv.second) victims.push_back(r);
+    p.posted.clear();
+    if (p.inbound.active && p.inbound.recv) victims.push_back(p.inbound.recv);
+    p.inbound = Inbound{};
+    for (Req* r : p.outq) victims.push_back(r);
+    p.outq.clear();
+    for (auto it = t->awaiting_fin.begin(); it != t->awaiting_fin.end();) {
+        if (it->second->peer == peer) {
+            victims.push_back(it->second);
+            it = t->awaiting_fin.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    for (Req* r : victims) complete(t, r, M4D_ERR_TRANSFER, r->kind == kSend ? r->sent : 0);
+}
+
+// -- producer side ---------------------------------------------------------------------
+
+bool flush_fins(m4d_transport* t, Peer& p) {
+    while (!p.fins.empty()) {
+        uint8_t* w = p.out.reserve(sizeof(FinRec));
+        if (!w) return false;
+        memcpy(w, &p.fins.front(), sizeof(FinRec));
+        p.out.commit(sizeof(FinRec));
+        p.fins.pop_front();
+    }
+    return true;
+}
+
+// Writes as much of the send at the head of the queue as fits; true when the
+// whole send is in the ring.
+bool push_send(m4d_transport* t, Peer& p, Req* r) {
+    if (r->device) {
+        uint8_t* w = p.out.reserve(sizeof(RtsRec));
+        if (!w) return false;
+        memcpy(w, &r->rts, sizeof(RtsRec));
+        p.out.commit(sizeof(RtsRec));
+        return true;
+    }
+    while (!r->started || r->sent < r->len) {
+        const uint64_t remaining = r->len - r->sent;
+        const uint64_t frag = remaining < t->frag_bytes ? remaining : t->frag_bytes;
+        const uint64_t head = r->started ? sizeof(ContRec) : sizeof(MsgRec);
+        const uint64_t bytes = align8(head + frag);
+        uint8_t* w = p.out.reserve(bytes);
+        if (!w) return false;
+        if (!r->started) {
+            MsgRec* m = reinterpret_cast<MsgRec*>(w);
+            m->h.bytes = static_cast<uint32_t>(bytes);
+            m->h.kind = kMsg;
+            m->h.flags = 0;
+            m->channel = r->channel;
+            m->tag = r->tag;
+            m->total = r->len;
+            m->frag = static_cast<uint32_t>(frag);
+            m->domain = static_cast<uint32_t>(r->domain);
+        } else {
+            ContRec* c = reinterpret_cast<ContRec*>(w);
+            c->h.bytes = static_cast<uint32_t>(bytes);
+            c->h.kind = kCont;
+            c->h.flags = 0;
+            c->frag = static_cast<uint32_t>(frag);
+            c->reserved = 0;
+        }
+        if (frag) memcpy(w + head, r->ptr + r->sent, frag);
+        p.out.commit(bytes);
+        r->sent += frag;
+        r->started = true;
+        t->stats.eager_bytes += frag;
+    }
+    return true;
+}
+
+int flush_peer(m4d_transport* t, int peer) {
+    Peer& p = t->peers[peer];
+    if (p.dead || !p.seg) return 0;
+    if (!flush_fins(t, p)) return 0;
+    int progressed = 0;
+    while (!p.outq.empty()) {
+        Req* r = p.outq.front();
+        if (!push_send(t, p, r)) break;
+        p.outq.pop_front();
+        r->in_outq = false;
+        ++progressed;
+        if (r->device) {
+            t->awaiting_fin[r->id] = r;
+        } else {
+            complete(t, r, M4D_OK, r->len);  // eager: complete once the bytes are in the ring
+        }
+    }
+    return progressed;
+}
+
+// -- consumer side -----------------------------------------------------------------------
+
+void on_msg(m4d_transport* t, int peer, const MsgRec* m) {
+    Peer& p = t->peers[peer];
+    const uint8_t* payload = reinterpret_cast<const uint8_t*>(m) + sizeof(MsgRec);
+    const uint64_t key = ckey(m->channel, m->tag);
+    Inbound in;
+    in.active = m->frag < m->total;
+    in.total = m->total;
+    in.got = m->frag;
+    auto q = p.posted.find(key);
+    if (q != p.posted.end() && !q->second.empty()) {
+        Req* r = q->second.front();
+        q->second.pop_front();
+        if (q->second.empty()) p.posted.erase(q);
+        r->in_posted = false;
+        if (m->total > r->len) {
+            fail(M4D_ERR_TRUNCATION, "incoming %llu bytes exceed posted buffer of %llu",
+                 (unsigned long long)m->total, (unsigned long long)r->len);
+            complete(t, r, M4D_ERR_TRUNCATION, 0);
+            // in.recv stays null: remaining fragments are discarded
+        } else {
+            int st = copy_in(t, r, 0, payload, m->frag);
+            if (st != M4D_OK) {
+                complete(t, r, st, 0);
+            } else if (!in.active) {
+                complete(t, r, M4D_OK, m->total);
+            } else {
+                in.recv = r;
+            }
+        }
+    } else {
+        auto u = std::make_shared<Unexpected>();
+        u->total = m->total;
+        u->data.assign(payload, payload + m->frag);
+        u->complete = !in.active;
+        p.unexpected[key].push_back(u);
+        if (in.active) in.buf = u;
+        t->stats.unexpected_messages++;
+    }
+    p.inbound = in;
+}
+
+void on_cont(m4d_transport* t, int peer, const ContRec* c) {
+    Peer& p = t->peers[peer];
+    Inbound& in = p.inbound;
+    if (!in.active) return;  // stray continuation (stream already failed)
+    const uint8_t* payload = reinterpret_cast<const uint8_t*>(c) + sizeof(ContRec);
+    if (in.recv) {
+        int st = copy_in(t, in.recv, in.got, payload, c->frag);
+        if (st != M4D_OK) {
+            complete(t, in.recv, st, in.got);
+            in.recv = nullptr;
+        }
+    } else if (in.buf) {
+        in.buf->data.insert(in.buf->data.end(), payload, payload + c->frag);
+    }
+    in.got += c->frag;
+    if (in.got >= in.total) {
+        if (in.recv) complete(t, in.recv, M4D_OK, in.total);
+        if (in.buf) in.buf->complete = true;
+        in = Inbound{};
+    }
+}
+
+void on_rts(m4d_transport* t, int peer, const RtsRec* rts) {
+    Peer& p = t->peers[peer];
+    const uint64_t key = ckey(rts->channel, rts->tag);
+    auto q = p.posted.find(key);
+    if (q != p.posted.end() && !q->second.empty()) {
+        Req* r = q->second.front();
+        q->second.pop_front();
+        if (q->second.empty()) p.posted.erase(q);
+        r->in_posted = false;
+        start_pull(t, peer, r, *rts);
+        return;
+    }
+    auto u = std::make_shared<Unexpected>();
+    u->rts = true;
+    u->rec = *rts;
+    u->total = rts->len;
+    u->complete = true;
+    p.unexpected[key].push_back(u);
+    t->stats.unexpected_messages++;
+}
+
+void on_fin(m4d_transport* t, const FinRec* f) {
+    auto it = t->awaiting_fin.find(f->send_id);
+    if (it == t->awaiting_fin.end()) return;
+    Req* r = it->second;
+    t->awaiting_fin.erase(it);
+    if (f->status == M4D_ERR_TRUNCATION)
+        fail(M4D_ERR_TRUNCATION, "peer buffer shorter than the %llu-byte message", (unsigned long long)r->len);
+    else if (f->status == M4D_ERR_CANCELLED)
+        fail(M4D_ERR_CANCELLED, "the matching receive side purged the message");
+    else if (f->status != M4D_OK)
+        fail(f->status, "peer failed to pull the message");
+    complete(t, r, f->status, f->bytes);
+}
+
+int drain_peer(m4d_transport* t, int peer) {
+    Peer& p = t->peers[peer];
+    Ring& ring = p.in;
+    const uint64_t tail = ring.ctl->tail.load(std::memory_order_acquire);
+    int n = 0;
+    while (ring.cursor < tail) {
+        const uint64_t pos = ring.cursor % ring.cap;
+        const RecHdr* h = reinterpret_cast<const RecHdr*>(ring.data + pos);
+        switch (h->kind) {
+            case kMsg: on_msg(t, peer, reinterpret_cast<const MsgRec*>(h)); break;
+            case kCont: on_cont(t, peer, reinterpret_cast<const ContRec*>(h)); break;
+            case kRts: on_rts(t, peer, reinterpret_cast<const RtsRec*>(h)); break;
+            case kFin: on_fin(t, reinterpret_cast<const FinRec*>(h)); break;
+            case kBye: p.said_bye = true; break;
+            default: break;  // kPad
+        }
+        ring.cursor += h->bytes;
+        ++n;
+    }
+    if (n) ring.ctl->head.store(ring.cursor, std::memory_order_release);
+    if (p.said_bye && !p.dead) fail_peer(t, peer, M4D_ERR_CLOSED, "closed the connection");
+    return n;
+}
+
+int poll_copies(m4d_transport* t) {
+    int n = 0;
+    for (size_t i = 0; i < t->copies.size();) {
+        Copy& c = t->copies[i];
+        cudaError_t e = cudaEventQuery(c.ev);
+        if (e == cudaErrorNotReady) {
+            ++i;
+            continue;
+        }
+        if (e == cudaSuccess) {
+            queue_fin(t, c.peer, c.send_id, M4D_OK, c.bytes);
+            complete(t, c.recv, M4D_OK, c.bytes);
+        } else {
+            m4d::cuda_fail(e, "rendezvous copy");
+            queue_fin(t, c.peer, c.send_id, M4D_ERR_TRANSFER, 0);
+            complete(t, c.recv, M4D_ERR_CUDA, 0);
+        }
+        t->spare_events.push_back(c.ev);
+        t->copies[i] = t->copies.back();
+        t->copies.pop_back();
+        ++n;
+    }
+    return n;
+}
+
+void check_liveness(m4d_transport* t) {
+    const double now = now_s();
+    if (now - t->last_liveness < 0.002) return;
+    t->last_liveness = now;
+    for (int q = 0; q < t->world; ++q) {
+        if (q == t->rank || t->peers[q].dead || !t->peers[q].seg) continue;
+        Peer& p = t->peers[q];
+        if (p.seg->state.load(std::memory_order_acquire) == kStateClosed) {
+            drain_peer(t, q);  // take what it sent before leaving
+            fail_peer(t, q, M4D_ERR_CLOSED, "closed the connection");
+        } else if (!pid_alive(p.pid)) {
+            fail_peer(t, q, M4D_ERR_TRANSFER, "died");
+        }
+    }
+}
+
+Req* find_req(m4d_transport* t, uint64_t id) {
+    auto it = t->reqs.find(id);
+    return it == t->reqs.end() ? nullptr : it->second.get();
+}
+
+int validate_peer(m4d_transport* t, int peer) {
+    if (peer == t->rank) return fail(M4D_ERR_USAGE, "cannot address self");
+    if (peer < 0 || peer >= t->world) return fail(M4D_ERR_USAGE, "peer %d outside world of size %d", peer, t->world);
+    return M4D_OK;
+}
+
+// Maps peer q's segment if it exists and is ready (non-blocking).  Returns
+// M4D_OK whether or not it is there yet; ConfigurationError on a mismatch.
+int try_map_peer(m4d_transport* t, int q) {
+    Peer& p = t->peers[q];
+    if (p.seg) return M4D_OK;
+    const std::string name = seg_name_for(t->session, q);
+    int pfd = shm_open(name.c_str(), O_RDWR, 0600);
+    if (pfd < 0) return M4D_OK;
+    struct stat sb;
+    if (fstat(pfd, &sb) != 0 || static_cast<size_t>(sb.st_size) < kHeaderBytes) {
+        close(pfd);
+        return M4D_OK;
+    }
+    void* pm = mmap(nullptr, sb.st_size, PROT_READ | PROT_WRITE, MAP_SHARED, pfd, 0);
+    close(pfd);
+    if (pm == MAP_FAILED) return M4D_OK;
+    SegHeader* ph = static_cast<SegHeader*>(pm);
+    if (ph->magic != kSegMagic || ph->state.load(std::memory_order_acquire) != kStateReady) {
+        munmap(pm, sb.st_size);
+        return M4D_OK;
+    }
+    if (ph->version != kSegVersion || ph->world != t->world || ph->rank != q || ph->ring_bytes != t->ring_bytes) {
+        const int w = ph->world;
+        const unsigned long long rb = ph->ring_bytes;
+        munmap(pm, sb.st_size);
+        return fail(M4D_ERR_CONFIGURATION, "rank %d's segment disagrees (world %d vs %d, ring %llu vs %llu)", q, w,
+                    t->world, rb, (unsigned long long)t->ring_bytes);
+    }
+    p.seg = ph;
+    p.seg_len = sb.st_size;
+    p.pid = ph->pid;
+    p.out = ring_in(p.seg, t->rank);  // we produce into (me -> q) inside q's segment
+    return M4D_OK;
+}
+
+void map_missing_peers(m4d_transport* t) {
+    const double now = now_s();
+    if (now - t->last_map_attempt < 0.0005) return;
+    t->last_map_attempt = now;
+    for (int q = 0; q < t->world; ++q)
+        if (q != t->rank && !t->peers[q].seg) try_map_peer(t, q);
+}
+
+}  // namespace
+
+extern "C" {
+
+m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** out) {
+    *out = nullptr;
+    if (!cfg || cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+        return fail(M4D_ERR_USAGE, "invalid world/rank");
+    if (!cfg->session || !cfg->session[0] || strchr(cfg->session, '/'))
+        return fail(M4D_ERR_CONFIGURATION, "transport session name must be non-empty and contain no '/'");
+    if (cfg->ring_bytes < 65536 || cfg->ring_bytes % 4096)
+        return fail(M4D_ERR_CONFIGURATION, "ring_bytes must be a multiple of 4096 and >= 64 KiB");
+    std::unique_ptr<m4d_transport> t(new m4d_transport());
+    t->world = cfg->world;
+    t->rank = cfg->rank;
+    t->device = cfg->device;
+    t->ring_bytes = cfg->ring_bytes;
+    t->frag_bytes = cfg->ring_bytes / 4 < (256u << 10) ? cfg->ring_bytes / 4 : (256u << 10);
+    t->session = cfg->session;
+    t->seg_name = seg_name_for(t->session, t->rank);
+    t->peers.resize(t->world);
+
+    // Own segment: header + one inbound ring per source rank.
+    const uint64_t stride = ring_stride(t->ring_bytes);
+    const size_t seg_len = kHeaderBytes + stride * t->world;
+    int fd = -1;
+    for (int attempt = 0; attempt < 2 && fd < 0; ++attempt) {
+        fd = shm_open(t->seg_name.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+        if (fd >= 0 || errno != EEXIST) break;
+        // Stale segment of a dead process, or a live rank collision?
+        int ofd = shm_open(t->seg_name.c_str(), O_RDWR, 0600);
+        if (ofd >= 0) {
+            struct stat sb;
+            bool live = false;
+            if (fstat(ofd, &sb) == 0 && static_cast<size_t>(sb.st_size) >= sizeof(SegHeader)) {
+                void* m = mmap(nullptr, sizeof(SegHeader), PROT_READ, MAP_SHARED, ofd, 0);
+                if (m != MAP_FAILED) {
+                    const SegHeader* h = static_cast<const SegHeader*>(m);
+                    live = h->magic == kSegMagic && h->state.load() != kStateClosed && pid_alive(h->pid);
+                    munmap(m, sizeof(SegHeader));
+                }
+            }
+            close(ofd);
+            if (live) return fail(M4D_ERR_CONFIGURATION, "rank %d already initialized in session %s (rank collision)",
+                                  t->rank, t->session.c_str());
+        }
+        shm_unlink(t->seg_name.c_str());
+    }
+    if (fd < 0) return fail(M4D_ERR_STARTUP, "shm_open(%s): %s", t->seg_name.c_str(), strerror(errno));
+    if (ftruncate(fd, static_cast<off_t>(seg_len)) != 0) {
+        close(fd);
+        shm_unlink(t->seg_name.c_str());
+        return fail(M4D_ERR_STARTUP, "ftruncate(%s): %s", t->seg_name.c_str(), strerror(errno));
+    }
+    void* mem = mmap(nullptr, seg_len, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (mem == MAP_FAILED) {
+        shm_unlink(t->seg_name.c_str());
+        return fail(M4D_ERR_STARTUP, "mmap(%s): %s", t->seg_name.c_str(), strerror(errno));
+    }
+    t->me = static_cast<SegHeader*>(mem);
+    t->me_len = seg_len;
+    SegHeader* h = t->me;
+    h->magic = kSegMagic;
+    h->version = kSegVersion;
+    h->world = t->world;
+    h->rank = t->rank;
+    h->pid = static_cast<int32_t>(getpid());
+    h->device = t->device;
+    h->ring_bytes = t->ring_bytes;
+    h->ring_stride = stride;
+    for (int s = 0; s < t->world; ++s) {
+        Ring r = ring_in(h, s);
+        new (r.ctl) RingCtl();
+        r.ctl->tail.store(0);
+        r.ctl->head.store(0);
+    }
+    h->state.store(kStateReady, std::memory_order_release);
+
+    for (int q = 0; q < t->world; ++q)
+        if (q != t->rank) t->peers[q].in = ring_in(t->me, q);  // inbound rings live in our segment
+    (void)cfg->connect_timeout;  // peers are mapped lazily (m4d_transport_wait_ready blocks)
+    for (int q = 0; q < t->world; ++q)
+        if (q != t->rank) {
+            int st = try_map_peer(t.get(), q);
+            if (st) {
+                m4d_transport* raw = t.release();
+                m4d_transport_close(raw);
+                return st;
+            }
+        }
+
+    if (t->device >= 0) {
+        cudaError_t e = cudaSetDevice(t->device);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            m4d_transport* raw = t.release();
+            m4d_transport_close(raw);
+            return m4d::cuda_fail(e, "transport stream");
+        }
+        int n = 0;
+        if (cudaGetDeviceCount(&n) == cudaSuccess)
+            for (int d = 0; d < n; ++d)
+                if (d != t->device) {
+                    int ok = 0;
+                    if (cudaDeviceCanAccessPeer(&ok, t->device, d) == cudaSuccess && ok)
+                        cudaDeviceEnablePeerAccess(d, 0);
+                }
+        cudaGetLastError();
+    }
+    *out = t.release();
+    return M4D_OK;
+}
+
+m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer, uint32_t tag, const void* ptr,
+                                   uint64_t len, int domain, int on_device, uint64_t req_id, m4d_completion* now) {
+    now->status = -1;
+    int st = validate_peer(t, peer);
+    if (st) return st;
+    Peer& p = t->peers[peer];
+    auto r = std::make_unique<Req>();
+    Req* raw = r.get();
+    raw->id = req_id;
+    raw->kind = kSend;
+    raw->channel = channel;
+    raw->tag = tag;
+    raw->peer = peer;
+    raw->ptr = static_cast<uint8_t*>(const_cast<void*>(ptr));
+    raw->len = len;
+    raw->domain = domain;
+    raw->device = on_device && len > 0;
+    if (raw->device && t->device < 0) return fail(M4D_ERR_USAGE, "device payload on a host-only transport");
+    if (p.dead) {
+        fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
+        now->req_id = req_id;
+        now->status = M4D_ERR_CLOSED;
+        now->kind = kSend;
+        now->bytes = 0;
+        return M4D_OK;
+    }
+    if (raw->device) {
+        RtsRec& rts = raw->rts;
+        memset(&rts, 0, sizeof rts);
+        rts.h.bytes = sizeof(RtsRec);
+        rts.h.kind = kRts;
+        rts.channel = channel;
+        rts.tag = tag;
+        rts.len = len;
+        rts.send_id = req_id;
+        rts.src_ptr = reinterpret_cast<uint64_t>(ptr);
+        rts.pid = static_cast<int32_t>(getpid());
+        rts.device = t->device;
+        st = m4d_ipc_export(ptr, rts.handle, &rts.offset);
+        if (st) return st;
+    }
+    t->reqs[req_id] = std::move(r);
+    raw->in_outq = true;
+    p.outq.push_back(raw);
+    const size_t before = t->done.size();
+    flush_peer(t, peer);
+    // Report an immediate completion (eager send fully in the ring) inline.
+    for (size_t i = before; i < t->done.size(); ++i)
+        if (t->done[i].req_id == req_id) {
+            *now = t->done[i];
+            t->done.erase(t->done.begin() + static_cast<long>(i));
+            break;
+        }
+    return M4D_OK;
+}
+
+m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer, uint32_t tag, void* ptr,
+                                   uint64_t cap, int domain, int on_device, uint64_t req_id, m4d_completion* now) {
+    now->status = -1;
+    int st = validate_peer(t, peer);
+    if (st) return st;
+    Peer& p = t->peers[peer];
+    drain_peer(t, peer);  // match against everything that already arrived
+    auto r = std::make_unique<Req>();
+    Req* raw = r.get();
+    raw->id = req_id;
+    raw->kind = kRecv;
+    raw->channel = channel;
+    raw->tag = tag;
+    raw->peer = peer;
+    raw->ptr = static_cast<uint8_t*>(ptr);
+    raw->len = cap;
+    raw->domain = domain;
+    raw->device = on_device && cap > 0;
+    if (raw->device && t->device < 0) return fail(M4D_ERR_USAGE, "device buffer on a host-only transport");
+    t->reqs[req_id] = std::move(r);
+    const size_t before = t->done.size();
+    const uint64_t key = ckey(channel, tag);
+    auto u = p.unexpected.find(key);
+    if (u != p.unexpected.end() && !u->second.empty()) {
+        std::shared_ptr<Unexpected> msg = u->second.front();
+        u->second.pop_front();
+        if (u->second.empty()) p.unexpected.erase(u);
+        deliver_unexpected(t, peer, raw, msg);
+    } else if (p.dead) {
+        fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
+        complete(t, raw, M4D_ERR_CLOSED, 0);
+    } else {
+        raw->in_posted = true;
+        p.posted[key].push_back(raw);
+    }
+    for (size_t i = before; i < t->done.size(); ++i)
+        if (t->done[i].req_id == req_id) {
+            *now = t->done[i];
+            t->done.erase(t->done.begin() + static_cast<long>(i));
+            break;
+        }
+    return M4D_OK;
+}
+
+int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
+    map_missing_peers(t);
+    for (int q = 0; q < t->world; ++q)
+        if (q != t->rank) {
+            drain_peer(t, q);
+            flush_peer(t, q);
+        }
+    if (!t->copies.empty()) poll_copies(t);
+    if (!t->reqs.empty()) check_liveness(t);
+    int n = 0;
+    const int avail = static_cast<int>(t->done.size());
+    n = avail < max ? avail : max;
+    if (n > 0) {
+        memcpy(out, t->done.data(), sizeof(m4d_completion) * n);
+        t->done.erase(t->done.begin(), t->done.begin() + n);
+    }
+    return n;
+}
+
+int m4d_transport_pending_completions(const m4d_transport* t) { return static_cast<int>(t->done.size()); }
+
+m4d_status m4d_transport_cancel(m4d_transport* t, uint64_t req_id, int* cancelled) {
+    *cancelled = 0;
+    Req* r = find_req(t, req_id);
+    if (!r) return M4D_OK;  // already finished
+    Peer& p = t->peers[r->peer];
+    if (r->kind == kRecv && r->in_posted) {
+        auto q = p.posted.find(ckey(r->channel, r->tag));
+        if (q != p.posted.end()) {
+            for (auto it = q->second.begin(); it != q->second.end(); ++it)
+                if (*it == r) {
+                    q->second.erase(it);
+                    break;
+                }
+            if (q->second.empty()) p.posted.erase(q);
+        }
+    } else if (r->kind == kSend && r->in_outq && !r->started) {
+        for (auto it = p.outq.begin(); it != p.outq.end(); ++it)
+            if (*it == r) {
+                p.outq.erase(it);
+                break;
+            }
+    } else {
+        return M4D_OK;  // matched or partly on the wire: no longer retractable
+    }
+    *cancelled = 1;
+    const uint64_t id = r->id;
+    t->reqs.erase(id);  // the caller records the cancellation itself
+    return M4D_OK;
+}
+
+m4d_status m4d_transport_purge_channel(m4d_transport* t, uint32_t channel) {
+    for (int q = 0; q < t->world; ++q) {
+        if (q == t->rank) continue;
+        Peer& p = t->peers[q];
+        drain_peer(t, q);
+        for (auto it = p.unexpected.begin(); it != p.unexpected.end();) {
+            if ((it->first >> 32) == channel) {
+                for (auto& u : it->second)
+                    if (u->rts) queue_fin(t, q, u->rec.send_id, M4D_ERR_CANCELLED, 0);
+                if (p.inbound.active && p.inbound.buf) {
+                    for (auto& u : it->second)
+                        if (u == p.inbound.buf) p.inbound.buf.reset();
+                }
+                it = p.unexpected.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        for (auto it = p.posted.begin(); it != p.posted.end();) {
+            if ((it->first >> 32) == channel) {
+                for (Req* r : it->second) {
+                    fail(M4D_ERR_CANCELLED, "transfer cancelled");
+                    complete(t, r, M4D_ERR_CANCELLED, 0);
+                }
+                it = p.posted.erase(it);
+            } else {
+                ++it;
+            }
+        }
+        flush_fins(t, p);
+    }
+    return M4D_OK;
+}
+
+m4d_status m4d_transport_wait_ready(m4d_transport* t, double timeout) {
+    const double deadline = now_s() + timeout;
+    for (;;) {
+        int missing = -1;
+        for (int q = 0; q < t->world && missing < 0; ++q) {
+            if (q == t->rank || t->peers[q].seg) continue;
+            int st = try_map_peer(t, q);
+            if (st) return st;
+            if (!t->peers[q].seg) missing = q;
+        }
+        if (missing < 0) return M4D_OK;
+        if (now_s() > deadline) return fail(M4D_ERR_STARTUP, "rank %d unreachable during startup", missing);
+        usleep(500);
+    }
+}
+
+int m4d_transport_mesh_ready(const m4d_transport* t) {
+    for (int q = 0; q < t->world; ++q)
+        if (q != t->rank && !t->peers[q].seg) return 0;
+    return 1;
+}
+
+int m4d_transport_peer_alive(const m4d_transport* t, int peer) {
+    if (peer < 0 || peer >= t->world || peer == t->rank) return 0;
+    return t->peers[peer].dead ? 0 : 1;
+}
+
+m4d_status m4d_transport_stats_get(const m4d_transport* t, m4d_transport_stats* out) {
+    *out = t->stats;
+    return M4D_OK;
+}
+
+m4d_status m4d_transport_close(m4d_transport* t) {
+    if (!t) return M4D_OK;
+    // Say goodbye through every ring that has room, then mark the segment closed.
+    for (int q = 0; q < t->world; ++q) {
+        if (q == t->rank || !t->peers[q].seg) continue;
+        Peer& p = t->peers[q];
+        flush_peer(t, q);
+        uint8_t* w = p.out.reserve(sizeof(RecHdr) + 8);
+        if (w) {
+            RecHdr* h = reinterpret_cast<RecHdr*>(w);
+            h->bytes = 16;
+            h->kind = kBye;
+            h->flags = 0;
+            p.out.commit(16);
+        }
+    }
+    if (t->me) t->me->state.store(kStateClosed, std::memory_order_release);
+    if (t->stream) {
+        cudaStreamSynchronize(t->stream);
+        for (Copy& c : t->copies) t->spare_events.push_back(c.ev);
+        for (cudaEvent_t e : t->spare_events) cudaEventDestroy(e);
+        cudaStreamDestroy(t->stream);
+    }
+    for (auto& kv : t->ipc_maps) cudaIpcCloseMemHandle(kv.second);
+    for (Peer& p : t->peers)
+        if (p.seg) munmap(p.seg, p.seg_len);
+    if (t->me) {
+        munmap(t->me, t->me_len);
+        shm_unlink(t->seg_name.c_str());
+    }
+    delete t;
+    return M4D_OK;
+}
+
+}  // extern "C"

@@ -70,6 +70,39 @@ class TsTask(ctypes.Structure):
     ]
 
 
+class TransportConfigC(ctypes.Structure):
+    """Mirror of ``m4d_transport_config``."""
+
+    _fields_ = [
+        ("world", ctypes.c_int32),
+        ("rank", ctypes.c_int32),
+        ("device", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("ring_bytes", ctypes.c_uint64),
+        ("connect_timeout", ctypes.c_double),
+        ("session", ctypes.c_char_p),
+    ]
+
+
+class Completion(ctypes.Structure):
+    """Mirror of ``m4d_completion``."""
+
+    _fields_ = [
+        ("req_id", ctypes.c_uint64),
+        ("status", ctypes.c_int32),
+        ("kind", ctypes.c_int32),
+        ("bytes", ctypes.c_uint64),
+    ]
+
+
+class TransportStats(ctypes.Structure):
+    """Mirror of ``m4d_transport_stats``."""
+
+    _fields_ = [(name, ctypes.c_uint64) for name in (
+        "sends_completed", "recvs_completed", "bytes_sent", "bytes_received", "eager_bytes",
+        "nvlink_bytes", "rendezvous_pulls", "unexpected_messages")]
+
+
 # name -> (restype, argtypes); every symbol include/m4d.h declares.
 SIGNATURES: dict[str, tuple] = {
     "m4d_last_error": (_size, [ctypes.c_char_p, _size]),
@@ -95,6 +128,20 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_ipc_import": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.POINTER(_c_void_p)]),
     "m4d_ipc_close": (ctypes.c_int, [_c_void_p]),
     "m4d_enable_peer": (ctypes.c_int, [ctypes.c_int, ctypes.c_int]),
+    "m4d_transport_open": (ctypes.c_int, [ctypes.POINTER(TransportConfigC), ctypes.POINTER(_c_void_p)]),
+    "m4d_transport_wait_ready": (ctypes.c_int, [_c_void_p, ctypes.c_double]),
+    "m4d_transport_mesh_ready": (ctypes.c_int, [_c_void_p]),
+    "m4d_transport_post_send": (ctypes.c_int, [_c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32, _c_void_p,
+                                               _u64, ctypes.c_int, ctypes.c_int, _u64, ctypes.POINTER(Completion)]),
+    "m4d_transport_post_recv": (ctypes.c_int, [_c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32, _c_void_p,
+                                               _u64, ctypes.c_int, ctypes.c_int, _u64, ctypes.POINTER(Completion)]),
+    "m4d_transport_progress": (ctypes.c_int, [_c_void_p, ctypes.POINTER(Completion), ctypes.c_int]),
+    "m4d_transport_pending_completions": (ctypes.c_int, [_c_void_p]),
+    "m4d_transport_cancel": (ctypes.c_int, [_c_void_p, _u64, ctypes.POINTER(ctypes.c_int)]),
+    "m4d_transport_purge_channel": (ctypes.c_int, [_c_void_p, ctypes.c_uint32]),
+    "m4d_transport_peer_alive": (ctypes.c_int, [_c_void_p, ctypes.c_int]),
+    "m4d_transport_stats_get": (ctypes.c_int, [_c_void_p, ctypes.POINTER(TransportStats)]),
+    "m4d_transport_close": (ctypes.c_int, [_c_void_p]),
     "m4d_fill_block_f64": (ctypes.c_int, [_c_void_p, _i64, _i64, _i64, _i64, _u64, _c_void_p]),
     "m4d_ts_plan_create": (
         ctypes.c_int,

@@ -1,0 +1,321 @@
+"""``kind="nvlink"``: the B200 transport, a ctypes facade over ``libm4d.so``.
+
+Replaces the reference transports (``pkg/src/commshim/transport/sim.py``,
+``tcp.py``) behind the same :class:`~.base.Transport` contract
+(``base.py:199-306``); selected by ``transport_init(world, rank,
+TransportConfig(kind="nvlink", ...))``.  The C side (``csrc/transport.cpp``,
+ABI in ``include/m4d.h`` §3) owns matching, protocols and progress:
+
+* host payloads (headers, control messages, host frames) travel *eagerly*
+  through per-pair shared-memory rings, so small sends complete at post time;
+* device payloads (:class:`CudaRegion` windows) travel by *rendezvous*: the
+  receiver maps the sender's allocation through CUDA IPC and pulls the bytes
+  device-to-device over NVLink with the copy engines.  Nothing is staged
+  through host memory, so ``device_aware`` is True and the staging counters
+  stay zero (``tests/test_messaging.py:158-180`` of the reference).
+
+Progress is cooperative: ``test()``/``progress()`` call into the library,
+which drains rings, flushes queued sends and polls copy events; no host
+threads exist.  Every rank of a world must be on one node and share
+``TransportConfig.session`` (default: ``$M4D_SESSION``, else derived from the
+torchrun rendezvous).  Ranks may also share one process (test mode).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .. import native
+from ..errors import CommClosedError, ConfigurationError, StartupError, TransferError, UsageError
+from ..loop import MonotonicClock
+from .base import (
+    DeviceRegion,
+    DeviceView,
+    MemoryDomain,
+    Transport,
+    TransportConfig,
+    TransferRequest,
+    as_view,
+)
+
+_BATCH = 64
+
+
+_Config = native.TransportConfigC
+Completion = native.Completion
+Stats = native.TransportStats
+
+
+# -- device memory ------------------------------------------------------------------------------
+
+
+class CudaRegion(DeviceRegion):
+    """Real B200 memory behind the reference ``DeviceRegion`` interface.
+
+    ``window(offset, length)`` hands out :class:`DeviceView` windows (pointer
+    + length), which the nvlink transport moves device-to-device.  Backed by a
+    dedicated ``cudaMalloc`` (exportable through CUDA IPC) or by an external
+    device pointer whose ``owner`` keeps it alive (e.g. a torch tensor).
+    """
+
+    __slots__ = ("ptr", "_nbytes", "device", "_owner")
+
+    def __init__(self, size_or_bytes, device: int = 0, *, ptr: int | None = None, owner=None):
+        if ptr is not None:
+            self._owner = owner
+            self.ptr = int(ptr)
+            self._nbytes = int(size_or_bytes)
+        else:
+            data = None if isinstance(size_or_bytes, int) else bytes(size_or_bytes)
+            n = size_or_bytes if data is None else len(data)
+            buf = native.DeviceBuffer(device, max(1, n))
+            self._owner = buf
+            self.ptr = buf.ptr
+            self._nbytes = n
+            if data:
+                host = ctypes.create_string_buffer(data, n)
+                native.memcpy(self.ptr, ctypes.addressof(host), n)
+                native.check(native.lib().m4d_stream_sync(None))
+        self.device = device
+
+    @classmethod
+    def from_tensor(cls, tensor) -> "CudaRegion":
+        """Wrap a contiguous CUDA torch tensor (plumbing only; no copy)."""
+        if not tensor.is_cuda or not tensor.is_contiguous():
+            raise UsageError("CudaRegion.from_tensor needs a contiguous CUDA tensor")
+        return cls(tensor.numel() * tensor.element_size(), tensor.device.index or 0, ptr=tensor.data_ptr(),
+                   owner=tensor)
+
+    @property
+    def nbytes(self) -> int:
+        return self._nbytes
+
+    def window(self, offset: int = 0, length: int | None = None) -> DeviceView:
+        offset, length = self._bounds(offset, length)
+        return DeviceView(self.ptr + offset, length, self.device, self)
+
+    def to_bytes(self) -> bytes:
+        return native.to_host(self.ptr, self._nbytes)
+
+    def __repr__(self):
+        return f"<CudaRegion cuda:{self.device} {self._nbytes} B>"
+
+
+class _RegionPool:
+    """Size-class cache of receive regions so recv_payload does not cudaMalloc per frame."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.free: dict[int, list] = {}
+
+    def get(self, n: int) -> CudaRegion:
+        size = 1 << max(12, (max(n, 1) - 1).bit_length())
+        bucket = self.free.get(size)
+        buf = bucket.pop() if bucket else native.DeviceBuffer(self.device, size)
+        region = CudaRegion(n, self.device, ptr=buf.ptr, owner=_Lease(self, size, buf))
+        return region
+
+    def put(self, size: int, buf) -> None:
+        bucket = self.free.setdefault(size, [])
+        if len(bucket) < 8:
+            bucket.append(buf)
+
+
+class _Lease:
+    __slots__ = ("pool", "size", "buf")
+
+    def __init__(self, pool, size, buf):
+        self.pool, self.size, self.buf = pool, size, buf
+
+    def __del__(self):
+        try:
+            self.pool.put(self.size, self.buf)
+        except Exception:
+            pass
+
+
+def _host_address(view: memoryview) -> int:
+    if len(view) == 0:
+        return 0
+    if not view.readonly:
+        return ctypes.addressof(ctypes.c_char.from_buffer(view))
+    return int(np.frombuffer(view, dtype=np.uint8).ctypes.data)
+
+
+def default_session() -> str:
+    env = os.environ.get("M4D_SESSION")
+    if env:
+        return env
+    run = os.environ.get("TORCHELASTIC_RUN_ID")
+    port = os.environ.get("MASTER_PORT")
+    if run or port:
+        return f"te_{run or 'x'}_{port or 'x'}".replace("/", "_")
+    return "default"
+
+
+# -- the transport ------------------------------------------------------------------------------
+
+
+class NvlinkTransport(Transport):
+    """One rank of an NVLink world (see the module docstring)."""
+
+    def __init__(self, world_size: int, rank: int, config: TransportConfig | None = None):
+        config = config or TransportConfig(kind="nvlink")
+        super().__init__(world_size, rank, config.max_count, True, MonotonicClock())
+        count = native.device_count()
+        if config.device is not None:
+            device = config.device
+            if device >= 0 and device >= count:
+                raise ConfigurationError(f"CUDA device {device} not present ({count} visible)")
+        else:
+            device = rank % count if count else -1
+        self.device = device
+        self.session = config.session or default_session()
+        cfg = _Config(world_size, rank, device, 0, config.ring_bytes, float(config.connect_timeout),
+                      self.session.encode())
+        handle = ctypes.c_void_p()
+        status = native.lib().m4d_transport_open(ctypes.byref(cfg), ctypes.byref(handle))
+        if status != native.OK:
+            raise native.error_for(status, native.last_error(), rank=_rank_in(native.last_error()))
+        self._h = handle.value
+        self._lib = native.lib()
+        self._live: dict[int, TransferRequest] = {}
+        self._now = Completion()
+        self._batch = (Completion * _BATCH)()
+        self._pool = _RegionPool(device) if device >= 0 else None
+        self.connect_timeout = config.connect_timeout
+
+    # -- mesh -----------------------------------------------------------------------------------
+
+    @property
+    def mesh_ready(self) -> bool:
+        return bool(self._lib.m4d_transport_mesh_ready(self._h))
+
+    def wait_ready(self, timeout: float | None = None) -> None:
+        """Block until every peer rank is up (StartupError names a missing rank)."""
+        status = self._lib.m4d_transport_wait_ready(self._h, self.connect_timeout if timeout is None else timeout)
+        if status != native.OK:
+            msg = native.last_error()
+            raise native.error_for(status, msg, rank=_rank_in(msg))
+
+    # -- posts ----------------------------------------------------------------------------------
+
+    def _post(self, direction: str, channel: int, peer: int, tag: int, data, domain) -> TransferRequest:
+        view = as_view(data)
+        if direction == "recv" and view.readonly:
+            raise UsageError("receive buffer must be writable")
+        self._check_post(channel, peer, tag, view)
+        req = TransferRequest(self, direction, channel, peer, tag, view, domain)
+        if isinstance(view, DeviceView):
+            addr, on_device = view.ptr, 1
+        else:
+            addr, on_device = _host_address(view), 0
+        fn = self._lib.m4d_transport_post_send if direction == "send" else self._lib.m4d_transport_post_recv
+        now = self._now
+        status = fn(self._h, channel, peer, tag, addr, len(view), int(domain), on_device, req.id, ctypes.byref(now))
+        if status != native.OK:
+            raise native.error_for(status, native.last_error())
+        if now.status == -1:
+            self._live[req.id] = req
+            req._native = req.id
+        else:
+            self._apply(req, now.status, now.bytes)
+        return self._track(req)
+
+    def post_send(self, channel: int, peer: int, tag: int, data,
+                  domain: MemoryDomain = MemoryDomain.HOST) -> TransferRequest:
+        return self._post("send", channel, peer, tag, data, domain)
+
+    def post_recv(self, channel: int, peer: int, tag: int, buffer,
+                  domain: MemoryDomain = MemoryDomain.HOST) -> TransferRequest:
+        return self._post("recv", channel, peer, tag, buffer, domain)
+
+    # -- completions ------------------------------------------------------------------------------
+
+    def _apply(self, req: TransferRequest, status: int, nbytes: int) -> None:
+        if status == native.OK:
+            m = self.metrics
+            if req.direction == "send":
+                m.sends_completed += 1
+                m.bytes_sent += nbytes
+            else:
+                m.recvs_completed += 1
+                m.bytes_received += nbytes
+            req._finish(TransferRequest.COMPLETE, nbytes)
+            return
+        message = native.last_error() or f"transfer failed (status {status})"
+        if status == native.ERR_CLOSED:
+            error = CommClosedError(f"rank {req.peer} connection closed")
+        elif status == native.ERR_TRANSFER:
+            error = TransferError(f"rank {req.peer} closed the connection", bytes_moved=nbytes)
+        else:
+            error = native.error_for(status, message, bytes_moved=nbytes)
+        req._finish(TransferRequest.FAILED, nbytes if status == native.ERR_TRANSFER else 0, error)
+
+    def progress(self) -> int:
+        finished = 0
+        batch = self._batch
+        while True:
+            n = self._lib.m4d_transport_progress(self._h, batch, _BATCH)
+            for k in range(n):
+                c = batch[k]
+                req = self._live.pop(c.req_id, None)
+                if req is not None:
+                    self._apply(req, c.status, c.bytes)
+                    finished += 1
+            if n < _BATCH:
+                return finished
+
+    def cancel(self, request: TransferRequest) -> bool:
+        if request._owner is not self:
+            raise UsageError("request belongs to a different transport")
+        if not request.pending:
+            return False
+        flag = ctypes.c_int(0)
+        native.check(self._lib.m4d_transport_cancel(self._h, request.id, ctypes.byref(flag)))
+        if not flag.value:
+            return False
+        self._live.pop(request.id, None)
+        self._cancelled(request)
+        return True
+
+    def purge_channel(self, channel: int) -> None:
+        native.check(self._lib.m4d_transport_purge_channel(self._h, channel))
+        self.progress()
+
+    def peer_alive(self, peer: int) -> bool:
+        return bool(self._lib.m4d_transport_peer_alive(self._h, peer))
+
+    def native_stats(self) -> dict:
+        st = Stats()
+        native.check(self._lib.m4d_transport_stats_get(self._h, ctypes.byref(st)))
+        return {name: int(getattr(st, name)) for name, _ in Stats._fields_}
+
+    # -- device regions ------------------------------------------------------------------------
+
+    def allocate_region(self, length: int, domain: MemoryDomain):
+        """Receive buffers: device frames land in pooled B200 memory, never in host RAM."""
+        if domain == MemoryDomain.DEVICE and self._pool is not None:
+            return self._pool.get(length)
+        return super().allocate_region(length, domain)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            self._lib.m4d_transport_close(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _rank_in(message: str) -> int | None:
+    import re
+
+    m = re.search(r"rank (\d+)", message or "")
+    return int(m.group(1)) if m else None
