@@ -903,6 +903,7 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
         u->second.pop_front();
         if (u->second.empty()) p.unexpected.erase(u);
         deliver_unexpected(t, peer, raw, msg);
+        flush_peer(t, peer);  // a truncation / empty-rendezvous FIN leaves now
     } else if (p.dead) {
         fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
         complete(t, raw, M4D_ERR_CLOSED, 0);
@@ -921,12 +922,14 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
 
 int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
     map_missing_peers(t);
+    // Copies first: a finished pull must send its FIN in this same call, or a
+    // sender whose peer stops polling would wait forever.
+    if (!t->copies.empty()) poll_copies(t);
     for (int q = 0; q < t->world; ++q)
         if (q != t->rank) {
             drain_peer(t, q);
             flush_peer(t, q);
         }
-    if (!t->copies.empty()) poll_copies(t);
     if (!t->reqs.empty()) check_liveness(t);
     int n = 0;
     const int avail = static_cast<int>(t->done.size());
