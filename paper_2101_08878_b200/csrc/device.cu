@@ -37,6 +37,37 @@ static PFN_getAddressRange address_range_fn() {
     return fn;
 }
 
+typedef CUresult (*PFN_pointerGetAttribute)(void*, CUpointer_attribute, CUdeviceptr);
+static PFN_pointerGetAttribute pointer_attribute_fn() {
+    static PFN_pointerGetAttribute fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuPointerGetAttribute", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_pointerGetAttribute>(p);
+    });
+    return fn;
+}
+
+int alloc_info(const void* ptr, uint64_t* base, uint64_t* size, uint64_t* buffer_id) {
+    PFN_getAddressRange range = address_range_fn();
+    PFN_pointerGetAttribute attr = pointer_attribute_fn();
+    if (!range || !attr) return fail(M4D_ERR_CUDA, "driver entry points unavailable");
+    CUdeviceptr b = 0;
+    size_t sz = 0;
+    if (range(&b, &sz, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+        return fail(M4D_ERR_USAGE, "pointer %p is not a device allocation", ptr);
+    unsigned long long id = 0;
+    if (attr(&id, CU_POINTER_ATTRIBUTE_BUFFER_ID, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
+        return fail(M4D_ERR_CUDA, "cuPointerGetAttribute(BUFFER_ID) failed for %p", ptr);
+    *base = static_cast<uint64_t>(b);
+    *size = sz;
+    *buffer_id = id;
+    return M4D_OK;
+}
+
 }  // namespace m4d
 
 using namespace m4d;
@@ -123,7 +154,12 @@ m4d_status m4d_event_elapsed_ms(void* start, void* stop, float* ms_out) {
 
 m4d_status m4d_malloc(int device, size_t nbytes, void** ptr_out) {
     M4D_CUDA_TRY(cudaSetDevice(device));
-    M4D_CUDA_TRY(cudaMalloc(ptr_out, nbytes ? nbytes : 1));
+    // Whole 2 MiB granules: small cudaMallocs can share one driver chunk, and
+    // legacy CUDA IPC then refuses to map a second allocation of that chunk in
+    // the peer (cudaErrorAlreadyMapped).  Every m4d allocation is exportable.
+    const size_t granule = 2u << 20;
+    const size_t rounded = ((nbytes ? nbytes : 1) + granule - 1) / granule * granule;
+    M4D_CUDA_TRY(cudaMalloc(ptr_out, rounded));
     return M4D_OK;
 }
 

@@ -13,6 +13,22 @@ namespace m4d {
 // Records a formatted message for m4d_last_error() and returns `code`.
 int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 
+// Allocation containing `ptr`: base, size and the driver's unique buffer id.
+int alloc_info(const void* ptr, uint64_t* base, uint64_t* size, uint64_t* buffer_id);
+
+// Rendezvous pulls launched as one SM copy kernel (pull.cu).
+constexpr int kMaxPull = 8;
+struct PullDesc {
+    const uint8_t* src;
+    uint8_t* dst;
+    size_t len;
+};
+struct PullBatch {
+    PullDesc d[kMaxPull];
+    int n;
+};
+int launch_pull_batch(const PullBatch& batch, cudaStream_t stream);
+
 inline int cuda_fail(cudaError_t err, const char* what) {
     return fail(M4D_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
 }

@@ -24,6 +24,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <errno.h>
+#include <stdlib.h>
 #include <fcntl.h>
 #include <signal.h>
 #include <string.h>
@@ -32,6 +33,7 @@
 #include <time.h>
 #include <unistd.h>
 
+#include <array>
 #include <atomic>
 #include <deque>
 #include <map>
@@ -108,6 +110,7 @@ struct RtsRec {
     uint64_t offset;   // ptr - allocation base
     int32_t pid;
     int32_t device;
+    uint64_t buffer_id;  // driver-unique id of the allocation (mapping cache key)
     uint8_t handle[64];
 };
 
@@ -198,8 +201,19 @@ struct Copy {
     int peer;
     uint64_t send_id;
     uint64_t bytes;
-    cudaEvent_t ev;
+    cudaEvent_t ev;   // may be shared by the messages of one batched launch
+    bool owns_event;  // the last message of a launch returns the event to the pool
 };
+
+struct PendingPull {
+    Req* recv;
+    int peer;
+    uint64_t send_id;
+    const uint8_t* src;
+    uint64_t len;
+};
+
+constexpr uint64_t kSmallPull = 64 * 1024;  // below this a copy-engine memcpy is cheaper than a launch
 
 inline uint64_t ckey(uint32_t channel, uint32_t tag) { return (static_cast<uint64_t>(channel) << 32) | tag; }
 
@@ -231,10 +245,15 @@ struct m4d_transport {
     std::unordered_map<uint64_t, std::unique_ptr<Req>> reqs;  // live requests by id
     std::unordered_map<uint64_t, Req*> awaiting_fin;           // rendezvous sends by id
     std::vector<Copy> copies;
+    std::vector<PendingPull> pending_pulls;
+    bool use_ce = false;                                        // M4D_PULL_ENGINE=ce: copy engine only
     std::vector<cudaEvent_t> spare_events;
     std::vector<m4d_completion> done;
-    std::map<std::string, void*> ipc_maps;                      // handle bytes -> mapped base
-    cudaStream_t stream = nullptr;
+    std::map<std::pair<int, uint64_t>, void*> ipc_maps;         // (pid, buffer id) -> mapped base
+    std::unordered_map<uint64_t, std::pair<uint64_t, std::array<uint8_t, 64>>> exports;  // buffer id -> (base, handle)
+    cudaStream_t stream = nullptr;                             // (kept: first of the pull streams)
+    std::vector<cudaStream_t> pull_streams;                     // copies round-robin over these
+    size_t next_stream = 0;
     double last_liveness = 0.0;
     double last_map_attempt = 0.0;
     int unmapped = 0;
@@ -301,13 +320,20 @@ void queue_fin(m4d_transport* t, int peer, uint64_t send_id, int status, uint64_
 void* map_peer_allocation(m4d_transport* t, const RtsRec& rts, int* status) {
     *status = M4D_OK;
     if (rts.pid == static_cast<int32_t>(getpid())) return reinterpret_cast<void*>(rts.src_ptr);
-    std::string key(reinterpret_cast<const char*>(rts.handle), 64);
+    const std::pair<int, uint64_t> key(rts.pid, rts.buffer_id);
     auto it = t->ipc_maps.find(key);
     if (it != t->ipc_maps.end()) return static_cast<uint8_t*>(it->second) + rts.offset;
     cudaIpcMemHandle_t h;
     memcpy(&h, rts.handle, 64);
     void* base = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e == cudaErrorAlreadyMapped) {
+        cudaGetLastError();
+        *status = fail(M4D_ERR_CUDA, "rendezvous source shares a driver chunk with an allocation already mapped "
+                                     "from rank pid %d: allocate device frames with m4d_malloc (2 MiB granules)",
+                       rts.pid);
+        return nullptr;
+    }
     if (e != cudaSuccess) {
         *status = m4d::cuda_fail(e, "cudaIpcOpenMemHandle (rendezvous source)");
         return nullptr;
@@ -333,28 +359,68 @@ void start_pull(m4d_transport* t, int peer, Req* r, const RtsRec& rts) {
     }
     int st;
     void* src = map_peer_allocation(t, rts, &st);
-    cudaError_t e = cudaSuccess;
-    cudaEvent_t ev = nullptr;
-    if (src) {
-        if (!t->spare_events.empty()) {
-            ev = t->spare_events.back();
-            t->spare_events.pop_back();
-        } else {
-            e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-        }
-        if (e == cudaSuccess) e = cudaMemcpyAsync(r->ptr, src, rts.len, cudaMemcpyDefault, t->stream);
-        if (e == cudaSuccess) e = cudaEventRecord(ev, t->stream);
-        if (e != cudaSuccess) st = m4d::cuda_fail(e, "rendezvous pull");
-    }
     if (st != M4D_OK) {
-        if (ev) t->spare_events.push_back(ev);
         queue_fin(t, peer, rts.send_id, M4D_ERR_TRANSFER, 0);
         complete(t, r, M4D_ERR_CUDA, 0);
         return;
     }
-    t->copies.push_back(Copy{r, peer, rts.send_id, rts.len, ev});
+    t->pending_pulls.push_back(PendingPull{r, peer, rts.send_id, static_cast<const uint8_t*>(src), rts.len});
     t->stats.rendezvous_pulls++;
     t->stats.nvlink_bytes += rts.len;
+}
+
+// Issues every pull matched since the last call.  Large ones go out as SM
+// copy kernels, up to kMaxPull messages per launch, round-robin over the pull
+// streams (several launches in flight); small ones use the copy engine, whose
+// fixed cost is lower than a launch.  One event per launch or copy.
+void flush_pulls(m4d_transport* t) {
+    if (t->pending_pulls.empty()) return;
+    cudaSetDevice(t->device);
+    auto take_event = [&](cudaEvent_t* ev) -> cudaError_t {
+        if (!t->spare_events.empty()) {
+            *ev = t->spare_events.back();
+            t->spare_events.pop_back();
+            return cudaSuccess;
+        }
+        return cudaEventCreateWithFlags(ev, cudaEventDisableTiming);
+    };
+    auto fail_all = [&](size_t from, size_t to, cudaError_t e) {
+        m4d::cuda_fail(e, "rendezvous pull");
+        for (size_t i = from; i < to; ++i) {
+            PendingPull& pp = t->pending_pulls[i];
+            queue_fin(t, pp.peer, pp.send_id, M4D_ERR_TRANSFER, 0);
+            complete(t, pp.recv, M4D_ERR_CUDA, 0);
+        }
+    };
+    std::vector<PendingPull>& v = t->pending_pulls;
+    size_t i = 0;
+    while (i < v.size()) {
+        cudaStream_t s = t->pull_streams[t->next_stream++ % t->pull_streams.size()];
+        cudaEvent_t ev = nullptr;
+        cudaError_t e = take_event(&ev);
+        size_t j = i + 1;
+        // The SM kernel needs a device destination; host buffers use the copy engine.
+        auto via_kernel = [&](const PendingPull& pp) { return !t->use_ce && pp.len >= kSmallPull && pp.recv->device; };
+        if (e == cudaSuccess && !via_kernel(v[i])) {
+            e = cudaMemcpyAsync(v[i].recv->ptr, v[i].src, v[i].len, cudaMemcpyDefault, s);
+        } else if (e == cudaSuccess) {
+            m4d::PullBatch batch;
+            batch.n = 0;
+            for (j = i; j < v.size() && batch.n < m4d::kMaxPull && via_kernel(v[j]); ++j)
+                batch.d[batch.n++] = m4d::PullDesc{v[j].src, v[j].recv->ptr, v[j].len};
+            if (m4d::launch_pull_batch(batch, s) != M4D_OK) e = cudaErrorLaunchFailure;
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(ev, s);
+        if (e != cudaSuccess) {
+            if (ev) t->spare_events.push_back(ev);
+            fail_all(i, j, e);
+        } else {
+            for (size_t k = i; k < j; ++k)
+                t->copies.push_back(Copy{v[k].recv, v[k].peer, v[k].send_id, v[k].len, ev, k + 1 == j});
+        }
+        i = j;
+    }
+    v.clear();
 }
 
 // A receive meets a buffered unexpected message.
@@ -606,6 +672,7 @@ int drain_peer(m4d_transport* t, int peer) {
         ++n;
     }
     if (n) ring.ctl->head.store(ring.cursor, std::memory_order_release);
+    flush_pulls(t);
     if (p.said_bye && !p.dead) fail_peer(t, peer, M4D_ERR_CLOSED, "closed the connection");
     return n;
 }
@@ -627,7 +694,7 @@ int poll_copies(m4d_transport* t) {
             queue_fin(t, c.peer, c.send_id, M4D_ERR_TRANSFER, 0);
             complete(t, c.recv, M4D_ERR_CUDA, 0);
         }
-        t->spare_events.push_back(c.ev);
+        if (c.owns_event) t->spare_events.push_back(c.ev);
         t->copies[i] = t->copies.back();
         t->copies.pop_back();
         ++n;
@@ -799,7 +866,14 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
 
     if (t->device >= 0) {
         cudaError_t e = cudaSetDevice(t->device);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking);
+        const int nstreams = getenv("M4D_PULL_STREAMS") ? atoi(getenv("M4D_PULL_STREAMS")) : 4;
+        for (int k = 0; k < (nstreams > 0 ? nstreams : 1) && e == cudaSuccess; ++k) {
+            cudaStream_t st = nullptr;
+            e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+            if (e == cudaSuccess) t->pull_streams.push_back(st);
+        }
+        if (e == cudaSuccess) t->stream = t->pull_streams[0];
+        if (const char* eng = getenv("M4D_PULL_ENGINE")) t->use_ce = strcmp(eng, "ce") == 0;
         if (e != cudaSuccess) {
             m4d_transport* raw = t.release();
             m4d_transport_close(raw);
@@ -857,8 +931,19 @@ m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer,
         rts.src_ptr = reinterpret_cast<uint64_t>(ptr);
         rts.pid = static_cast<int32_t>(getpid());
         rts.device = t->device;
-        st = m4d_ipc_export(ptr, rts.handle, &rts.offset);
+        uint64_t base = 0, size = 0;
+        st = m4d::alloc_info(ptr, &base, &size, &rts.buffer_id);
         if (st) return st;
+        rts.offset = reinterpret_cast<uint64_t>(ptr) - base;
+        auto ex = t->exports.find(rts.buffer_id);
+        if (ex == t->exports.end() || ex->second.first != base) {
+            std::array<uint8_t, 64> h;
+            uint64_t off0 = 0;
+            st = m4d_ipc_export(reinterpret_cast<void*>(base), h.data(), &off0);
+            if (st) return st;
+            ex = t->exports.insert_or_assign(rts.buffer_id, std::make_pair(base, h)).first;
+        }
+        memcpy(rts.handle, ex->second.second.data(), 64);
     }
     t->reqs[req_id] = std::move(r);
     raw->in_outq = true;
@@ -903,6 +988,7 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
         u->second.pop_front();
         if (u->second.empty()) p.unexpected.erase(u);
         deliver_unexpected(t, peer, raw, msg);
+        flush_pulls(t);
         flush_peer(t, peer);  // a truncation / empty-rendezvous FIN leaves now
     } else if (p.dead) {
         fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
@@ -1056,11 +1142,12 @@ m4d_status m4d_transport_close(m4d_transport* t) {
         }
     }
     if (t->me) t->me->state.store(kStateClosed, std::memory_order_release);
-    if (t->stream) {
-        cudaStreamSynchronize(t->stream);
-        for (Copy& c : t->copies) t->spare_events.push_back(c.ev);
+    if (!t->pull_streams.empty()) {
+        for (cudaStream_t st : t->pull_streams) cudaStreamSynchronize(st);
+        for (Copy& c : t->copies)
+            if (c.owns_event) t->spare_events.push_back(c.ev);
         for (cudaEvent_t e : t->spare_events) cudaEventDestroy(e);
-        cudaStreamDestroy(t->stream);
+        for (cudaStream_t st : t->pull_streams) cudaStreamDestroy(st);
     }
     for (auto& kv : t->ipc_maps) cudaIpcCloseMemHandle(kv.second);
     for (Peer& p : t->peers)
