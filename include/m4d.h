@@ -207,6 +207,39 @@ int m4d_ts_plan_uses_tma(const m4d_ts_plan* plan);
 /* Number of kernel launches one m4d_ts_run of this plan issues (gpu_launches accounting). */
 int m4d_ts_launches_per_run(const m4d_ts_plan* plan);
 
+/* ------------------------------------------------------------------------ */
+/* 5. key_merge (K5 partition, K7 join, K8 digest)                          */
+/* ------------------------------------------------------------------------ */
+
+enum {
+    M4D_PART_LOCAL = 0,  /* bucket = (h & 0xffffffff) >> (32 - log2 buckets), h = splitmix64(key) */
+    M4D_PART_RANK = 1    /* bucket = owner rank = (uint32(h >> 32) * buckets) >> 32               */
+};
+
+/* Table generator: keys[i] = band + splitmix64(seed + row0 + i) % total,
+ * vals[i] = row0 + i (the global row index). */
+m4d_status m4d_merge_generate(int64_t* keys, int64_t* vals, int64_t row0, int64_t count,
+                              uint64_t total, uint64_t seed, uint64_t band, void* stream);
+/* Device scratch m4d_partition needs for n rows and `buckets` buckets. */
+size_t m4d_partition_scratch_bytes(int64_t n, int buckets);
+/* Hash partition of one SoA table (keys, vals) into `buckets` buckets, written
+ * bucket-major to (out_keys, out_vals); bounds[buckets + 1] (device) receives
+ * the bucket start offsets.  The hash shuffle of SPEC.md:425. */
+m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
+                         int64_t* out_keys, int64_t* out_vals, int64_t* bounds, void* scratch,
+                         size_t scratch_bytes, void* stream);
+int m4d_partition_launches(void);
+/* Inner join of partitioned build (left) and probe (right) tables, partition
+ * by partition (bounds from m4d_partition, same bucket count).  Writes at most
+ * `capacity` rows (key, lval, rval) and result[4] (device) =
+ * {rows produced, rows, sum of row hashes, sum of keys} (mod 2^64); a row
+ * count above `capacity` means the output was cut: retry with a larger
+ * buffer. */
+m4d_status m4d_hash_join(const int64_t* lkeys, const int64_t* lvals, const int64_t* lbounds,
+                         const int64_t* rkeys, const int64_t* rvals, const int64_t* rbounds, int parts,
+                         int64_t* out_keys, int64_t* out_lvals, int64_t* out_rvals, int64_t capacity,
+                         unsigned long long* result, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

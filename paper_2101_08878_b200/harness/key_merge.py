@@ -1,0 +1,247 @@
+"""``key_merge``: inner merge of two int64-key dataframes across B200s.
+
+Operator definition: SPEC.md:422-430 (each worker generates its partitions of
+the left and right tables with a match-fraction overlap band, hash-shuffles
+rows to their owner, joins locally, reports the global row count), PAPER.md
+:387-389 and :438 (cuDF merge, chunk 1e8, ``Shuffle: True``, fraction 0.3).
+
+Generator: ``total`` rows per side over all workers (weak
+scaling: ``rows_per_rank * world``), worker ``r`` owns global rows
+``[r*n, (r+1)*n)``; left key = ``splitmix64(seed_l + g) % total``, right key
+= ``floor((1-f)*total) + splitmix64(seed_r + g) % total``; payload = ``g``.
+
+B200 pipeline per rank (one CUDA stream, SoA device columns):
+
+1. world > 1: hash-partition both tables by owner rank (``m4d_partition``
+   mode RANK) and move every peer's segment with the nvlink transport:
+   device-frame rendezvous, i.e. the owner pulls the rows straight out of
+   the sender's HBM over NVLink (one message per column, counts first);
+2. hash-partition the rows this rank owns into ``parts`` local partitions
+   of ~6K rows (mode LOCAL), small enough for a shared-memory hash table;
+3. ``m4d_hash_join``: one CTA per partition builds and probes, writes the
+   (key, lval, rval) rows and an order-independent digest (count, sum of
+   row hashes, sum of keys, mod 2^64).
+
+The global result is the digest summed over ranks: identical for every
+worker count, and equal to the oracle's (tests/test_key_merge_gpu.py).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import struct
+
+from .. import native
+from ..errors import CommShimError, UsageError
+from ..messaging import await_request
+from ..transport import MemoryDomain
+
+SEED_LEFT = 0x4C454654
+SEED_RIGHT = 0x52494748
+EXCHANGE_TAG = 900
+DATA_TAG = 910
+_MASK64 = (1 << 64) - 1
+
+
+def merge_band(total: int, fraction: float) -> int:
+    """floor((1 - f) * total) in IEEE double (the overlap band start)."""
+    return int(math.floor((1.0 - fraction) * float(total)))
+
+
+def choose_parts(rows: int) -> int:
+    parts = 1
+    while parts < 16384 and rows / parts > 6000:
+        parts *= 2
+    return parts
+
+
+class _Columns:
+    """keys + vals device columns of one table (capacity rows)."""
+
+    def __init__(self, device: int, capacity: int):
+        self.capacity = max(1, int(capacity))
+        self.keys = native.DeviceBuffer(device, self.capacity * 8)
+        self.vals = native.DeviceBuffer(device, self.capacity * 8)
+
+
+async def allgather(transport, payload: bytes, tag: int = EXCHANGE_TAG) -> list[bytes]:
+    """Every rank's ``payload`` (same length everywhere) over the world channel."""
+    world, me = transport.world_size, transport.rank
+    out = [b""] * world
+    out[me] = payload
+    if world == 1:
+        return out
+    bufs = {p: bytearray(len(payload)) for p in range(world) if p != me}
+    reqs = [transport.post_recv(0, p, tag, bufs[p]) for p in bufs]
+    reqs += [transport.post_send(0, p, tag, payload) for p in bufs]
+    for r in reqs:
+        await await_request(transport, r)
+    for p, b in bufs.items():
+        out[p] = bytes(b)
+    return out
+
+
+class KeyMerge:
+    """One rank's share of a distributed inner merge on an int64 key."""
+
+    def __init__(self, rows_per_rank: int, fraction: float = 0.3, *, rank: int = 0, world: int = 1,
+                 device: int = 0, transport=None, seed_l: int = SEED_LEFT, seed_r: int = SEED_RIGHT,
+                 parts: int | None = None, stream: native.Stream | None = None):
+        if rows_per_rank < 0 or not 0.0 <= fraction <= 1.0:
+            raise UsageError("rows per rank must be >= 0 and fraction in [0, 1]")
+        if world > 1 and transport is None:
+            raise UsageError("a multi-worker key_merge needs a transport")
+        self.n = int(rows_per_rank)
+        self.fraction = fraction
+        self.rank, self.world, self.device = rank, world, device
+        self.transport = transport
+        self.total = self.n * world
+        self.band = merge_band(self.total, fraction) if self.total else 0
+        self.seeds = (seed_l, seed_r)
+        native.set_device(device)
+        self.stream = stream or native.Stream(device)
+        self.parts = parts or choose_parts(self.n)
+        slack = self.n + int(6 * math.sqrt(max(self.n, 1))) + 4096
+        self.inputs = [_Columns(device, self.n), _Columns(device, self.n)]
+        self.sendbuf = [_Columns(device, self.n), _Columns(device, self.n)] if world > 1 else None
+        self.recv = [_Columns(device, slack), _Columns(device, slack)] if world > 1 else None
+        self.parted = [_Columns(device, slack), _Columns(device, slack)]
+        self.bounds = [native.DeviceBuffer(device, (max(self.parts, world) + 1) * 8) for _ in range(2)]
+        self.rank_bounds = [native.DeviceBuffer(device, (world + 1) * 8) for _ in range(2)]
+        scratch = max(native.lib().m4d_partition_scratch_bytes(slack, self.parts),
+                      native.lib().m4d_partition_scratch_bytes(self.n, max(world, 1)))
+        self.scratch = native.DeviceBuffer(device, scratch)
+        self.scratch_bytes = scratch
+        self.out_capacity = int(fraction * self.n * 1.25) + 65536
+        self.out = [native.DeviceBuffer(device, self.out_capacity * 8) for _ in range(3)]
+        self.result = native.DeviceBuffer(device, 4 * 8)
+        self.received = [0, 0]
+        self.launches = 0
+
+    # -- data -------------------------------------------------------------------------------
+
+    def generate(self) -> None:
+        lib = native.lib()
+        row0 = self.rank * self.n
+        for side, (cols, seed, band) in enumerate(zip(self.inputs, self.seeds, (0, self.band))):
+            if self.n:
+                native.check(lib.m4d_merge_generate(cols.keys.ptr, cols.vals.ptr, row0, self.n, self.total, seed,
+                                                    band, self.stream.handle))
+        self.stream.synchronize()
+
+    # -- pipeline ---------------------------------------------------------------------------
+
+    def _partition(self, src: _Columns, n: int, mode: int, buckets: int, dst: _Columns, bounds) -> None:
+        native.check(native.lib().m4d_partition(src.keys.ptr, src.vals.ptr, n, mode, buckets, dst.keys.ptr,
+                                                dst.vals.ptr, bounds.ptr, self.scratch.ptr, self.scratch_bytes,
+                                                self.stream.handle))
+        self.launches += native.lib().m4d_partition_launches()
+
+    def _read_bounds(self, buf, count: int) -> list[int]:
+        raw = native.to_host(buf.ptr, (count + 1) * 8, self.stream)
+        return list(struct.unpack(f"<{count + 1}q", raw))
+
+    async def _shuffle(self) -> list[int]:
+        """Partition by owner rank and pull every peer's segments over NVLink."""
+        from ..transport.base import DeviceView
+
+        t, P, me = self.transport, self.world, self.rank
+        sends = []  # per side: row bounds per destination
+        for side in range(2):
+            self._partition(self.inputs[side], self.n, 1, P, self.sendbuf[side], self.rank_bounds[side])
+            sends.append(self._read_bounds(self.rank_bounds[side], P))
+        counts = [[sends[s][d + 1] - sends[s][d] for d in range(P)] for s in range(2)]
+        blob = struct.pack(f"<{2 * P}q", *counts[0], *counts[1])
+        table = [struct.unpack(f"<{2 * P}q", b) for b in await allgather(t, blob)]
+        incoming = [[table[src][side * P + me] for src in range(P)] for side in range(2)]
+        received = []
+        reqs = []
+        for side in range(2):
+            total = sum(incoming[side])
+            if total > self.recv[side].capacity:
+                self.recv[side] = _Columns(self.device, int(total * 1.1) + 4096)
+            if total > self.parted[side].capacity:
+                self.parted[side] = _Columns(self.device, int(total * 1.1) + 4096)
+            received.append(total)
+            at = 0
+            for src in range(P):
+                rows = incoming[side][src]
+                for col in ("keys", "vals"):
+                    dst = getattr(self.recv[side], col).ptr + at * 8
+                    if src == me:
+                        lo = sends[side][me]
+                        native.memcpy(dst, getattr(self.sendbuf[side], col).ptr + lo * 8, rows * 8, self.stream)
+                    elif rows:
+                        tag = DATA_TAG + side * 2 + (col == "vals")
+                        view = DeviceView(dst, rows * 8, self.device)
+                        reqs.append(t.post_recv(0, src, tag, view, MemoryDomain.DEVICE))
+                at += rows
+            for dst_rank in range(P):
+                rows = counts[side][dst_rank]
+                if dst_rank == me or not rows:
+                    continue
+                lo = sends[side][dst_rank]
+                for col in ("keys", "vals"):
+                    tag = DATA_TAG + side * 2 + (col == "vals")
+                    view = DeviceView(getattr(self.sendbuf[side], col).ptr + lo * 8, rows * 8, self.device)
+                    reqs.append(t.post_send(0, dst_rank, tag, view, MemoryDomain.DEVICE))
+        # the send buffers were written on self.stream: make them visible before peers pull
+        self.stream.synchronize()
+        for r in reqs:
+            await await_request(t, r)
+        return received
+
+    async def run(self) -> tuple[int, int, int]:
+        """One full step (partition [+ shuffle] + join).  Returns this rank's digest."""
+        if self.world > 1:
+            self.received = await self._shuffle()
+            tables = self.recv
+        else:
+            self.received = [self.n, self.n]
+            tables = self.inputs
+        for side in range(2):
+            self._partition(tables[side], self.received[side], 0, self.parts, self.parted[side], self.bounds[side])
+        while True:
+            native.check(native.lib().m4d_hash_join(
+                self.parted[0].keys.ptr, self.parted[0].vals.ptr, self.bounds[0].ptr,
+                self.parted[1].keys.ptr, self.parted[1].vals.ptr, self.bounds[1].ptr, self.parts,
+                self.out[0].ptr, self.out[1].ptr, self.out[2].ptr, self.out_capacity, self.result.ptr,
+                self.stream.handle))
+            self.launches += 2
+            raw = native.to_host(self.result.ptr, 32, self.stream)
+            produced, count, hsum, ksum = struct.unpack("<4Q", raw)
+            if count <= self.out_capacity:
+                self.rows_out = count
+                return count, hsum, ksum
+            # output cut short: grow and re-join (rare: skewed keys)
+            self.out_capacity = int(count * 1.1) + 65536
+            self.out = [native.DeviceBuffer(self.device, self.out_capacity * 8) for _ in range(3)]
+
+    async def run_global(self) -> tuple[int, int, int]:
+        """run() plus the digest summed over all ranks (the global row count of SPEC.md:426)."""
+        mine = await self.run()
+        if self.world == 1:
+            return mine
+        parts = await allgather(self.transport, struct.pack("<3Q", *mine), tag=EXCHANGE_TAG + 1)
+        total = [0, 0, 0]
+        for blob in parts:
+            for k, v in enumerate(struct.unpack("<3Q", blob)):
+                total[k] = (total[k] + v) & _MASK64
+        return tuple(total)
+
+    def output_rows(self, limit: int | None = None):
+        """The materialised (key, lval, rval) rows of this rank (host copy, for tests)."""
+        import numpy as np
+
+        n = self.rows_out if limit is None else min(limit, self.rows_out)
+        cols = [np.frombuffer(native.to_host(b.ptr, n * 8, self.stream), dtype=np.int64) for b in self.out]
+        return cols
+
+    def algorithmic_bytes(self) -> dict:
+        """read both input tables once (16 B/row/side), write the
+        output once (24 B/row); NVLink: the rows that change owner (16 B/row/side)."""
+        moved = 0
+        if self.world > 1:
+            moved = 2 * self.n * 16 * (self.world - 1) // self.world
+        return {"hbm": 2 * self.n * 16 + getattr(self, "rows_out", 0) * 24, "nvlink": moved}

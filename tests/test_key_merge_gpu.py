@@ -1,0 +1,99 @@
+"""key_merge parity on a B200: GPU digest (row count, sum of row hashes, sum of keys)
+and the row multiset vs the CPU oracle; worker-count independence."""
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def run_world(rows_per_rank, world, fraction, parts=None):
+    from paper_2101_08878_b200.harness.key_merge import KeyMerge
+    from paper_2101_08878_b200.loop import MonotonicClock, TaskLoop, gather
+
+    from nvlink_fixtures import close_all, nvlink_transports
+
+    ts = nvlink_transports(world, 0) if world > 1 else [None]
+    ranks = [KeyMerge(rows_per_rank, fraction, rank=r, world=world, device=0, transport=ts[r], parts=parts)
+             for r in range(world)]
+    for km in ranks:
+        km.generate()
+    loop = TaskLoop(MonotonicClock())
+
+    async def main():
+        return await gather(*(km.run_global() for km in ranks))
+
+    try:
+        results = loop.run_until_complete(main())
+    finally:
+        if world > 1:
+            close_all(ts)
+    assert all(r == results[0] for r in results)
+    return ranks, results[0]
+
+
+@pytest.mark.parametrize("rows,fraction", [(100_000, 0.3), (100_000, 0.0), (100_000, 1.0), (1, 0.3), (0, 0.3),
+                                           (250_000, 0.5)])
+def test_single_gpu_digest_matches_oracle(rows, fraction):
+    _, got = run_world(rows, 1, fraction)
+    assert got == oracle.key_merge_c(rows, 1, fraction)
+
+
+def test_rows_match_pandas_multiset():
+    ranks, got = run_world(20_000, 1, 0.3, parts=64)
+    k, l, r = ranks[0].output_rows()
+    want = oracle.key_merge_pandas(20_000, 1, 0.3)
+    assert oracle.join_digest_np(k, l, r) == want == got
+    # and the exact multiset against the C oracle's materialised rows
+    lk, lv = oracle.gen_side_c(0, 20_000, 20_000, oracle.SEED_LEFT, 0)
+    rk, rv = oracle.gen_side_c(0, 20_000, 20_000, oracle.SEED_RIGHT, oracle.merge_band(20_000, 0.3))
+    _, (ok, ol, orr) = oracle.hash_join_c(lk, lv, rk, rv, want_rows=True)
+    assert sorted(zip(k.tolist(), l.tolist(), r.tolist())) == sorted(zip(ok.tolist(), ol.tolist(), orr.tolist()))
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_worker_count_independent_and_equal_to_oracle(world):
+    rows = 40_000
+    _, got = run_world(rows, world, 0.3)
+    assert got == oracle.key_merge_c(rows, world, 0.3)
+    _, one = run_world(rows * world, 1, 0.3)
+    assert one == got
+
+
+def test_skewed_partitions_use_multiple_build_chunks():
+    """Few partitions -> partitions far above the 12288-row table chunk: still exact."""
+    _, got = run_world(300_000, 1, 0.3, parts=4)
+    assert got == oracle.key_merge_c(300_000, 1, 0.3)
+
+
+def test_duplicate_heavy_keys():
+    """Many duplicates per key (tiny key space): multimap semantics and output regrowth."""
+    from paper_2101_08878_b200 import native
+    from paper_2101_08878_b200.harness.key_merge import KeyMerge
+    from paper_2101_08878_b200.loop import MonotonicClock, TaskLoop
+
+    n = 50_000
+    km = KeyMerge(n, 0.3, device=0)
+    rng = np.random.default_rng(9)
+    lk = rng.integers(0, 50, n).astype(np.int64)
+    rk = rng.integers(25, 75, n).astype(np.int64)
+    lv = np.arange(n, dtype=np.int64)
+    rv = np.arange(n, dtype=np.int64) + 10**9
+    for cols, k, v in ((km.inputs[0], lk, lv), (km.inputs[1], rk, rv)):
+        native.memcpy(cols.keys.ptr, k.ctypes.data, n * 8)
+        native.memcpy(cols.vals.ptr, v.ctypes.data, n * 8)
+    native.check(native.lib().m4d_device_sync(0))
+    got = TaskLoop(MonotonicClock()).run_until_complete(km.run())
+    want = oracle.hash_join_c(lk, lv, rk, rv)
+    assert got == want and got[0] > km.n  # the output buffer had to grow
+
+
+def test_large_config_properties():
+    """1e7 rows/side on one GPU: count near f*n, digest equal to the oracle."""
+    rows = 10_000_000
+    ranks, got = run_world(rows, 1, 0.3)
+    assert abs(got[0] / rows - 0.3) < 0.005
+    assert got == oracle.key_merge_c(rows, 1, 0.3)
+    assert ranks[0].received == [rows, rows]
