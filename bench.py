@@ -166,6 +166,15 @@ class Dist:
             self.dist.destroy_process_group()
 
 
+def open_transport(dist: "Dist", device: int):
+    """This rank's nvlink transport (session derived from the torchrun rendezvous)."""
+    from paper_2101_08878_b200.transport import TransportConfig, transport_init
+
+    t = transport_init(dist.world, dist.rank, TransportConfig(kind="nvlink", device=device, connect_timeout=60))
+    t.wait_ready()
+    return t
+
+
 def emit(line: dict) -> None:
     print(json.dumps(line), flush=True)
 
@@ -210,8 +219,14 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
     n, b = args.n, args.block
     device = dist.local_rank
     native.set_device(device)
-    ts = TransposeSum(n, b, rank=dist.rank, world=dist.world, device=device,
-                      exchange=dist.allgather_bytes).setup()
+    exchange = None
+    if dist.world > 1:
+        from paper_2101_08878_b200.harness.collectives import allgather_sync
+
+        transport = open_transport(dist, device)
+        tags = iter(range(920, 10**9))
+        exchange = lambda blob: allgather_sync(transport, blob, next(tags))  # noqa: E731
+    ts = TransposeSum(n, b, rank=dist.rank, world=dist.world, device=device, exchange=exchange).setup()
     stream = ts.stream
     e0, e1 = native.Event(), native.Event()
 
@@ -345,6 +360,173 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
     }
 
 
+# -- key_merge ------------------------------------------------------------------------------------
+
+
+def km_cpu_sample(rows: int, target_rows: int, min_seconds: float = 10.0) -> dict:
+    """Oracle (C restatement, 1 thread) joins of `rows` rows per side, repeated to >= min_seconds."""
+    import oracle
+
+    done, t0 = 0, time.perf_counter()
+    while True:
+        oracle.key_merge_c(rows, 1, 0.3)
+        done += 1
+        dt = time.perf_counter() - t0
+        if dt >= min_seconds:
+            break
+    per = dt / done
+    return {"seconds": dt, "runs": done, "rows": rows, "full_ms": per * target_rows / rows * 1e3}
+
+
+def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
+    from paper_2101_08878_b200 import native
+    from paper_2101_08878_b200.harness.key_merge import KeyMerge
+    from paper_2101_08878_b200.loop import MonotonicClock, TaskLoop
+
+    device = dist.local_rank
+    native.set_device(device)
+    transport = open_transport(dist, device) if dist.world > 1 else None
+    km = KeyMerge(args.rows, args.fraction, rank=dist.rank, world=dist.world, device=device, transport=transport)
+    km.generate()
+    loop = TaskLoop(MonotonicClock())
+    stream = km.stream
+    e0, e1 = native.Event(), native.Event()
+    for _ in range(args.warmup):
+        digest = loop.run_until_complete(km.run_global())
+    sampler = ClockSampler(device)
+    dist.barrier()
+    stream.synchronize()
+    sampler.start()
+    km.launches = 0
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        got = loop.run_until_complete(km.run_global())
+    e1.record(stream)
+    e1.synchronize()
+    wall = (time.perf_counter() - t0) * 1e3 / args.steps
+    step_ms = dist.max(max(wall, e0.elapsed_ms(e1) / args.steps))
+    dist.barrier()
+    clocks = sampler.stop()
+    if got != digest:
+        raise RuntimeError("merge digest changed between steps")
+    launches = km.launches
+
+    # per-phase device timing (partition / join) on this rank, one extra step
+    phase = {}
+    if dist.world == 1:
+        ev = [native.Event() for _ in range(4)]
+        ev[0].record(stream)
+        for side in range(2):
+            km._partition(km.inputs[side], km.n, 0, km.parts, km.parted[side], km.bounds[side])
+        ev[1].record(stream)
+        native.check(native.lib().m4d_hash_join(
+            km.parted[0].ptr, km.bounds[0].ptr, km.parted[1].ptr, km.bounds[1].ptr, km.parts, km.out[0].ptr,
+            km.out[1].ptr, km.out[2].ptr, km.out_capacity, km.result.ptr, stream.handle))
+        ev[2].record(stream)
+        ev[2].synchronize()
+        phase = {"partition_ms": ev[0].elapsed_ms(ev[1]), "join_ms": ev[1].elapsed_ms(ev[2])}
+
+    alg = km.algorithmic_bytes()
+    hbm_peak = float(peaks["hbm_gbs"])
+    t_hbm = alg["hbm"] / (hbm_peak * 1e9)
+    t_nvl = alg["nvlink"] / (NVLINK_PEER_GBS * 1e9)
+    t_meas = step_ms * 1e-3
+    if t_nvl > t_hbm:
+        roof = {"bound": "nvlink", "achieved": alg["nvlink"] / t_meas / 1e9, "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+                "peak_source": "measured peer copy, B200_PROFILING.md"}
+    else:
+        roof = {"bound": "hbm", "achieved": alg["hbm"] / t_meas / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "peak_source": peaks["_source"]}
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": args.traffic,
+                 "kernel": "whole merge step (partition + shuffle + join kernels)",
+                 "algorithmic_bytes_per_step": alg, "t_roof_ms": max(t_hbm, t_nvl) * 1e3, "phases": phase})
+
+    e2e = None
+    if not args.skip_e2e:
+        cols = [km.inputs[0].keys, km.inputs[0].vals, km.inputs[1].keys, km.inputs[1].vals]
+        nbytes = km.n * 8
+        host = [native.PinnedHostBuffer(max(1, nbytes)) for _ in cols]
+        for h, c in zip(host, cols):
+            native.memcpy(h.ptr, c.ptr, nbytes, stream)
+        stream.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 3))):
+            for h, c in zip(host, cols):
+                native.memcpy(c.ptr, h.ptr, nbytes, stream)
+            r = loop.run_until_complete(km.run_global())
+        e2e_ms = dist.max((time.perf_counter() - t0) * 1e3 / max(1, min(args.steps, 3)))
+        if r != digest:
+            raise RuntimeError("e2e merge digest differs")
+        e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(dist.sum(4 * nbytes)),
+               "d2h_bytes_per_step": int(dist.sum(32 + 8 * (2 * dist.world + 2)))}
+
+    cpu, parity = None, None
+    if dist.rank == 0:
+        import oracle
+
+        sample_rows = min(args.rows, 2_000_000)
+        small = KeyMerge(sample_rows, args.fraction, device=device)
+        small.generate()
+        got_small = TaskLoop(MonotonicClock()).run_until_complete(small.run())
+        want_small = oracle.key_merge_c(sample_rows, 1, args.fraction)
+        parity = {"sample_rows_per_side": sample_rows, "digest_equal": got_small == want_small,
+                  "full_rows_out": digest[0], "expected_fraction": args.fraction,
+                  "observed_fraction": digest[0] / max(1, args.rows * dist.world)}
+        if not args.skip_cpu:
+            c = km_cpu_sample(min(args.rows, 2_000_000), args.rows * dist.world, min(10.0, args.cpu_seconds))
+            cpu = {"value": c["full_ms"], "unit": "ms", "cores": 1, "kind": "port",
+                   "sample": f"oracle C hash join (1 thread), {c['rows']} rows/side x {c['runs']} runs in "
+                             f"{c['seconds']:.1f} s, extrapolated linearly to {args.rows * dist.world} rows/side"}
+    if dist.rank != 0:
+        return None
+    return {
+        "metric": f"merge wall time ({args.rows} rows/side/GPU, int64 key, fraction {args.fraction})",
+        "value": step_ms, "unit": "ms", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
+        "config": {"workload": "key_merge", "rows_per_side_per_gpu": args.rows, "fraction": args.fraction,
+                   "partitions": km.parts, "digest": list(digest),
+                   "l2": "inputs (3.2 GB per GPU) far larger than the 126 MB L2"},
+        "gpu_launches": launches, "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
+        "clocks": clocks, "wall_ms_per_step": wall,
+    }
+
+
+# -- p2p ---------------------------------------------------------------------------------------------
+
+
+def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
+    from paper_2101_08878_b200.harness import p2p
+
+    if dist.world != 2:
+        raise SystemExit("--workload p2p needs exactly 2 ranks (torchrun --nproc-per-node 2)")
+    device = dist.local_rank
+    t = open_transport(dist, device)
+    rows, n = [], 1
+    while n <= args.max_size:
+        p2p.verify_once(t, 1 - dist.rank, n, True)
+        lat = p2p.osu_latency(t, 1 - dist.rank, n, 1000 if n <= 65536 else 100, True)
+        bw = p2p.osu_bw(t, 1 - dist.rank, n, 64, 10 if n <= (1 << 20) else 4, True)
+        rows.append({"size": n, "osu_latency_us": lat, "osu_bw_GBps": bw})
+        n *= 4
+    t.close()
+    if dist.rank != 0:
+        return None
+    big = [r for r in rows if r["size"] >= (4 << 20)]  # north_star: >= 4 MB messages
+    best = max(big, key=lambda r: r["osu_bw_GBps"]) if big else rows[-1]
+    return {
+        "metric": "p2p GB/s (osu_bw, device frames, >= 4 MiB)", "value": best["osu_bw_GBps"], "unit": "GB/s",
+        "n_gpus": 2, "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
+        "config": {"workload": "p2p", "sizes": [r["size"] for r in rows], "window": 64},
+        "latency_1B_us": rows[0]["osu_latency_us"], "sweep": rows,
+        "roofline": {"bound": "nvlink", "achieved": best["osu_bw_GBps"], "peak": 900.0, "unit": "GB/s",
+                     "frac": best["osu_bw_GBps"] / 900.0, "traffic": None, "peak_source": "nominal NVLink 5"},
+    }
+
+
 def reference_transpose_sum(args) -> dict:
     threads = len(os.sched_getaffinity(0))
     per_step = []
@@ -377,6 +559,24 @@ def reference_transpose_sum(args) -> dict:
     }
 
 
+def reference_key_merge(args) -> dict:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    per = [km_cpu_sample(min(args.rows, 2_000_000), args.rows * world, max(2.0, args.cpu_seconds / max(1, args.steps)))
+           for _ in range(args.steps)]
+    value = statistics.mean(p["full_ms"] for p in per)
+    return {
+        "impl": "reference",
+        "metric": f"merge wall time ({args.rows} rows/side/GPU, int64 key, fraction {args.fraction})",
+        "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
+        "config": {"workload": "key_merge", "rows_per_side_per_gpu": args.rows, "fraction": args.fraction},
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": 1, "kind": "port",
+                         "sample": f"oracle C hash join, {per[0]['rows']} rows/side per step, extrapolated"},
+        "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
 # -- main -------------------------------------------------------------------------------------------
 
 
@@ -386,7 +586,10 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["transpose_sum"], default="transpose_sum")
+    ap.add_argument("--workload", choices=["transpose_sum", "key_merge", "p2p"], default="transpose_sum")
+    ap.add_argument("--rows", type=int, default=100_000_000, help="key_merge rows per side per GPU")
+    ap.add_argument("--fraction", type=float, default=0.3)
+    ap.add_argument("--max-size", type=int, default=64 << 20, help="p2p largest message")
     ap.add_argument("--n", type=int, default=40000)
     ap.add_argument("--block", type=int, default=2000)
     ap.add_argument("--cpu-pairs", type=int, default=48, help="output blocks in the CPU baseline sample")
@@ -403,13 +606,20 @@ def main(argv=None) -> int:
     if args.impl == "reference":
         if int(os.environ.get("RANK", "0")) != 0:
             return 0
-        emit(reference_transpose_sum(args))
+        if args.workload == "transpose_sum":
+            emit(reference_transpose_sum(args))
+        elif args.workload == "key_merge":
+            emit(reference_key_merge(args))
+        else:
+            emit({"impl": "reference", "unavailable": "p2p reference arm needs the reference SocketTransport, "
+                                                      "which is not installed on the GPU box"})
         return 0
 
     dist = Dist()
     peaks = load_peaks()
+    runner = {"transpose_sum": bench_transpose_sum, "key_merge": bench_key_merge, "p2p": bench_p2p}[args.workload]
     try:
-        line = bench_transpose_sum(args, dist, peaks)
+        line = runner(args, dist, peaks)
     finally:
         dist.close()
     if line is not None:

@@ -222,23 +222,26 @@ m4d_status m4d_merge_generate(int64_t* keys, int64_t* vals, int64_t row0, int64_
                               uint64_t total, uint64_t seed, uint64_t band, void* stream);
 /* Device scratch m4d_partition needs for n rows and `buckets` buckets. */
 size_t m4d_partition_scratch_bytes(int64_t n, int buckets);
-/* Hash partition of one SoA table (keys, vals) into `buckets` buckets, written
- * bucket-major to (out_keys, out_vals); bounds[buckets + 1] (device) receives
- * the bucket start offsets.  The hash shuffle of SPEC.md:425. */
+/* Hash partition of one table into `buckets` buckets, written bucket-major as
+ * 16-byte (key, payload) pairs to out_pairs[2n]; bounds[buckets + 1] (device)
+ * receives the bucket start rows.  Input: SoA columns (keys, vals), or pairs
+ * (keys = pairs, vals = NULL).  n < 2^32.  The hash shuffle of SPEC.md:425.
+ * LOCAL with more than 512 buckets (power of two, <= 32768) runs as two
+ * L2-friendly scatter passes; RANK allows up to 16384 buckets. */
 m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
-                         int64_t* out_keys, int64_t* out_vals, int64_t* bounds, void* scratch,
-                         size_t scratch_bytes, void* stream);
-int m4d_partition_launches(void);
-/* Inner join of partitioned build (left) and probe (right) tables, partition
- * by partition (bounds from m4d_partition, same bucket count).  Writes at most
+                         int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
+                         void* stream);
+/* Kernel launches (plus memsets) one m4d_partition call issues for that bucket count. */
+int m4d_partition_launches(int buckets);
+/* Inner join of partitioned build (left) and probe (right) pair arrays,
+ * partition by partition (bounds from m4d_partition, same bucket count).  Writes at most
  * `capacity` rows (key, lval, rval) and result[4] (device) =
  * {rows produced, rows, sum of row hashes, sum of keys} (mod 2^64); a row
  * count above `capacity` means the output was cut: retry with a larger
  * buffer. */
-m4d_status m4d_hash_join(const int64_t* lkeys, const int64_t* lvals, const int64_t* lbounds,
-                         const int64_t* rkeys, const int64_t* rvals, const int64_t* rbounds, int parts,
-                         int64_t* out_keys, int64_t* out_lvals, int64_t* out_rvals, int64_t capacity,
-                         unsigned long long* result, void* stream);
+m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const int64_t* rpairs,
+                         const int64_t* rbounds, int parts, int64_t* out_keys, int64_t* out_lvals,
+                         int64_t* out_rvals, int64_t capacity, unsigned long long* result, void* stream);
 
 #ifdef __cplusplus
 }

@@ -11,16 +11,19 @@
 //
 // Partition (K5) is histogram -> exclusive scan -> scatter with per-(bucket,
 // CTA) offsets: every CTA owns one contiguous run of rows, so the output is
-// bucket-major with one contiguous sub-run per CTA.  With <= 8192 buckets the
-// L2 (126 MB) holds the whole write frontier, so the scattered 8-byte stores
-// reach DRAM as full sectors.
+// bucket-major with one contiguous sub-run per CTA.  Partitioned rows are
+// written as 16-byte (key, payload) pairs, one store per row: with at most
+// 2 x 148 resident CTAs the write frontier (CTAs x buckets x one 32-byte
+// sector) stays inside the 126 MB L2 even at 16384 buckets, so the scattered
+// stores leave L2 as full sectors instead of DRAM read-modify-writes.
 //
 // Join (K7): one CTA per partition builds an open-addressing table (keys +
 // build row index, 16384 slots, 192 KB of shared memory) over chunks of at
-// most 12288 build rows and streams the partition's probe rows through it;
-// matches are emitted with warp-aggregated output reservations and folded into
-// an order-independent digest (K8: row count, sum of row hashes, sum of keys,
-// all mod 2^64) in the same pass.
+// most 12288 build rows and streams the partition's probe rows through it
+// twice: a counting walk (block scan -> one output reservation per CTA), then
+// an emitting walk that writes (key, lval, rval) rows and folds them into an
+// order-independent digest (K8: row count, sum of row hashes, sum of keys,
+// all mod 2^64, reduced per CTA before one atomic each).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -30,9 +33,12 @@
 namespace {
 
 constexpr int kHistThreads = 512;
-constexpr int kMaxBuckets = 16384;
-constexpr int kJoinThreads = 1024;
-constexpr int kSlots = 16384;
+constexpr int kRowsPerThread = 8;        // rows each thread loads before using any (memory-level parallelism)
+constexpr int kMaxBuckets = 16384;       // single-pass partition limit (shared-memory counters)
+constexpr int kMaxParts = 1 << 15;       // two-pass LOCAL partition limit (128 KB of counters)
+constexpr int kSinglePassMax = 512;      // above this the scatter's L2 write frontier overflows
+constexpr int kJoinThreads = 512;
+constexpr int kSlots = 8192;
 constexpr int kChunk = kSlots * 3 / 4;
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr size_t kJoinSmem = kSlots * (sizeof(int64_t) + sizeof(uint32_t));
@@ -59,16 +65,31 @@ __global__ void generate_kernel(int64_t* keys, int64_t* vals, int64_t row0, int6
     }
 }
 
+// Key of row i: SoA input (vals != null) or 16-byte (key, payload) pairs.
+__device__ __forceinline__ int64_t key_at(const int64_t* keys, const int64_t* vals, int64_t i) {
+    return vals ? __ldcs(keys + i) : __ldcs(keys + 2 * i);
+}
+
 // hist[b * ctas + cta] = rows of this CTA's run that fall in bucket b.
-__global__ void __launch_bounds__(kHistThreads) hist_kernel(const int64_t* __restrict__ keys, int64_t n,
+__global__ void __launch_bounds__(kHistThreads) hist_kernel(const int64_t* __restrict__ keys,
+                                                            const int64_t* __restrict__ vals, int64_t n,
                                                             int64_t run, int mode, int buckets, int log2b,
                                                             uint32_t* __restrict__ hist) {
     extern __shared__ uint32_t h[];
     for (int b = threadIdx.x; b < buckets; b += blockDim.x) h[b] = 0;
     __syncthreads();
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x)
-        atomicAdd(&h[bucket_of(__ldcs(keys + i), mode, buckets, log2b)], 1u);
+    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+        int64_t k[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {  // all loads first: kRowsPerThread in flight
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            k[u] = i < hi ? key_at(keys, vals, i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u)
+            if (base + u * blockDim.x + threadIdx.x < hi) atomicAdd(&h[bucket_of(k[u], mode, buckets, log2b)], 1u);
+    }
     __syncthreads();
     for (int b = threadIdx.x; b < buckets; b += blockDim.x) hist[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = h[b];
 }
@@ -152,19 +173,136 @@ __global__ void __launch_bounds__(kHistThreads) scatter_kernel(const int64_t* __
                                                                const int64_t* __restrict__ vals, int64_t n,
                                                                int64_t run, int mode, int buckets, int log2b,
                                                                const int64_t* __restrict__ offsets,
-                                                               int64_t* __restrict__ out_keys,
-                                                               int64_t* __restrict__ out_vals) {
-    extern __shared__ unsigned long long cursor[];
+                                                               longlong2* __restrict__ out) {
+    extern __shared__ uint32_t cursor[];  // row positions fit 32 bits (n < 2^32, checked by the host)
     for (int b = threadIdx.x; b < buckets; b += blockDim.x)
-        cursor[b] = static_cast<unsigned long long>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]);
+        cursor[b] = static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]);
     __syncthreads();
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
-    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const int64_t k = __ldcs(keys + i);
-        const int64_t v = __ldcs(vals + i);
-        const unsigned long long pos = atomicAdd(&cursor[bucket_of(k, mode, buckets, log2b)], 1ull);
-        out_keys[pos] = k;
-        out_vals[pos] = v;
+    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+        longlong2 row[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            if (i < hi) {
+                if (vals) {
+                    row[u].x = __ldcs(keys + i);
+                    row[u].y = __ldcs(vals + i);
+                } else {
+                    row[u] = __ldcs(reinterpret_cast<const longlong2*>(keys) + i);
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u)
+            if (base + u * blockDim.x + threadIdx.x < hi)
+                out[atomicAdd(&cursor[bucket_of(row[u].x, mode, buckets, log2b)], 1u)] = row[u];
+    }
+}
+
+// ---- two-pass LOCAL partition (buckets > kSinglePassMax) -------------------------------
+// Pass 1 groups rows by the top b1 bits of the partition id into a scratch
+// pair array; pass 2 (one CTA per pass-1 segment) splits every segment by
+// the low b2 bits straight into its final place.  One histogram of the full
+// id (per CTA: counts by top bits for pass 1; summed globally: the final
+// bounds) serves both passes, so no second histogram read is needed.  Both
+// passes keep their write frontier (CTAs x fan-out x 32 B) inside L2.
+
+__global__ void __launch_bounds__(kHistThreads) hist2_kernel(const int64_t* __restrict__ keys,
+                                                             const int64_t* __restrict__ vals, int64_t n,
+                                                             int64_t run, int log2b, int b1,
+                                                             uint32_t* __restrict__ hist_top,
+                                                             unsigned long long* __restrict__ hist_all) {
+    extern __shared__ uint32_t h[];  // 2^log2b counters
+    const int buckets = 1 << log2b;
+    for (int b = threadIdx.x; b < buckets; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
+    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+        int64_t k[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            k[u] = i < hi ? key_at(keys, vals, i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u)
+            if (base + u * blockDim.x + threadIdx.x < hi)
+                atomicAdd(&h[bucket_of(k[u], M4D_PART_LOCAL, buckets, log2b)], 1u);
+    }
+    __syncthreads();
+    const int sub = 1 << (log2b - b1);
+    for (int b = threadIdx.x; b < buckets; b += blockDim.x)
+        if (h[b]) atomicAdd(hist_all + b, static_cast<unsigned long long>(h[b]));
+    for (int t = threadIdx.x; t < (1 << b1); t += blockDim.x) {
+        uint32_t c = 0;
+        for (int k = 0; k < sub; ++k) c += h[t * sub + k];
+        hist_top[static_cast<int64_t>(t) * gridDim.x + blockIdx.x] = c;
+    }
+}
+
+__global__ void exclusive_scan_u64_kernel(const unsigned long long* __restrict__ v, int n, int64_t* __restrict__ out,
+                                          int64_t total) {
+    // one CTA of 1024 threads; n <= 65536
+    __shared__ int64_t warp_tot[32];
+    const int per = (n + 1023) / 1024;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    int64_t local = 0;
+    for (int k = 0; k < per; ++k) {
+        const int i = t * per + k;
+        if (i < n) local += static_cast<int64_t>(v[i]);
+    }
+    int64_t incl = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) warp_tot[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int64_t w = warp_tot[lane], wi = w;
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        warp_tot[lane] = wi - w;
+    }
+    __syncthreads();
+    int64_t run = warp_tot[warp] + incl - local;
+    for (int k = 0; k < per; ++k) {
+        const int i = t * per + k;
+        if (i < n) {
+            out[i] = run;
+            run += static_cast<int64_t>(v[i]);
+        }
+    }
+    if (t == 0) out[n] = total;
+}
+
+__global__ void __launch_bounds__(1024) scatter_pass2_kernel(const longlong2* __restrict__ in,
+                                                             const int64_t* __restrict__ bounds, int log2b, int b1,
+                                                             longlong2* __restrict__ out) {
+    extern __shared__ uint32_t cursor[];  // 2^(log2b - b1)
+    const int sub = 1 << (log2b - b1);
+    const int seg = blockIdx.x;
+    for (int k = threadIdx.x; k < sub; k += blockDim.x) cursor[k] = static_cast<uint32_t>(bounds[seg * sub + k]);
+    __syncthreads();
+    const int64_t lo = bounds[seg * sub], hi = bounds[(seg + 1) * sub];
+    const uint32_t mask = sub - 1;
+    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+        longlong2 row[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            if (i < hi) row[u] = __ldcs(in + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            if (base + u * blockDim.x + threadIdx.x >= hi) continue;
+            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(row[u].x));
+            const uint32_t b2 = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) & mask;
+            out[atomicAdd(&cursor[b2], 1u)] = row[u];
+        }
     }
 }
 
@@ -174,92 +312,114 @@ __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int bu
         bounds[b] = b < buckets ? offsets[static_cast<int64_t>(b) * ctas] : total;
 }
 
-__device__ __forceinline__ void warp_emit(bool has, int64_t key, int64_t lval, int64_t rval,
-                                          unsigned long long* cursor, int64_t capacity, int64_t* ok,
-                                          int64_t* ol, int64_t* orr, int lane) {
-    const unsigned mask = __ballot_sync(0xffffffffu, has);
-    if (!mask) return;
-    unsigned long long base = 0;
-    const int leader = __ffs(mask) - 1;
-    if (lane == leader) base = atomicAdd(cursor, static_cast<unsigned long long>(__popc(mask)));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (has) {
-        const unsigned long long pos = base + __popc(mask & ((1u << lane) - 1));
-        if (static_cast<int64_t>(pos) < capacity) {
-            ok[pos] = key;
-            ol[pos] = lval;
-            orr[pos] = rval;
-        }
-    }
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* red) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+    return t;
 }
 
-__global__ void __launch_bounds__(kJoinThreads, 1)
-    join_kernel(const int64_t* __restrict__ lk, const int64_t* __restrict__ lv, const int64_t* __restrict__ loff,
-                const int64_t* __restrict__ rk, const int64_t* __restrict__ rv, const int64_t* __restrict__ roff,
-                int64_t* __restrict__ ok, int64_t* __restrict__ ol, int64_t* __restrict__ orr, int64_t capacity,
+__global__ void __launch_bounds__(kJoinThreads, 2)
+    join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
+                const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
+                int64_t* __restrict__ ol, int64_t* __restrict__ orr, int64_t capacity,
                 unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ digest) {
     extern __shared__ unsigned char smem[];
     int64_t* tkey = reinterpret_cast<int64_t*>(smem);
     uint32_t* tidx = reinterpret_cast<uint32_t*>(smem + kSlots * sizeof(int64_t));
+    __shared__ unsigned long long red[kJoinThreads / 32];
+    __shared__ unsigned long long block_base;
     const int part = blockIdx.x;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t b0 = loff[part], b1 = loff[part + 1];
     const int64_t p0 = roff[part], p1 = roff[part + 1];
+    constexpr int kPer = kRowsPerThread;
     unsigned long long cnt = 0, hsum = 0, ksum = 0;
     for (int64_t c0 = b0; c0 < b1; c0 += kChunk) {
         const int64_t c1 = c0 + kChunk < b1 ? c0 + kChunk : b1;
         for (int s = threadIdx.x; s < kSlots; s += blockDim.x) tidx[s] = kEmpty;
         __syncthreads();
-        for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
-            const int64_t k = lk[i];
-            uint32_t s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(k))) & (kSlots - 1);
-            while (atomicCAS(&tidx[s], kEmpty, static_cast<uint32_t>(i - c0)) != kEmpty) s = (s + 1) & (kSlots - 1);
-            tkey[s] = k;
+        for (int64_t base = c0; base < c1; base += static_cast<int64_t>(blockDim.x) * kPer) {
+            int64_t k[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int64_t i = base + u * blockDim.x + threadIdx.x;
+                k[u] = i < c1 ? build[i].x : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int64_t i = base + u * blockDim.x + threadIdx.x;
+                if (i >= c1) continue;
+                uint32_t s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(k[u]))) & (kSlots - 1);
+                while (atomicCAS(&tidx[s], kEmpty, static_cast<uint32_t>(i - c0)) != kEmpty) s = (s + 1) & (kSlots - 1);
+                tkey[s] = k[u];
+            }
         }
         __syncthreads();
-        // probe: the loop trip count is uniform per warp so the emits stay converged
-        for (int64_t base = p0; base < p1; base += blockDim.x) {
-            const int64_t j = base + threadIdx.x;
-            const bool live = j < p1;
-            int64_t k = 0, r = 0;
-            uint32_t s = 0;
-            if (live) {
-                k = rk[j];
-                r = rv[j];
-                s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(k))) & (kSlots - 1);
+        // probe rows kPer per thread at a time; the trip count is uniform over the block
+        for (int64_t base = p0; base < p1; base += static_cast<int64_t>(blockDim.x) * kPer) {
+            longlong2 r[kPer];
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                const int64_t j = base + u * blockDim.x + threadIdx.x;
+                if (j < p1) r[u] = probe[j];
             }
-            bool walking = live;
-            while (__any_sync(0xffffffffu, walking)) {
-                bool hit = false;
-                int64_t l = 0;
-                if (walking) {
-                    const uint32_t idx = tidx[s];
-                    if (idx == kEmpty) {
-                        walking = false;
-                    } else {
-                        if (tkey[s] == k) {
-                            hit = true;
-                            l = lv[c0 + idx];
-                        }
-                        s = (s + 1) & (kSlots - 1);
+            unsigned long long mine = 0;  // pass 1: count
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {
+                if (base + u * blockDim.x + threadIdx.x >= p1) continue;
+                for (uint32_t s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(r[u].x))) & (kSlots - 1);
+                     tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1))
+                    mine += tkey[s] == r[u].x;
+            }
+            unsigned long long incl = mine;
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) red[warp] = incl;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                unsigned long long run = 0;
+                for (int w = 0; w < kJoinThreads / 32; ++w) {
+                    const unsigned long long t = red[w];
+                    red[w] = run;
+                    run += t;
+                }
+                block_base = run ? atomicAdd(cursor, run) : 0;
+            }
+            __syncthreads();
+            unsigned long long pos = block_base + red[warp] + incl - mine;
+            __syncthreads();  // red / block_base are reused by the next probe batch
+#pragma unroll
+            for (int u = 0; u < kPer; ++u) {  // pass 2: emit
+                if (base + u * blockDim.x + threadIdx.x >= p1) continue;
+                const longlong2 pr = r[u];
+                for (uint32_t s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(pr.x))) & (kSlots - 1);
+                     tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1)) {
+                    if (tkey[s] != pr.x) continue;
+                    const int64_t l = build[c0 + tidx[s]].y;
+                    if (static_cast<int64_t>(pos) < capacity) {
+                        ok[pos] = pr.x;
+                        ol[pos] = l;
+                        orr[pos] = pr.y;
                     }
-                }
-                if (hit) {
+                    ++pos;
                     ++cnt;
-                    hsum += row_hash(k, l, r);
-                    ksum += static_cast<unsigned long long>(k);
+                    hsum += row_hash(pr.x, l, pr.y);
+                    ksum += static_cast<unsigned long long>(pr.x);
                 }
-                warp_emit(hit, k, l, r, cursor, capacity, ok, ol, orr, lane);
             }
         }
         __syncthreads();
     }
-    for (int o = 16; o; o >>= 1) {
-        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
-        ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
-    }
-    if (lane == 0 && cnt) {
+    cnt = block_sum(cnt, red);
+    hsum = block_sum(hsum, red);
+    ksum = block_sum(ksum, red);
+    if (threadIdx.x == 0 && cnt) {
         atomicAdd(digest + 0, cnt);
         atomicAdd(digest + 1, hsum);
         atomicAdd(digest + 2, ksum);
@@ -290,31 +450,72 @@ m4d_status m4d_merge_generate(int64_t* keys, int64_t* vals, int64_t row0, int64_
 }
 
 static int partition_ctas(int64_t n) {
-    const int64_t per = 65536;  // rows per CTA run (>= 64 rows per bucket at 1024 buckets)
+    // <= 2 resident CTAs per SM: the scatter's L2 write frontier must fit (see top).
+    const int64_t per = 65536;
     int64_t c = (n + per - 1) / per;
     if (c < 1) c = 1;
-    if (c > 148 * 8) c = 148 * 8;
+    if (c > 148 * 2) c = 148 * 2;
     return static_cast<int>(c);
 }
 
+static int pass1_bits(int log2b) { return log2b > 8 ? 8 : log2b; }
+
 size_t m4d_partition_scratch_bytes(int64_t n, int buckets) {
     const int64_t ctas = partition_ctas(n);
-    const int64_t entries = ctas * buckets;
+    const int64_t fan = buckets > kSinglePassMax ? (int64_t(1) << pass1_bits(log2_exact(buckets) < 0 ? 14 : log2_exact(buckets))) : buckets;
+    const int64_t entries = ctas * fan;
     const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
-    return entries * sizeof(uint32_t) + entries * sizeof(int64_t) + (tiles + 1) * sizeof(int64_t) + 256;
+    size_t bytes = entries * sizeof(uint32_t) + entries * sizeof(int64_t) + (tiles + 1) * sizeof(int64_t) + 512;
+    if (buckets > kSinglePassMax)  // global histogram + pass-1 pairs
+        bytes += buckets * sizeof(unsigned long long) + 256 + static_cast<size_t>(n) * 16 + 256;
+    return bytes;
 }
 
 m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
-                         int64_t* out_keys, int64_t* out_vals, int64_t* bounds, void* scratch,
-                         size_t scratch_bytes, void* stream) {
-    if (n < 0 || buckets < 1 || buckets > kMaxBuckets) return fail(M4D_ERR_USAGE, "bucket count %d outside [1, %d]", buckets, kMaxBuckets);
+                         int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes, void* stream) {
+    if (n < 0 || n >= (int64_t(1) << 32)) return fail(M4D_ERR_USAGE, "partition of %lld rows outside [0, 2^32)", (long long)n);
     const int log2b = log2_exact(buckets);
+    const bool two_pass = mode == M4D_PART_LOCAL && buckets > kSinglePassMax;
+    if (n < 0 || buckets < 1 || buckets > (mode == M4D_PART_LOCAL ? kMaxParts : kMaxBuckets))
+        return fail(M4D_ERR_USAGE, "bucket count %d outside the supported range", buckets);
     if (mode == M4D_PART_LOCAL && log2b < 0) return fail(M4D_ERR_USAGE, "local partition count must be a power of two");
     if (mode != M4D_PART_LOCAL && mode != M4D_PART_RANK) return fail(M4D_ERR_USAGE, "unknown partition mode %d", mode);
     if (scratch_bytes < m4d_partition_scratch_bytes(n, buckets)) return fail(M4D_ERR_USAGE, "partition scratch too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int ctas = partition_ctas(n);
     const int64_t run = (n + ctas - 1) / ctas;
+    if (two_pass) {
+        const int b1 = pass1_bits(log2b);
+        const int fan = 1 << b1;
+        const int64_t entries = static_cast<int64_t>(ctas) * fan;
+        const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
+        char* base = static_cast<char*>(scratch);
+        uint32_t* hist = reinterpret_cast<uint32_t*>(base);
+        base += (entries * sizeof(uint32_t) + 255) & ~size_t(255);
+        int64_t* offs = reinterpret_cast<int64_t*>(base);
+        int64_t* tile_sums = offs + entries;
+        int64_t* total = tile_sums + tiles;
+        base += ((entries + tiles + 1) * sizeof(int64_t) + 255) & ~size_t(255);
+        unsigned long long* hist_all = reinterpret_cast<unsigned long long*>(base);
+        base += (buckets * sizeof(unsigned long long) + 255) & ~size_t(255);
+        longlong2* tmp = reinterpret_cast<longlong2*>(base);
+        M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 4));
+        M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
+        M4D_CUDA_TRY(cudaMemsetAsync(hist_all, 0, buckets * sizeof(unsigned long long), s));
+        hist2_kernel<<<ctas, kHistThreads, buckets * sizeof(uint32_t), s>>>(keys, vals, n, run, log2b, b1, hist, hist_all);
+        scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
+        scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
+        scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
+        // pass 1: by the top b1 bits of the partition id (mode LOCAL with 2^b1 buckets == those bits)
+        scatter_kernel<<<ctas, kHistThreads, fan * sizeof(uint32_t), s>>>(keys, vals, n, run, M4D_PART_LOCAL, fan, b1,
+                                                                           offs, tmp);
+        exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
+        scatter_pass2_kernel<<<fan, 1024, (buckets >> b1) * sizeof(uint32_t), s>>>(
+            tmp, bounds, log2b, b1, reinterpret_cast<longlong2*>(out_pairs));
+        M4D_CUDA_TRY(cudaGetLastError());
+        return M4D_OK;
+    }
+    if (buckets > kMaxBuckets) return fail(M4D_ERR_USAGE, "bucket count %d above the single-pass limit", buckets);
     const int64_t entries = static_cast<int64_t>(ctas) * buckets;
     const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
     uint32_t* hist = static_cast<uint32_t*>(scratch);
@@ -322,34 +523,36 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
     int64_t* tile_sums = offs + entries;
     int64_t* total = tile_sums + tiles;
     const size_t hist_smem = buckets * sizeof(uint32_t);
-    const size_t cur_smem = buckets * sizeof(unsigned long long);
+    const size_t cur_smem = buckets * sizeof(uint32_t);
     // (per device; cheap enough to repeat on every call)
     M4D_CUDA_TRY(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
-    M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 8));
-    hist_kernel<<<ctas, kHistThreads, hist_smem, s>>>(keys, n, run, mode, buckets, log2b, hist);
+    M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
+    hist_kernel<<<ctas, kHistThreads, hist_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, hist);
     scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
     scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
     scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
-    scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs, out_keys, out_vals);
+    scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+                                                        reinterpret_cast<longlong2*>(out_pairs));
     bucket_bounds_kernel<<<(buckets + 256) / 256, 256, 0, s>>>(offs, buckets, ctas, n, bounds);
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }
 
-int m4d_partition_launches(void) { return 6; }
+int m4d_partition_launches(int buckets) { return buckets > kSinglePassMax ? 8 : 6; }
 
-m4d_status m4d_hash_join(const int64_t* lkeys, const int64_t* lvals, const int64_t* lbounds, const int64_t* rkeys,
-                         const int64_t* rvals, const int64_t* rbounds, int parts, int64_t* out_keys,
-                         int64_t* out_lvals, int64_t* out_rvals, int64_t capacity, unsigned long long* result,
-                         void* stream) {
+m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const int64_t* rpairs,
+                         const int64_t* rbounds, int parts, int64_t* out_keys, int64_t* out_lvals,
+                         int64_t* out_rvals, int64_t capacity, unsigned long long* result, void* stream) {
     if (parts < 0) return fail(M4D_ERR_USAGE, "negative partition count");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     M4D_CUDA_TRY(cudaFuncSetAttribute(join_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kJoinSmem)));
     // result = {cursor, count, hash_sum, key_sum}
     M4D_CUDA_TRY(cudaMemsetAsync(result, 0, 4 * sizeof(unsigned long long), s));
     if (parts)
-        join_kernel<<<parts, kJoinThreads, kJoinSmem, s>>>(lkeys, lvals, lbounds, rkeys, rvals, rbounds, out_keys,
-                                                           out_lvals, out_rvals, capacity, result, result + 1);
+        join_kernel<<<parts, kJoinThreads, kJoinSmem, s>>>(reinterpret_cast<const longlong2*>(lpairs), lbounds,
+                                                           reinterpret_cast<const longlong2*>(rpairs), rbounds,
+                                                           out_keys, out_lvals, out_rvals, capacity, result,
+                                                           result + 1);
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }

@@ -694,6 +694,7 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
         return M4D_OK;
     }
     if (!block_sums) return fail(M4D_ERR_USAGE, "block_sums must not be NULL");
+    M4D_CUDA_TRY(cudaSetDevice(plan->device));  // the stream belongs to the plan's device
     TsParams p;
     p.tasks = plan->d_tasks;
     p.refs = plan->d_refs;

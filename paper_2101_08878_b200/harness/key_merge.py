@@ -35,6 +35,7 @@ import struct
 from .. import native
 from ..errors import CommShimError, UsageError
 from ..messaging import await_request
+from .collectives import allgather
 from ..transport import MemoryDomain
 
 SEED_LEFT = 0x4C454654
@@ -50,14 +51,15 @@ def merge_band(total: int, fraction: float) -> int:
 
 
 def choose_parts(rows: int) -> int:
+    """Power-of-two partition count with ~3K rows per partition (8192-slot shared tables)."""
     parts = 1
-    while parts < 16384 and rows / parts > 6000:
+    while parts < 32768 and rows / parts > 3000:
         parts *= 2
     return parts
 
 
 class _Columns:
-    """keys + vals device columns of one table (capacity rows)."""
+    """keys + vals device columns of one table (capacity rows): the user-facing SoA layout."""
 
     def __init__(self, device: int, capacity: int):
         self.capacity = max(1, int(capacity))
@@ -65,21 +67,13 @@ class _Columns:
         self.vals = native.DeviceBuffer(device, self.capacity * 8)
 
 
-async def allgather(transport, payload: bytes, tag: int = EXCHANGE_TAG) -> list[bytes]:
-    """Every rank's ``payload`` (same length everywhere) over the world channel."""
-    world, me = transport.world_size, transport.rank
-    out = [b""] * world
-    out[me] = payload
-    if world == 1:
-        return out
-    bufs = {p: bytearray(len(payload)) for p in range(world) if p != me}
-    reqs = [transport.post_recv(0, p, tag, bufs[p]) for p in bufs]
-    reqs += [transport.post_send(0, p, tag, payload) for p in bufs]
-    for r in reqs:
-        await await_request(transport, r)
-    for p, b in bufs.items():
-        out[p] = bytes(b)
-    return out
+class _Pairs:
+    """(key, payload) 16-byte pairs: the internal layout of partitioned / shuffled rows."""
+
+    def __init__(self, device: int, capacity: int):
+        self.capacity = max(1, int(capacity))
+        self.buf = native.DeviceBuffer(device, self.capacity * 16)
+        self.ptr = self.buf.ptr
 
 
 class KeyMerge:
@@ -104,9 +98,9 @@ class KeyMerge:
         self.parts = parts or choose_parts(self.n)
         slack = self.n + int(6 * math.sqrt(max(self.n, 1))) + 4096
         self.inputs = [_Columns(device, self.n), _Columns(device, self.n)]
-        self.sendbuf = [_Columns(device, self.n), _Columns(device, self.n)] if world > 1 else None
-        self.recv = [_Columns(device, slack), _Columns(device, slack)] if world > 1 else None
-        self.parted = [_Columns(device, slack), _Columns(device, slack)]
+        self.sendbuf = [_Pairs(device, self.n), _Pairs(device, self.n)] if world > 1 else None
+        self.recv = [_Pairs(device, slack), _Pairs(device, slack)] if world > 1 else None
+        self.parted = [_Pairs(device, slack), _Pairs(device, slack)]
         self.bounds = [native.DeviceBuffer(device, (max(self.parts, world) + 1) * 8) for _ in range(2)]
         self.rank_bounds = [native.DeviceBuffer(device, (world + 1) * 8) for _ in range(2)]
         scratch = max(native.lib().m4d_partition_scratch_bytes(slack, self.parts),
@@ -132,11 +126,11 @@ class KeyMerge:
 
     # -- pipeline ---------------------------------------------------------------------------
 
-    def _partition(self, src: _Columns, n: int, mode: int, buckets: int, dst: _Columns, bounds) -> None:
-        native.check(native.lib().m4d_partition(src.keys.ptr, src.vals.ptr, n, mode, buckets, dst.keys.ptr,
-                                                dst.vals.ptr, bounds.ptr, self.scratch.ptr, self.scratch_bytes,
-                                                self.stream.handle))
-        self.launches += native.lib().m4d_partition_launches()
+    def _partition(self, src, n: int, mode: int, buckets: int, dst: _Pairs, bounds) -> None:
+        keys, vals = (src.keys.ptr, src.vals.ptr) if isinstance(src, _Columns) else (src.ptr, None)
+        native.check(native.lib().m4d_partition(keys, vals, n, mode, buckets, dst.ptr, bounds.ptr, self.scratch.ptr,
+                                                self.scratch_bytes, self.stream.handle))
+        self.launches += native.lib().m4d_partition_launches(buckets)
 
     def _read_bounds(self, buf, count: int) -> list[int]:
         raw = native.to_host(buf.ptr, (count + 1) * 8, self.stream)
@@ -153,39 +147,33 @@ class KeyMerge:
             sends.append(self._read_bounds(self.rank_bounds[side], P))
         counts = [[sends[s][d + 1] - sends[s][d] for d in range(P)] for s in range(2)]
         blob = struct.pack(f"<{2 * P}q", *counts[0], *counts[1])
-        table = [struct.unpack(f"<{2 * P}q", b) for b in await allgather(t, blob)]
+        table = [struct.unpack(f"<{2 * P}q", b) for b in await allgather(t, blob, EXCHANGE_TAG)]
         incoming = [[table[src][side * P + me] for src in range(P)] for side in range(2)]
         received = []
         reqs = []
         for side in range(2):
             total = sum(incoming[side])
             if total > self.recv[side].capacity:
-                self.recv[side] = _Columns(self.device, int(total * 1.1) + 4096)
+                self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096)
             if total > self.parted[side].capacity:
-                self.parted[side] = _Columns(self.device, int(total * 1.1) + 4096)
+                self.parted[side] = _Pairs(self.device, int(total * 1.1) + 4096)
             received.append(total)
             at = 0
-            for src in range(P):
+            for src in range(P):  # receive layout: source-major, each source's rows contiguous
                 rows = incoming[side][src]
-                for col in ("keys", "vals"):
-                    dst = getattr(self.recv[side], col).ptr + at * 8
-                    if src == me:
-                        lo = sends[side][me]
-                        native.memcpy(dst, getattr(self.sendbuf[side], col).ptr + lo * 8, rows * 8, self.stream)
-                    elif rows:
-                        tag = DATA_TAG + side * 2 + (col == "vals")
-                        view = DeviceView(dst, rows * 8, self.device)
-                        reqs.append(t.post_recv(0, src, tag, view, MemoryDomain.DEVICE))
+                dst = self.recv[side].ptr + at * 16
+                if src == me:
+                    native.memcpy(dst, self.sendbuf[side].ptr + sends[side][me] * 16, rows * 16, self.stream)
+                elif rows:
+                    view = DeviceView(dst, rows * 16, self.device)
+                    reqs.append(t.post_recv(0, src, DATA_TAG + side, view, MemoryDomain.DEVICE))
                 at += rows
             for dst_rank in range(P):
                 rows = counts[side][dst_rank]
                 if dst_rank == me or not rows:
                     continue
-                lo = sends[side][dst_rank]
-                for col in ("keys", "vals"):
-                    tag = DATA_TAG + side * 2 + (col == "vals")
-                    view = DeviceView(getattr(self.sendbuf[side], col).ptr + lo * 8, rows * 8, self.device)
-                    reqs.append(t.post_send(0, dst_rank, tag, view, MemoryDomain.DEVICE))
+                view = DeviceView(self.sendbuf[side].ptr + sends[side][dst_rank] * 16, rows * 16, self.device)
+                reqs.append(t.post_send(0, dst_rank, DATA_TAG + side, view, MemoryDomain.DEVICE))
         # the send buffers were written on self.stream: make them visible before peers pull
         self.stream.synchronize()
         for r in reqs:
@@ -204,8 +192,7 @@ class KeyMerge:
             self._partition(tables[side], self.received[side], 0, self.parts, self.parted[side], self.bounds[side])
         while True:
             native.check(native.lib().m4d_hash_join(
-                self.parted[0].keys.ptr, self.parted[0].vals.ptr, self.bounds[0].ptr,
-                self.parted[1].keys.ptr, self.parted[1].vals.ptr, self.bounds[1].ptr, self.parts,
+                self.parted[0].ptr, self.bounds[0].ptr, self.parted[1].ptr, self.bounds[1].ptr, self.parts,
                 self.out[0].ptr, self.out[1].ptr, self.out[2].ptr, self.out_capacity, self.result.ptr,
                 self.stream.handle))
             self.launches += 2

@@ -96,6 +96,7 @@ class TransposeSum:
     def generate(self) -> None:
         """Fill this rank's x blocks with the deterministic generator."""
         lib = native.lib()
+        native.set_device(self.device)
         for g in self.owned:
             i, j = divmod(g, self.nb)
             native.check(lib.m4d_fill_block_f64(self.x_ptr(g), self.n, i * self.b, j * self.b, self.b,
@@ -165,11 +166,12 @@ class TransposeSum:
     # -- step ------------------------------------------------------------------------------------
 
     def launch(self) -> None:
-        """Enqueue the fused kernel (one launch) on ``self.stream``."""
+        """Enqueue the fused kernel on ``self.stream``."""
         native.check(native.lib().m4d_ts_run(self._plan, self.sums.ptr,
                                              self.sums.ptr + len(self.owned) * 8, self.stream.handle))
 
     def read_block_sums(self) -> dict:
+        native.set_device(self.device)
         raw = native.to_host(self.sums.ptr, len(self.owned) * 8, self.stream)
         values = struct.unpack(f"<{len(self.owned)}d", raw)
         return dict(zip(self.owned, values))
@@ -194,6 +196,7 @@ class TransposeSum:
         return self.combine(self.read_block_sums())
 
     def read_y_block(self, g: int) -> bytes:
+        native.set_device(self.device)
         return native.to_host(self.y_ptr(g), self.block_bytes, self.stream)
 
     def close(self) -> None:

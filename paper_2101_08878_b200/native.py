@@ -144,10 +144,10 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_transport_close": (ctypes.c_int, [_c_void_p]),
     "m4d_merge_generate": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _i64, _u64, _u64, _u64, _c_void_p]),
     "m4d_partition_scratch_bytes": (_size, [_i64, ctypes.c_int]),
-    "m4d_partition": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p, _c_void_p,
+    "m4d_partition": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
                                      _c_void_p, _c_void_p, _size, _c_void_p]),
-    "m4d_partition_launches": (ctypes.c_int, []),
-    "m4d_hash_join": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int,
+    "m4d_partition_launches": (ctypes.c_int, [ctypes.c_int]),
+    "m4d_hash_join": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int,
                                      _c_void_p, _c_void_p, _c_void_p, _i64, _c_void_p, _c_void_p]),
     "m4d_fill_block_f64": (ctypes.c_int, [_c_void_p, _i64, _i64, _i64, _i64, _u64, _c_void_p]),
     "m4d_ts_plan_create": (

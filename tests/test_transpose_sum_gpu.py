@@ -148,3 +148,27 @@ def test_full_config_sampled_blocks(cuda):
     for r in ranks:
         again.update(r.read_block_sums())
     assert again == sums
+
+
+def test_two_gpus_partner_tiles_read_over_nvlink(cuda):
+    """Ranks on distinct B200s: the TMA producer reads peer HBM through NVLink."""
+    from paper_2101_08878_b200 import native
+    from paper_2101_08878_b200.harness.transpose_sum import TransposeSum
+
+    if native.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    n, b = 2048, 256
+    ranks = TransposeSum.local_world(n, b, 2, devices=[0, 1])
+    for r in ranks:
+        r.launch()
+    sums = {}
+    for r in ranks:
+        sums.update(r.read_block_sums())
+    want_sums, want = oracle.transpose_sum_checksum(n, b, threads=8)
+    assert abs(math.fsum(sums[g] for g in sorted(sums)) - want) <= REL_TOL * want
+    assert sum(r.tasks_single for r in ranks) > 0
+    for g in (1, 9, 17):
+        i, j = divmod(g, n // b)
+        a = oracle.gen_block_c(n, i * b, j * b, b)
+        bt = oracle.gen_block_c(n, j * b, i * b, b)
+        assert np.array_equal(y_block(ranks, g), oracle.transpose_block_c(a, bt))
