@@ -36,7 +36,7 @@ constexpr int kHistThreads = 512;
 constexpr int kRowsPerThread = 8;        // rows each thread loads before using any (memory-level parallelism)
 constexpr int kMaxBuckets = 16384;       // single-pass partition limit (shared-memory counters)
 constexpr int kMaxParts = 1 << 15;       // two-pass LOCAL partition limit (128 KB of counters)
-constexpr int kSinglePassMax = 512;      // above this the scatter's L2 write frontier overflows
+constexpr int kSinglePassMax = 256;      // LOCAL above this: two passes (L2 write frontier)
 constexpr int kJoinThreads = 512;
 constexpr int kSlots = 8192;
 constexpr int kChunk = kSlots * 3 / 4;
@@ -197,6 +197,123 @@ __global__ void __launch_bounds__(kHistThreads) scatter_kernel(const int64_t* __
         for (int u = 0; u < kRowsPerThread; ++u)
             if (base + u * blockDim.x + threadIdx.x < hi)
                 out[atomicAdd(&cursor[bucket_of(row[u].x, mode, buckets, log2b)], 1u)] = row[u];
+    }
+}
+
+// Tile-sorted scatter for <= 256 buckets.  Each CTA stages a tile of 4096
+// rows in shared memory ordered by bucket (warp-level multisplit with
+// __match_any_sync: no atomics with return), then copies each bucket's run
+// of the tile to its global position, so every global store belongs to a
+// contiguous run (about 16 rows = 256 B per bucket per tile) and DRAM sees
+// full sectors.  Rows keep their input order within a bucket (deterministic).
+constexpr int kTileRows = kHistThreads * kRowsPerThread;  // 4096
+constexpr int kTileBuckets = 256;
+constexpr size_t kTileSmem = kTileRows * sizeof(longlong2) + kTileRows + (kHistThreads / 32) * kTileBuckets * 2;
+
+__global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int64_t* __restrict__ keys,
+                                                                       const int64_t* __restrict__ vals, int64_t n,
+                                                                       int64_t run, int mode, int buckets, int log2b,
+                                                                       const int64_t* __restrict__ offsets,
+                                                                       longlong2* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char tsm[];
+    longlong2* stage = reinterpret_cast<longlong2*>(tsm);
+    uint8_t* sbucket = tsm + kTileRows * sizeof(longlong2);
+    uint16_t* wbase = reinterpret_cast<uint16_t*>(sbucket + kTileRows);  // [warps][256]
+    __shared__ uint32_t gcur[kTileBuckets];
+    __shared__ uint32_t tstart[kTileBuckets + 1];
+    __shared__ uint32_t scan_tmp[kTileBuckets / 32];
+    constexpr int kW = kHistThreads / 32;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned lower = (1u << lane) - 1u;
+    for (int b = threadIdx.x; b < kTileBuckets; b += blockDim.x)
+        gcur[b] = b < buckets ? static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]) : 0u;
+    const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
+    for (int64_t tile = lo; tile < hi; tile += kTileRows) {
+        // 1. load: warp w owns rows [tile + 256 w, tile + 256 w + 256)
+        longlong2 row[kRowsPerThread];
+        uint32_t bk[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = tile + w * 256 + u * 32 + lane;
+            if (i < hi) {
+                if (vals) {
+                    row[u].x = __ldcs(keys + i);
+                    row[u].y = __ldcs(vals + i);
+                } else {
+                    row[u] = __ldcs(reinterpret_cast<const longlong2*>(keys) + i);
+                }
+            }
+        }
+        for (int b = lane; b < kTileBuckets; b += 32) wbase[w * kTileBuckets + b] = 0;
+        __syncwarp();
+        // 2. warp multisplit: rank of each row among the warp's rows of its bucket
+        uint16_t off[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const bool live = tile + w * 256 + u * 32 + lane < hi;
+            bk[u] = live ? bucket_of(row[u].x, mode, buckets, log2b) : 0xffffffffu;
+            const unsigned peers = __match_any_sync(0xffffffffu, bk[u]);
+            const int leader = __ffs(peers) - 1;
+            uint32_t start = 0;
+            if (live && lane == leader) {
+                start = wbase[w * kTileBuckets + bk[u]];
+                wbase[w * kTileBuckets + bk[u]] = static_cast<uint16_t>(start + __popc(peers));
+            }
+            start = __shfl_sync(0xffffffffu, start, leader);
+            off[u] = static_cast<uint16_t>(start + __popc(peers & lower));
+            __syncwarp();
+        }
+        __syncthreads();
+        // 3. per-bucket tile totals, exclusive over buckets; warp bases within each bucket
+        uint32_t total = 0;
+        if (threadIdx.x < kTileBuckets) {
+            const int b = threadIdx.x;
+            for (int ww = 0; ww < kW; ++ww) {
+                const uint32_t c = wbase[ww * kTileBuckets + b];
+                wbase[ww * kTileBuckets + b] = static_cast<uint16_t>(total);
+                total += c;
+            }
+            uint32_t incl = total;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) scan_tmp[w] = incl;
+        }
+        __syncthreads();
+        if (threadIdx.x < kTileBuckets) {
+            const int b = threadIdx.x;
+            uint32_t before = 0;
+            for (int ww = 0; ww < w; ++ww) before += scan_tmp[ww];
+            uint32_t incl = total;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            tstart[b] = before + incl - total;
+            if (b == kTileBuckets - 1) tstart[kTileBuckets] = before + incl;
+            for (int ww = 0; ww < kW; ++ww)
+                wbase[ww * kTileBuckets + b] = static_cast<uint16_t>(wbase[ww * kTileBuckets + b] + tstart[b]);
+        }
+        __syncthreads();
+        // 4. stage rows in bucket order
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            if (bk[u] == 0xffffffffu) continue;
+            const uint32_t pos = wbase[w * kTileBuckets + bk[u]] + off[u];
+            stage[pos] = row[u];
+            sbucket[pos] = static_cast<uint8_t>(bk[u]);
+        }
+        __syncthreads();
+        // 5. copy each bucket's run to its global place
+        const uint32_t valid = tstart[kTileBuckets];
+        for (uint32_t r = threadIdx.x; r < valid; r += blockDim.x) {
+            const uint32_t b = sbucket[r];
+            out[gcur[b] + (r - tstart[b])] = stage[r];
+        }
+        __syncthreads();
+        if (threadIdx.x < kTileBuckets) gcur[threadIdx.x] += tstart[threadIdx.x + 1] - tstart[threadIdx.x];
+        __syncthreads();
     }
 }
 
@@ -507,8 +624,9 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
         scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
         // pass 1: by the top b1 bits of the partition id (mode LOCAL with 2^b1 buckets == those bits)
-        scatter_kernel<<<ctas, kHistThreads, fan * sizeof(uint32_t), s>>>(keys, vals, n, run, M4D_PART_LOCAL, fan, b1,
-                                                                           offs, tmp);
+        M4D_CUDA_TRY(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kTileSmem)));
+        tile_scatter_kernel<<<ctas, kHistThreads, kTileSmem, s>>>(keys, vals, n, run, M4D_PART_LOCAL, fan, b1, offs, tmp);
         exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
         scatter_pass2_kernel<<<fan, 1024, (buckets >> b1) * sizeof(uint32_t), s>>>(
             tmp, bounds, log2b, b1, reinterpret_cast<longlong2*>(out_pairs));
@@ -531,8 +649,15 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
     scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
     scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
     scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
-    scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
-                                                        reinterpret_cast<longlong2*>(out_pairs));
+    if (buckets <= kTileBuckets) {
+        M4D_CUDA_TRY(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kTileSmem)));
+        tile_scatter_kernel<<<ctas, kHistThreads, kTileSmem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+                                                                  reinterpret_cast<longlong2*>(out_pairs));
+    } else {
+        scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+                                                            reinterpret_cast<longlong2*>(out_pairs));
+    }
     bucket_bounds_kernel<<<(buckets + 256) / 256, 256, 0, s>>>(offs, buckets, ctas, n, bounds);
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
