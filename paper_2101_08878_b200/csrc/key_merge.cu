@@ -7,7 +7,7 @@
 // every placement decision, from disjoint bit ranges:
 //   owner rank      = mulhi32(h >> 32, P)                     (mode RANK)
 //   local partition = (h & 0xffffffff) >> (32 - log2 parts)   (mode PART)
-//   hash-table slot = h & (slots - 1)                          (join)
+//   hash-table slot = 13-bit multiplicative hash of the folded key (join)
 //
 // Partition (K5) is histogram -> exclusive scan -> scatter with per-(bucket,
 // CTA) offsets: every CTA owns one contiguous run of rows, so the output is
@@ -37,16 +37,26 @@ constexpr int kRowsPerThread = 8;        // rows each thread loads before using 
 constexpr int kMaxBuckets = 16384;       // single-pass partition limit (shared-memory counters)
 constexpr int kMaxParts = 1 << 15;       // two-pass LOCAL partition limit (128 KB of counters)
 constexpr int kSinglePassMax = 256;      // LOCAL above this: two passes (L2 write frontier)
-constexpr int kJoinThreads = 512;
-constexpr int kSlots = 8192;
+constexpr int kJoinThreads = 1024;
+constexpr int kSlotBits = 14;
+constexpr int kSlots = 1 << kSlotBits;
 constexpr int kChunk = kSlots * 3 / 4;
 constexpr uint32_t kEmpty = 0xffffffffu;
-constexpr size_t kJoinSmem = kSlots * (sizeof(int64_t) + sizeof(uint32_t));
+constexpr int kStage = 256;  // staged matches per warp per emit round
+constexpr size_t kJoinSmem = kSlots * (sizeof(int64_t) + sizeof(uint32_t)) + (kJoinThreads / 32) * kStage * sizeof(uint32_t);
+static_assert(kSlotBits + 13 <= 32 && kJoinThreads * kRowsPerThread <= (1 << 13), "stage entry packing");
 
 __device__ __forceinline__ uint32_t bucket_of(int64_t key, int mode, int buckets, int log2b) {
     const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(key));
     if (mode == M4D_PART_RANK) return __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(buckets));
     return log2b ? static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) : 0u;
+}
+
+// Shared-table slot: a 32-bit multiplicative hash of the folded key (cheap;
+// independent of the partition bits, which come from splitmix64).
+__device__ __forceinline__ uint32_t slot_of(int64_t k) {
+    const uint32_t x = static_cast<uint32_t>(k) ^ static_cast<uint32_t>(static_cast<uint64_t>(k) >> 32);
+    return (x * 0x9E3779B1u) >> (32 - kSlotBits);
 }
 
 __device__ __forceinline__ uint64_t row_hash(int64_t k, int64_t l, int64_t r) {
@@ -429,17 +439,15 @@ __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int bu
         bounds[b] = b < buckets ? offsets[static_cast<int64_t>(b) * ctas] : total;
 }
 
-__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long* red) {
-    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    unsigned long long t = 0;
-    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
-    return t;
-}
-
-__global__ void __launch_bounds__(kJoinThreads, 2)
+// One CTA per partition: build an open-addressing table of the left rows in
+// shared memory (chunks of kChunk rows), then probe with the right rows in
+// batches of kJoinThreads * kRowsPerThread.  Per batch: (1) every thread
+// counts its matches (the walks are divergent but cheap), (2) a block scan
+// plus one global atomic reserves the batch's output range, (3) each thread
+// re-walks and records its matches as packed (slot, row) entries in its
+// warp's stage, (4) the warp emits the staged matches with all 32 lanes:
+// coalesced output stores and a full-width row-hash for the digest.
+__global__ void __launch_bounds__(kJoinThreads, 1)
     join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
                 const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
                 int64_t* __restrict__ ol, int64_t* __restrict__ orr, int64_t capacity,
@@ -447,10 +455,11 @@ __global__ void __launch_bounds__(kJoinThreads, 2)
     extern __shared__ unsigned char smem[];
     int64_t* tkey = reinterpret_cast<int64_t*>(smem);
     uint32_t* tidx = reinterpret_cast<uint32_t*>(smem + kSlots * sizeof(int64_t));
-    __shared__ unsigned long long red[kJoinThreads / 32];
+    __shared__ unsigned long long red[kJoinThreads / 32][3];
     __shared__ unsigned long long block_base;
     const int part = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t* stage = tidx + kSlots + warp * kStage;
     const int64_t b0 = loff[part], b1 = loff[part + 1];
     const int64_t p0 = roff[part], p1 = roff[part + 1];
     constexpr int kPer = kRowsPerThread;
@@ -470,76 +479,109 @@ __global__ void __launch_bounds__(kJoinThreads, 2)
             for (int u = 0; u < kPer; ++u) {
                 const int64_t i = base + u * blockDim.x + threadIdx.x;
                 if (i >= c1) continue;
-                uint32_t s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(k[u]))) & (kSlots - 1);
+                uint32_t s = slot_of(k[u]);
                 while (atomicCAS(&tidx[s], kEmpty, static_cast<uint32_t>(i - c0)) != kEmpty) s = (s + 1) & (kSlots - 1);
                 tkey[s] = k[u];
             }
         }
         __syncthreads();
-        // probe rows kPer per thread at a time; the trip count is uniform over the block
         for (int64_t base = p0; base < p1; base += static_cast<int64_t>(blockDim.x) * kPer) {
-            longlong2 r[kPer];
+            int64_t r[kPer];
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {
                 const int64_t j = base + u * blockDim.x + threadIdx.x;
-                if (j < p1) r[u] = probe[j];
+                r[u] = j < p1 ? probe[j].x : 0;
             }
-            unsigned long long mine = 0;  // pass 1: count
+            uint32_t mine = 0;  // (1) count
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {
                 if (base + u * blockDim.x + threadIdx.x >= p1) continue;
-                for (uint32_t s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(r[u].x))) & (kSlots - 1);
-                     tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1))
-                    mine += tkey[s] == r[u].x;
+                for (uint32_t s = slot_of(r[u]); tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1)) mine += tkey[s] == r[u];
             }
-            unsigned long long incl = mine;
+            uint32_t incl = mine;
             for (int o = 1; o < 32; o <<= 1) {
-                unsigned long long y = __shfl_up_sync(0xffffffffu, incl, o);
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            if (lane == 31) red[warp] = incl;
+            const uint32_t warp_total = __shfl_sync(0xffffffffu, incl, 31);
+            if (lane == 31) red[warp][0] = warp_total;
             __syncthreads();
-            if (threadIdx.x == 0) {
+            if (threadIdx.x == 0) {  // (2) reserve
                 unsigned long long run = 0;
                 for (int w = 0; w < kJoinThreads / 32; ++w) {
-                    const unsigned long long t = red[w];
-                    red[w] = run;
+                    const unsigned long long t = red[w][0];
+                    red[w][0] = run;
                     run += t;
                 }
                 block_base = run ? atomicAdd(cursor, run) : 0;
             }
             __syncthreads();
-            unsigned long long pos = block_base + red[warp] + incl - mine;
-            __syncthreads();  // red / block_base are reused by the next probe batch
+            const unsigned long long wbase = block_base + red[warp][0];
+            __syncthreads();  // red / block_base are reused by the next batch
+            const uint32_t my0 = incl - mine;
+            for (uint32_t win = 0; win < warp_total; win += kStage) {  // warp-uniform rounds
+                if (mine && my0 < win + kStage && my0 + mine > win) {  // (3) stage
+                    uint32_t e = my0;
 #pragma unroll
-            for (int u = 0; u < kPer; ++u) {  // pass 2: emit
-                if (base + u * blockDim.x + threadIdx.x >= p1) continue;
-                const longlong2 pr = r[u];
-                for (uint32_t s = static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(pr.x))) & (kSlots - 1);
-                     tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1)) {
-                    if (tkey[s] != pr.x) continue;
-                    const int64_t l = build[c0 + tidx[s]].y;
-                    if (static_cast<int64_t>(pos) < capacity) {
-                        ok[pos] = pr.x;
-                        ol[pos] = l;
-                        orr[pos] = pr.y;
+                    for (int u = 0; u < kPer; ++u) {
+                        if (base + u * blockDim.x + threadIdx.x >= p1) continue;
+                        const uint32_t loc = static_cast<uint32_t>(u * blockDim.x + threadIdx.x) << kSlotBits;
+                        for (uint32_t s = slot_of(r[u]); tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1)) {
+                            if (tkey[s] != r[u]) continue;
+                            if (e >= win && e < win + kStage) stage[e - win] = loc | s;
+                            ++e;
+                        }
                     }
-                    ++pos;
-                    ++cnt;
-                    hsum += row_hash(pr.x, l, pr.y);
-                    ksum += static_cast<unsigned long long>(pr.x);
                 }
+                __syncwarp();
+                const uint32_t n = warp_total - win < kStage ? warp_total - win : kStage;
+                for (uint32_t q = lane; q < n; q += 32) {  // (4) emit, all lanes
+                    const uint32_t ent = stage[q];
+                    const uint32_t s = ent & (kSlots - 1);
+                    const int64_t key = tkey[s];
+                    const int64_t l = build[c0 + tidx[s]].y;
+                    const int64_t rv = probe[base + (ent >> kSlotBits)].y;
+                    const unsigned long long pos = wbase + win + q;
+                    if (static_cast<int64_t>(pos) < capacity) {
+                        ok[pos] = key;
+                        ol[pos] = l;
+                        orr[pos] = rv;
+                    }
+                    ++cnt;
+                    hsum += row_hash(key, l, rv);
+                    ksum += static_cast<unsigned long long>(key);
+                }
+                __syncwarp();
             }
         }
         __syncthreads();
     }
-    cnt = block_sum(cnt, red);
-    hsum = block_sum(hsum, red);
-    ksum = block_sum(ksum, red);
-    if (threadIdx.x == 0 && cnt) {
-        atomicAdd(digest + 0, cnt);
-        atomicAdd(digest + 1, hsum);
-        atomicAdd(digest + 2, ksum);
+    for (int o = 16; o; o >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+        ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+    }
+    if (lane == 0) {
+        red[warp][0] = cnt;
+        red[warp][1] = hsum;
+        red[warp][2] = ksum;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        static_assert(kJoinThreads / 32 <= 32, "one warp folds the per-warp sums");
+        cnt = lane < kJoinThreads / 32 ? red[lane][0] : 0;
+        hsum = lane < kJoinThreads / 32 ? red[lane][1] : 0;
+        ksum = lane < kJoinThreads / 32 ? red[lane][2] : 0;
+        for (int o = 16; o; o >>= 1) {
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+            hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
+            ksum += __shfl_xor_sync(0xffffffffu, ksum, o);
+        }
+        if (lane == 0 && cnt) {
+            atomicAdd(digest + 0, cnt);
+            atomicAdd(digest + 1, hsum);
+            atomicAdd(digest + 2, ksum);
+        }
     }
 }
 
