@@ -188,7 +188,9 @@ typedef struct m4d_ts_task {
     int32_t slot_y;
     int32_t slot_y2;
     int32_t diag;
-    int32_t reserved;
+    int32_t remote;   /* 1 when bt is read from a peer GPU over NVLink: the plan
+                         runs remote and local tasks as two concurrent item
+                         streams so NVLink and HBM traffic overlap */
 } m4d_ts_task;
 
 typedef struct m4d_ts_plan m4d_ts_plan;

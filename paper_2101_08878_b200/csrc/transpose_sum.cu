@@ -82,11 +82,13 @@ struct TsParams {
     int T;                    // tiles per block edge
     int64_t b;                // block edge (elements)
     int64_t items;            // total tile items
+    int64_t items_remote;     // items [0, items_remote) read a peer tile (tasks sorted remote-first)
+    int remote_ctas;          // CTAs that start on the remote stream (dynamic TMA path)
     int nslots;
     double* tile_sums;        // [nslots][T*T]
     unsigned* block_done;     // [nslots]
     unsigned* all_done;       // [1]
-    unsigned long long* work; // [1] dynamic item cursor (TMA path)
+    unsigned long long* work; // [2] dynamic item cursors: remote stream, local stream (TMA path)
     unsigned* exits;          // [1] CTAs done (TMA path)
     double* block_sums;       // [nslots]
     double* total;            // [1] or null
@@ -282,11 +284,26 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         if (lane == 0) {
             int task = 0;
             int k = 0;
-            int64_t next = p.dynamic ? static_cast<int64_t>(atomicAdd(p.work, 1ull)) : blockIdx.x;
+            // Two item streams share the grid: remote items (x(j,i) read over
+            // NVLink) and local ones.  The first remote_ctas CTAs start on the
+            // remote stream, the rest on the local one; a CTA whose stream
+            // runs dry moves to the other, so NVLink and HBM stay busy together.
+            int st = (blockIdx.x < p.remote_ctas && p.items_remote > 0) ? 0 : 1;
+            unsigned dry = (p.items_remote == 0 ? 1u : 0u) | (p.items_remote == p.items ? 2u : 0u);  // bit per stream
+            auto claim = [&]() -> int64_t {
+                for (int tries = 0; tries < 2; ++tries, st ^= 1) {
+                    if (dry >> st & 1u) continue;
+                    const int64_t v = (st ? p.items_remote : 0) + static_cast<int64_t>(atomicAdd(p.work + st, 1ull));
+                    if (v < (st ? p.items : p.items_remote)) return v;
+                    dry |= 1u << st;
+                }
+                return p.items;
+            };
+            int64_t next = p.dynamic ? claim() : blockIdx.x;
             for (;; ++k) {
                 const int64_t item = next;
                 if (item < p.items)  // claim the following item early: its latency overlaps this one
-                    next = p.dynamic ? static_cast<int64_t>(atomicAdd(p.work, 1ull)) : item + gridDim.x;
+                    next = p.dynamic ? claim() : item + gridDim.x;
                 const int s = k % kStages;
                 const uint32_t ph = (k / kStages) & 1;
                 m4d::ptx::mbar_wait(&empty_bar[s], ph ^ 1);
@@ -297,7 +314,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     m4d::ptx::mbar_arrive(&full_bar[s]);
                     break;
                 }
-                while (item_off[task + 1] <= item) ++task;  // items ascend: walk forward
+                if (item < item_off[task]) task = 0;  // moved back to the remote stream
+                while (item_off[task + 1] <= item) ++task;  // items ascend within a stream: walk forward
                 const m4d_ts_task t = p.tasks[task];
                 const int4 ref = p.refs[task];
                 int64_t local = item - item_off[task];
@@ -390,7 +408,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     if (p.dynamic && threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(p.exits, 1u) + 1u == gridDim.x) {  // last CTA out re-arms the cursor
-            *p.work = 0;
+            p.work[0] = 0;
+            p.work[1] = 0;
             *p.exits = 0;
         }
     }
@@ -498,6 +517,16 @@ PFN_encodeTiled encode_tiled_fn() {
     return fn;
 }
 
+// L2 promotion of peer-pool tensor maps (M4D_TS_REMOTE_PROMO = none|64|128|256).
+CUtensorMapL2promotion remote_promotion() {
+    const char* v = getenv("M4D_TS_REMOTE_PROMO");
+    if (!v) return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+    if (!strcmp(v, "none")) return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    if (!strcmp(v, "64")) return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    if (!strcmp(v, "128")) return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 // Groups the x-block pointers of the tasks into pools (a base plus whole
 // blocks) and encodes one 2-D tensor map per pool: rows = slot * b + row,
 // cols = col, 128-byte swizzled 64x16 boxes.  Returns false when the tasks
@@ -508,24 +537,29 @@ bool build_maps(const m4d_ts_task* tasks, int ntasks, int64_t b, TsMaps* maps, s
     if (!encode) return false;
     const uint64_t block_bytes = static_cast<uint64_t>(b) * b * sizeof(double);
     std::vector<uintptr_t> ptrs;
+    std::map<uintptr_t, bool> remote;  // pointer -> read over NVLink
     for (int t = 0; t < ntasks; ++t) {
         ptrs.push_back(reinterpret_cast<uintptr_t>(tasks[t].a));
         ptrs.push_back(reinterpret_cast<uintptr_t>(tasks[t].bt));
+        remote[reinterpret_cast<uintptr_t>(tasks[t].a)] |= false;
+        remote[reinterpret_cast<uintptr_t>(tasks[t].bt)] |= tasks[t].remote != 0;
     }
     std::sort(ptrs.begin(), ptrs.end());
     ptrs.erase(std::unique(ptrs.begin(), ptrs.end()), ptrs.end());
     std::vector<uintptr_t> bases;
     std::vector<uint64_t> slots;  // max slot + 1 per base
+    std::vector<bool> pool_remote;
     std::map<uintptr_t, std::pair<int, int>> where;
     for (uintptr_t p : ptrs) {
         if (p & 15) return false;
         int found = -1;
         for (size_t k = 0; k < bases.size(); ++k)
-            if ((p - bases[k]) % block_bytes == 0) { found = static_cast<int>(k); break; }
+            if ((p - bases[k]) % block_bytes == 0 && pool_remote[k] == remote[p]) { found = static_cast<int>(k); break; }
         if (found < 0) {
             if (bases.size() == kMaxMaps) return false;
             bases.push_back(p);
             slots.push_back(0);
+            pool_remote.push_back(remote[p]);
             found = static_cast<int>(bases.size()) - 1;
         }
         const uint64_t slot = (p - bases[found]) / block_bytes;
@@ -540,7 +574,8 @@ bool build_maps(const m4d_ts_task* tasks, int ntasks, int64_t b, TsMaps* maps, s
         cuuint32_t estr[2] = {1, 1};
         if (encode(&maps->m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, reinterpret_cast<void*>(bases[k]), dims,
                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+                   pool_remote[k] ? remote_promotion() : CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return false;
     }
     refs->resize(ntasks);
@@ -561,6 +596,8 @@ struct m4d_ts_plan {
     int ntasks = 0;
     int nslots = 0;
     int64_t items = 0;
+    int64_t items_remote = 0;
+    int remote_ctas = 0;
     m4d_ts_task* d_tasks = nullptr;
     int4* d_refs = nullptr;
     int64_t* d_off = nullptr;
@@ -592,9 +629,19 @@ m4d_status m4d_fill_block_f64(double* dst, int64_t n, int64_t row0, int64_t col0
 }
 
 
-m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks, int64_t block,
+m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks_in, int ntasks, int64_t block,
                               int nslots, m4d_ts_plan** plan_out) {
     *plan_out = nullptr;
+    if (ntasks > 0 && !tasks_in) return fail(M4D_ERR_USAGE, "null task array");
+    // Remote tasks first (stable): items [0, items_remote) form the NVLink stream.
+    std::vector<m4d_ts_task> sorted;
+    sorted.reserve(ntasks > 0 ? ntasks : 0);
+    for (int pass = 0; pass < 2; ++pass)
+        for (int t = 0; t < ntasks; ++t)
+            if ((tasks_in[t].remote != 0) == (pass == 0)) sorted.push_back(tasks_in[t]);
+    const m4d_ts_task* tasks = sorted.data();
+    int nremote = 0;
+    while (nremote < ntasks && tasks[nremote].remote) ++nremote;
     if (block <= 0) return fail(M4D_ERR_USAGE, "block edge must be positive");
     if (ntasks < 0 || nslots < 0) return fail(M4D_ERR_USAGE, "negative task or slot count");
     const int64_t T64 = (block + kTile - 1) / kTile;
@@ -640,6 +687,7 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks, 
     plan->ntasks = ntasks;
     plan->nslots = nslots;
     plan->items = off[ntasks];
+    plan->items_remote = off[nremote];
     auto cleanup = [&](int code) {
         m4d_ts_plan_destroy(plan);
         return code;
@@ -670,8 +718,8 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks, 
             cudaSuccess ||
         (e = cudaMalloc(&plan->d_counters, sizeof(unsigned) * (nslots + 2))) != cudaSuccess ||
         (e = cudaMemset(plan->d_counters, 0, sizeof(unsigned) * (nslots + 2))) != cudaSuccess ||
-        (e = cudaMalloc(&plan->d_work, sizeof(unsigned long long))) != cudaSuccess ||
-        (e = cudaMemset(plan->d_work, 0, sizeof(unsigned long long))) != cudaSuccess)
+        (e = cudaMalloc(&plan->d_work, 2 * sizeof(unsigned long long))) != cudaSuccess ||
+        (e = cudaMemset(plan->d_work, 0, 2 * sizeof(unsigned long long))) != cudaSuccess)
         return cleanup(m4d::cuda_fail(e, "plan scratch"));
     if ((e = cudaFuncSetAttribute(ts_kernel_ldg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemLdg))) != cudaSuccess ||
@@ -682,6 +730,10 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks, int ntasks, 
         return cleanup(m4d::cuda_fail(e, "ts kernel attributes"));
     if ((e = cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
         return cleanup(m4d::cuda_fail(e, "SM count"));
+    // CTAs that start on the remote stream: in proportion to its share of the
+    // items (M4D_TS_REMOTE_CTAS overrides, for the ablation in DESIGN.md).
+    plan->remote_ctas = plan->items ? static_cast<int>((plan->sms * plan->items_remote + plan->items - 1) / plan->items) : 0;
+    if (const char* v = getenv("M4D_TS_REMOTE_CTAS")) plan->remote_ctas = atoi(v);
     *plan_out = plan;
     return M4D_OK;
 }
@@ -704,6 +756,8 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
     p.b = plan->b;
     p.nslots = plan->nslots;
     p.items = plan->items;
+    p.items_remote = plan->items_remote;
+    p.remote_ctas = plan->remote_ctas;
     p.tile_sums = plan->d_tile_sums;
     p.block_done = plan->d_counters;
     p.all_done = plan->d_counters + plan->nslots;

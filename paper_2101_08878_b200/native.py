@@ -66,7 +66,7 @@ class TsTask(ctypes.Structure):
         ("slot_y", _i32),
         ("slot_y2", _i32),
         ("diag", _i32),
-        ("reserved", _i32),
+        ("remote", _i32),
     ]
 
 
