@@ -34,6 +34,7 @@ import subprocess
 import sys
 import threading
 import time
+from types import SimpleNamespace
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, HERE)
@@ -536,6 +537,176 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
     }
 
 
+# -- small-frame storm ---------------------------------------------
+
+
+def storm_line(r, args, world: int) -> dict:
+    return {
+        "metric": f"small-frame storm throughput ({args.frames} frames of 1 B-8 KiB, {args.conns} endpoints "
+                  f"per ordered worker pair)",
+        "value": r.frames_per_s, "unit": "frames/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": r.wall_s / max(1, args.steps) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (log-uniform sizes, seed 0x5EED; payload checked)",
+        "config": {"workload": "storm", "frames": args.frames, "conns": args.conns, "workers": world,
+                   "max_frame": 8192},
+        "latency_us": {"p50": r.p50_us, "p99": r.p99_us, "max": r.max_us}, "verified_frames": r.verified,
+    }
+
+
+def bench_storm(args, dist: Dist, peaks: dict) -> dict | None:
+    from paper_2101_08878_b200.harness import storm
+
+    if dist.world < 2:
+        raise SystemExit("--workload storm needs >= 2 ranks (torchrun --nproc-per-node N)")
+    t = open_transport(dist, dist.local_rank)
+    sampler = ClockSampler(dist.local_rank)
+    sampler.start()
+    r = storm.run_worker(storm.namespace_of("paper_2101_08878_b200"), t, dist.allgather_bytes,
+                         conns=args.conns, total=args.frames, rounds=args.steps, warmup=args.warmup)
+    clocks = sampler.stop()
+    t.close()
+    if dist.rank != 0:
+        return None
+    line = storm_line(r, args, dist.world)
+    line.update({
+        "gpu_launches": 0,
+        "note": "host frames through the nvlink transport's shared-memory rings (eager path); no kernels",
+        "roofline": None,
+        "e2e": {"value": r.frames_per_s, "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "note": "host frames through Endpoint.write/read: end to end by construction"},
+        "clocks": clocks,
+    })
+    if not args.skip_cpu:
+        ref = run_ref_workers("storm", dist.world, args, rounds=1, warmup=0)
+        if "value" in ref:
+            line["cpu_baseline"] = {"value": ref["value"], "unit": "frames/s", "cores": dist.world,
+                                    "kind": "reference", "sample": ref.get("sample", "")}
+    return line
+
+
+# -- reference arms over the reference's own SocketTransport (baseline/_ref) --------------------
+
+REF_DIR = os.path.join(HERE, "baseline", "_ref")
+
+
+def _free_ports(n: int) -> list[int]:
+    import socket
+
+    socks, ports = [], []
+    for _ in range(n):
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        socks.append(s)
+        ports.append(s.getsockname()[1])
+    for s in socks:
+        s.close()
+    return ports
+
+
+def run_ref_workers(kind: str, world: int, args, rounds: int, warmup: int, timeout: float = 900.0) -> dict:
+    """Spawn ``world`` reference worker processes (baseline/_ref commshim, SocketTransport on
+    127.0.0.1) and return rank 0's JSON summary."""
+    if not os.path.isdir(os.path.join(REF_DIR, "commshim")):
+        return {"unavailable": "baseline/_ref (the installed reference package) is missing"}
+    ports = ",".join(map(str, _free_ports(world)))
+    cmd = [sys.executable, os.path.abspath(__file__), "--ref-worker", kind, "--ref-world", str(world),
+           "--ref-ports", ports, "--frames", str(args.frames), "--conns", str(args.conns),
+           "--max-size", str(args.max_size), "--steps", str(rounds), "--warmup", str(warmup)]
+    procs = [subprocess.Popen(cmd + ["--ref-rank", str(r)], stdout=subprocess.PIPE, stderr=subprocess.PIPE,
+                              text=True) for r in range(world)]
+    outs = []
+    for p in procs:
+        try:
+            outs.append(p.communicate(timeout=timeout))
+        except subprocess.TimeoutExpired:
+            p.kill()
+            outs.append(p.communicate())
+    if any(p.returncode for p in procs):
+        bad = next((o[1] for p, o in zip(procs, outs) if p.returncode), "")
+        return {"unavailable": "reference workers failed: " + bad.strip().splitlines()[-1][:200] if bad.strip()
+                else "reference workers failed"}
+    return json.loads(outs[0][0].strip().splitlines()[-1])
+
+
+def ref_worker_main(args) -> int:
+    """One reference worker: the UNMODIFIED reference package over its SocketTransport."""
+    sys.path.insert(0, REF_DIR)
+    import commshim  # noqa: F401  (must resolve to baseline/_ref, not this repo's alias)
+
+    if not os.path.abspath(commshim.__file__).startswith(os.path.abspath(REF_DIR)):
+        raise SystemExit(f"reference import resolved to {commshim.__file__}")
+    from commshim.transport import TransportConfig, transport_init
+    from paper_2101_08878_b200.harness import p2p, storm
+
+    ports = [int(p) for p in args.ref_ports.split(",")]
+    rank, world = args.ref_rank, args.ref_world
+    t = transport_init(world, rank, TransportConfig(kind="socket", connect_timeout=60.0,
+                                                    rank_map={r: ("127.0.0.1", p) for r, p in enumerate(ports)}))
+    t.wait_ready(60.0)
+    ns = storm.namespace_of("commshim")
+    if args.ref_worker == "storm":
+        r = storm.run_worker(ns, t, storm.transport_sync(t), conns=args.conns, total=args.frames,
+                             rounds=args.steps, warmup=args.warmup)
+        out = {"value": r.frames_per_s, "wall_s": r.wall_s, "p50_us": r.p50_us, "p99_us": r.p99_us,
+               "verified": r.verified,
+               "sample": f"reference SocketTransport + Endpoint, {world} processes, {args.steps} round(s) of "
+                         f"{args.frames} frames"}
+    else:  # p2p: the same raw-post osu tests and comm-path ping-pong, host frames over sockets
+        rows, n = [], 1
+        while n <= args.max_size:
+            p2p.verify_once(t, 1 - rank, n, False)
+            lat_iters = max(3, min(1000, (64 << 20) // max(n, 1)))
+            window = max(1, min(64, (64 << 20) // n))
+            lat = p2p.osu_latency(t, 1 - rank, n, lat_iters, False)
+            bw = p2p.osu_bw(t, 1 - rank, n, window, 2 if n >= (1 << 20) else 10, False)
+            rows.append({"size": n, "osu_latency_us": lat, "osu_bw_GBps": bw, "window": window})
+            n *= 4
+        pp = {sz: p2p.pingpong(t, 1 - rank, sz, 200 if sz < (1 << 20) else 10, False, ns=ns) for sz in (1, 4 << 20)}
+        big = [r for r in rows if r["size"] >= (4 << 20)] or rows[-1:]
+        out = {"value": max(r["osu_bw_GBps"] for r in big), "latency_1B_us": rows[0]["osu_latency_us"],
+               "sweep": rows,
+               "comm_path": {str(k): {"latency_us": v["mean_s"] * 1e6, "GBps": v["throughput_Bps"] / 1e9}
+                             for k, v in pp.items() if v},
+               "sample": "reference SocketTransport, 2 processes, host frames; osu_bw window <= 64 MiB in flight"}
+    t.close()
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    return 0
+
+
+def reference_storm(args) -> dict:
+    world = max(2, int(os.environ.get("WORLD_SIZE", str(args.gpus))))
+    ref = run_ref_workers("storm", world, args, rounds=args.steps, warmup=min(args.warmup, 1))
+    if "value" not in ref:
+        return {"impl": "reference", **ref}
+    line = storm_line(SimpleNamespace(frames_per_s=ref["value"], wall_s=ref["wall_s"], p50_us=ref["p50_us"],
+                                      p99_us=ref["p99_us"], max_us=ref["p99_us"], verified=ref["verified"]),
+                      args, world)
+    line.pop("latency_us")
+    line.update({"impl": "reference", "latency_us": {"p50": ref["p50_us"], "p99": ref["p99_us"]},
+                 "cpu_baseline": {"value": ref["value"], "unit": "frames/s", "cores": world, "kind": "reference",
+                                  "sample": ref["sample"]},
+                 "e2e": {"value": ref["value"], "unit": "frames/s", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 0}})
+    return line
+
+
+def reference_p2p(args) -> dict:
+    ref = run_ref_workers("p2p", 2, args, rounds=1, warmup=0)
+    if "value" not in ref:
+        return {"impl": "reference", **ref}
+    return {
+        "impl": "reference", "metric": "p2p GB/s (osu_bw, >= 4 MiB)", "value": ref["value"], "unit": "GB/s",
+        "n_gpus": 2, "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
+        "config": {"workload": "p2p", "sizes": [r["size"] for r in ref["sweep"]], "frames": "host (socket)"},
+        "latency_1B_us": ref["latency_1B_us"], "sweep": ref["sweep"], "comm_path": ref["comm_path"],
+        "cpu_baseline": {"value": ref["value"], "unit": "GB/s", "cores": 2, "kind": "reference",
+                         "sample": ref["sample"]},
+        "e2e": {"value": ref["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
 def reference_transpose_sum(args) -> dict:
     threads = len(os.sched_getaffinity(0))
     per_step = []
@@ -595,7 +766,13 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=["transpose_sum", "key_merge", "p2p"], default="transpose_sum")
+    ap.add_argument("--workload", choices=["transpose_sum", "key_merge", "p2p", "storm"], default="transpose_sum")
+    ap.add_argument("--frames", type=int, default=100_000, help="storm frames per round")
+    ap.add_argument("--conns", type=int, default=8, help="storm endpoints per ordered worker pair")
+    ap.add_argument("--ref-worker", choices=["p2p", "storm"], help=argparse.SUPPRESS)
+    ap.add_argument("--ref-rank", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--ref-world", type=int, default=2, help=argparse.SUPPRESS)
+    ap.add_argument("--ref-ports", default="", help=argparse.SUPPRESS)
     ap.add_argument("--rows", type=int, default=100_000_000, help="key_merge rows per side per GPU")
     ap.add_argument("--fraction", type=float, default=0.3)
     ap.add_argument("--max-size", type=int, default=64 << 20, help="p2p largest message")
@@ -608,6 +785,8 @@ def main(argv=None) -> int:
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture (reported as roofline.traffic)")
     args = ap.parse_args(argv)
+    if args.ref_worker:
+        return ref_worker_main(args)
     if args.warmup < 3 and args.impl == "ours":
         print("bench: W >= 3 warm-up steps required; raising to 3", file=sys.stderr)
         args.warmup = 3
@@ -619,14 +798,16 @@ def main(argv=None) -> int:
             emit(reference_transpose_sum(args))
         elif args.workload == "key_merge":
             emit(reference_key_merge(args))
+        elif args.workload == "storm":
+            emit(reference_storm(args))
         else:
-            emit({"impl": "reference", "unavailable": "p2p reference arm needs the reference SocketTransport, "
-                                                      "which is not installed on the GPU box"})
+            emit(reference_p2p(args))
         return 0
 
     dist = Dist()
     peaks = load_peaks()
-    runner = {"transpose_sum": bench_transpose_sum, "key_merge": bench_key_merge, "p2p": bench_p2p}[args.workload]
+    runner = {"transpose_sum": bench_transpose_sum, "key_merge": bench_key_merge, "p2p": bench_p2p,
+              "storm": bench_storm}[args.workload]
     try:
         line = runner(args, dist, peaks)
     finally:

@@ -21,6 +21,7 @@ timed loop.
 from __future__ import annotations
 
 import time
+from types import SimpleNamespace
 
 from ..channels import build_comm_table
 from ..loop import MonotonicClock, TaskLoop
@@ -120,25 +121,32 @@ def osu_latency(transport: Transport, peer: int, n: int, iters: int, device: boo
     return (time.perf_counter() - start) / iters / 2 * 1e6
 
 
-def pingpong(transport: Transport, peer: int, n: int, iters: int, device: bool) -> dict:
-    """Comm-path ping-pong through send_payload/recv_payload on the TaskLoop."""
-    loop = TaskLoop(MonotonicClock())
-    table = build_comm_table(transport)
+def pingpong(transport: Transport, peer: int, n: int, iters: int, device: bool, ns=None) -> dict:
+    """Comm-path ping-pong through send_payload/recv_payload on the TaskLoop.
+
+    ``ns`` (see ``storm.namespace_of``) selects whose comm stack runs: this
+    package by default, or the reference package for the bench's reference arm."""
+    if ns is None:
+        ns = SimpleNamespace(TaskLoop=TaskLoop, MonotonicClock=MonotonicClock, build_comm_table=build_comm_table,
+                             send_payload=send_payload, recv_payload=recv_payload, make_frame=make_frame)
+    send_payload_, recv_payload_ = ns.send_payload, ns.recv_payload
+    loop = ns.TaskLoop(ns.MonotonicClock())
+    table = ns.build_comm_table(transport)
     channel = table.lookup(peer)
     if device:
         from ..transport.nvlink import CudaRegion
 
         frame = Frame(CudaRegion(pattern(n), transport.device), n, MemoryDomain.DEVICE)
     else:
-        frame = make_frame(pattern(n))
+        frame = ns.make_frame(pattern(n))
     warm = max(5, iters // 10)
     samples = []
 
     async def leader():
         for it in range(iters + warm):
             t0 = time.perf_counter()
-            await send_payload(transport, channel, 50, frame)
-            echo = await recv_payload(transport, channel, 51)
+            await send_payload_(transport, channel, 50, frame)
+            echo = await recv_payload_(transport, channel, 51)
             if it >= warm:
                 samples.append((time.perf_counter() - t0) / 2)
             if it == 0 and echo.to_bytes() != pattern(n):
@@ -146,8 +154,8 @@ def pingpong(transport: Transport, peer: int, n: int, iters: int, device: bool) 
 
     async def echo():
         for _ in range(iters + warm):
-            got = await recv_payload(transport, channel, 50)
-            await send_payload(transport, channel, 51, got)
+            got = await recv_payload_(transport, channel, 50)
+            await send_payload_(transport, channel, 51, got)
 
     loop.run_until_complete(leader() if transport.rank == 0 else echo())
     if not samples:
