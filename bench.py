@@ -521,17 +521,36 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
         bw = p2p.osu_bw(t, 1 - dist.rank, n, 64, 10 if n <= (1 << 20) else 4, True)
         rows.append({"size": n, "osu_latency_us": lat, "osu_bw_GBps": bw})
         n *= 4
+    # the public comm path (send_payload / recv_payload, Listing 2/3) with device frames
+    pp = {sz: p2p.pingpong(t, 1 - dist.rank, sz, 1000 if sz < (1 << 20) else 50, True)
+          for sz in sorted({1, min(4 << 20, args.max_size), args.max_size})}
     t.close()
+    cpu = None
+    if dist.rank == 0 and not args.skip_cpu:
+        sample = SimpleNamespace(**{**vars(args), "max_size": 4 << 20})
+        ref = run_ref_workers("p2p", 2, sample, rounds=1, warmup=0)
+        if "value" in ref:
+            cpu = {"value": ref["value"], "unit": "GB/s", "cores": 2, "kind": "reference",
+                   "sample": ref["sample"] + ", sizes 1 B - 4 MiB", "latency_1B_us": ref["latency_1B_us"]}
+    dist.barrier()
     if dist.rank != 0:
         return None
     big = [r for r in rows if r["size"] >= (4 << 20)]  # north_star: >= 4 MB messages
     best = max(big, key=lambda r: r["osu_bw_GBps"]) if big else rows[-1]
+    top = pp[args.max_size]
     return {
         "metric": "p2p GB/s (osu_bw, device frames, >= 4 MiB)", "value": best["osu_bw_GBps"], "unit": "GB/s",
         "n_gpus": 2, "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
         "config": {"workload": "p2p", "sizes": [r["size"] for r in rows], "window": 64},
         "latency_1B_us": rows[0]["osu_latency_us"], "sweep": rows,
+        "comm_path": {str(k): {"latency_us": v["mean_s"] * 1e6, "GBps": v["throughput_Bps"] / 1e9}
+                      for k, v in pp.items() if v},
+        "gpu_launches": None,
+        "e2e": {"value": top["throughput_Bps"] / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0,
+                "note": f"send_payload/recv_payload ping-pong of {args.max_size}-byte device frames (2*size/RTT)"},
+        "cpu_baseline": cpu,
         "roofline": {"bound": "nvlink", "achieved": best["osu_bw_GBps"], "peak": 900.0, "unit": "GB/s",
                      "frac": best["osu_bw_GBps"] / 900.0, "traffic": None, "peak_source": "nominal NVLink 5"},
     }
@@ -661,13 +680,15 @@ def ref_worker_main(args) -> int:
             bw = p2p.osu_bw(t, 1 - rank, n, window, 2 if n >= (1 << 20) else 10, False)
             rows.append({"size": n, "osu_latency_us": lat, "osu_bw_GBps": bw, "window": window})
             n *= 4
-        pp = {sz: p2p.pingpong(t, 1 - rank, sz, 200 if sz < (1 << 20) else 10, False, ns=ns) for sz in (1, 4 << 20)}
+        pp = {sz: p2p.pingpong(t, 1 - rank, sz, 200 if sz < (1 << 20) else 10, False, ns=ns)
+              for sz in sorted({1, min(4 << 20, args.max_size), args.max_size})}
         big = [r for r in rows if r["size"] >= (4 << 20)] or rows[-1:]
         out = {"value": max(r["osu_bw_GBps"] for r in big), "latency_1B_us": rows[0]["osu_latency_us"],
                "sweep": rows,
                "comm_path": {str(k): {"latency_us": v["mean_s"] * 1e6, "GBps": v["throughput_Bps"] / 1e9}
                              for k, v in pp.items() if v},
                "sample": "reference SocketTransport, 2 processes, host frames; osu_bw window <= 64 MiB in flight"}
+    storm.transport_sync(t, tag=960)(b"done")  # no rank closes while a peer still drains its last frames
     t.close()
     if rank == 0:
         print(json.dumps(out), flush=True)
@@ -703,7 +724,9 @@ def reference_p2p(args) -> dict:
         "latency_1B_us": ref["latency_1B_us"], "sweep": ref["sweep"], "comm_path": ref["comm_path"],
         "cpu_baseline": {"value": ref["value"], "unit": "GB/s", "cores": 2, "kind": "reference",
                          "sample": ref["sample"]},
-        "e2e": {"value": ref["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": ref["comm_path"][str(args.max_size)]["GBps"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0,
+                "note": f"send_payload/recv_payload ping-pong of {args.max_size}-byte host frames (2*size/RTT)"},
     }
 
 
