@@ -187,6 +187,27 @@ def lib():
     return _lib
 
 
+_fast = None
+
+
+def fast():
+    """The CPython fast path of the transport calls (csrc/pyfast.cpp), bound to
+    this process's libm4d.so; raises loudly when it was not built."""
+    global _fast
+    if _fast is not None:
+        return _fast
+    handle = lib()
+    try:
+        from . import _m4dfast
+    except ImportError as exc:
+        raise NativeLibraryMissing(f"_m4dfast extension not built ({exc}): run __graft_entry__.build()") from exc
+    addr = [ctypes.cast(getattr(handle, n), ctypes.c_void_p).value
+            for n in ("m4d_transport_post_send", "m4d_transport_post_recv", "m4d_transport_progress")]
+    _m4dfast.bind(*addr)
+    _fast = _m4dfast
+    return _fast
+
+
 def last_error() -> str:
     buf = ctypes.create_string_buffer(512)
     lib().m4d_last_error(buf, len(buf))

@@ -26,10 +26,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-import numpy as np
-
 from .. import native
-from ..errors import CommClosedError, ConfigurationError, StartupError, TransferError, UsageError
+from ..errors import CommClosedError, ConfigurationError, TransferError, UsageError
 from ..loop import MonotonicClock
 from .base import (
     DeviceRegion,
@@ -40,9 +38,6 @@ from .base import (
     TransferRequest,
     as_view,
 )
-
-_BATCH = 64
-
 
 _Config = native.TransportConfigC
 Completion = native.Completion
@@ -137,14 +132,6 @@ class _Lease:
             pass
 
 
-def _host_address(view: memoryview) -> int:
-    if len(view) == 0:
-        return 0
-    if not view.readonly:
-        return ctypes.addressof(ctypes.c_char.from_buffer(view))
-    return int(np.frombuffer(view, dtype=np.uint8).ctypes.data)
-
-
 def default_session() -> str:
     env = os.environ.get("M4D_SESSION")
     if env:
@@ -182,9 +169,8 @@ class NvlinkTransport(Transport):
             raise native.error_for(status, native.last_error(), rank=_rank_in(native.last_error()))
         self._h = handle.value
         self._lib = native.lib()
+        self._fast = native.fast()
         self._live: dict[int, TransferRequest] = {}
-        self._now = Completion()
-        self._batch = (Completion * _BATCH)()
         self._pool = _RegionPool(device) if device >= 0 else None
         self.connect_timeout = config.connect_timeout
 
@@ -210,19 +196,19 @@ class NvlinkTransport(Transport):
         self._check_post(channel, peer, tag, view)
         req = TransferRequest(self, direction, channel, peer, tag, view, domain)
         if isinstance(view, DeviceView):
-            addr, on_device = view.ptr, 1
+            obj, device_len = view.ptr, len(view)
         else:
-            addr, on_device = _host_address(view), 0
-        fn = self._lib.m4d_transport_post_send if direction == "send" else self._lib.m4d_transport_post_recv
-        now = self._now
-        status = fn(self._h, channel, peer, tag, addr, len(view), int(domain), on_device, req.id, ctypes.byref(now))
-        if status != native.OK:
-            raise native.error_for(status, native.last_error())
-        if now.status == -1:
+            obj, device_len = view, -1  # host: address taken through the buffer protocol
+        try:
+            done = self._fast.post(self._h, direction == "send", channel, peer, tag, obj, int(domain), device_len,
+                                   req.id)
+        except OSError as exc:
+            raise native.error_for(exc.args[0], native.last_error()) from None
+        if done is None:
             self._live[req.id] = req
             req._native = req.id
         else:
-            self._apply(req, now.status, now.bytes)
+            self._apply(req, done[0], done[1])
         return self._track(req)
 
     def post_send(self, channel: int, peer: int, tag: int, data,
@@ -256,18 +242,17 @@ class NvlinkTransport(Transport):
         req._finish(TransferRequest.FAILED, nbytes if status == native.ERR_TRANSFER else 0, error)
 
     def progress(self) -> int:
+        done = self._fast.progress(self._h)
+        if done is None:
+            return 0
         finished = 0
-        batch = self._batch
-        while True:
-            n = self._lib.m4d_transport_progress(self._h, batch, _BATCH)
-            for k in range(n):
-                c = batch[k]
-                req = self._live.pop(c.req_id, None)
-                if req is not None:
-                    self._apply(req, c.status, c.bytes)
-                    finished += 1
-            if n < _BATCH:
-                return finished
+        live = self._live
+        for req_id, status, nbytes in done:
+            req = live.pop(req_id, None)
+            if req is not None:
+                self._apply(req, status, nbytes)
+                finished += 1
+        return finished
 
     def cancel(self, request: TransferRequest) -> bool:
         if request._owner is not self:

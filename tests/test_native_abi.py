@@ -58,3 +58,15 @@ def test_product_never_imports_the_oracle():
             if f.endswith((".py", ".cu", ".cpp", ".h", ".cuh")):
                 src = open(os.path.join(dirpath, f), encoding="utf-8").read()
                 assert "import oracle" not in src and "from oracle" not in src and "liboracle" not in src, f
+
+
+def test_fast_path_extension_binds_to_the_same_library():
+    from paper_2101_08878_b200 import native
+
+    fast = native.fast()
+    assert fast is native.fast()
+    assert fast.progress.__doc__ and fast.post.__doc__
+    import pytest
+
+    with pytest.raises(TypeError):
+        fast.post(0)
