@@ -188,9 +188,11 @@ typedef struct m4d_ts_task {
     int32_t slot_y;
     int32_t slot_y2;
     int32_t diag;
-    int32_t remote;   /* 1 when bt is read from a peer GPU over NVLink: the plan
-                         runs remote and local tasks as two concurrent item
-                         streams so NVLink and HBM traffic overlap */
+    int32_t remote;   /* 0 when bt is local; otherwise a group id (e.g. 1 + the
+                         peer's rank) of the GPU bt is read from over NVLink.
+                         The plan runs one item stream per group plus the local
+                         one concurrently, so every peer is read at once and
+                         NVLink and HBM traffic overlap */
 } m4d_ts_task;
 
 typedef struct m4d_ts_plan m4d_ts_plan;

@@ -69,6 +69,7 @@ constexpr int kTmaThreads = kThreads + 64;  // 8 consumer warps + producer warp 
 constexpr int kSmemOffsets = 1024;  // item offsets kept in shared memory up to this many tasks + 1
 constexpr size_t kSmemTma = kStages * 2ull * kTileBytes + kSmemOffsets * sizeof(int64_t) + 1024;  // + alignment slack
 constexpr int kMaxMaps = 16;
+constexpr int kMaxStreams = 16;  // item streams of the dynamic scheduler: <= 15 peer groups + local
 
 struct TsMaps {
     CUtensorMap m[kMaxMaps];
@@ -83,7 +84,10 @@ struct TsParams {
     int64_t b;                // block edge (elements)
     int64_t items;            // total tile items
     int64_t items_remote;     // items [0, items_remote) read a peer tile (tasks sorted remote-first)
-    int remote_ctas;          // CTAs that start on the remote stream (dynamic TMA path)
+    int64_t stream_off[kMaxStreams + 1];  // item range of each stream: peer groups, then local
+    int nstreams;             // peer streams + 1 (local is the last one)
+    int remote_ctas;          // CTAs that start on a peer stream (dynamic TMA path)
+    int remote_cap;           // CTAs [remote_cap, grid) never take remote items
     int nslots;
     double* tile_sums;        // [nslots][T*T]
     unsigned* block_done;     // [nslots]
@@ -284,17 +288,23 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         if (lane == 0) {
             int task = 0;
             int k = 0;
-            // Two item streams share the grid: remote items (x(j,i) read over
-            // NVLink) and local ones.  The first remote_ctas CTAs start on the
-            // remote stream, the rest on the local one; a CTA whose stream
-            // runs dry moves to the other, so NVLink and HBM stay busy together.
-            int st = (blockIdx.x < p.remote_ctas && p.items_remote > 0) ? 0 : 1;
-            unsigned dry = (p.items_remote == 0 ? 1u : 0u) | (p.items_remote == p.items ? 2u : 0u);  // bit per stream
+            // Item streams share the grid: one per peer GPU whose tiles are read
+            // over NVLink, then the local one.  The first remote_ctas CTAs start
+            // spread over the peer streams (so every peer is read at once and no
+            // peer's links become a hotspot), the rest on the local stream; a CTA
+            // whose stream runs dry moves on to the next, so NVLink and HBM stay
+            // busy together until the end.
+            const int S = p.nstreams - 1;  // peer streams
+            int st = (static_cast<int>(blockIdx.x) < p.remote_ctas && S > 0) ? static_cast<int>(blockIdx.x) % S : S;
+            unsigned dry = 0;
+            for (int q = 0; q < p.nstreams; ++q)
+                if (p.stream_off[q] == p.stream_off[q + 1] || (q < S && static_cast<int>(blockIdx.x) >= p.remote_cap))
+                    dry |= 1u << q;
             auto claim = [&]() -> int64_t {
-                for (int tries = 0; tries < 2; ++tries, st ^= 1) {
+                for (int tries = 0; tries < p.nstreams; ++tries, st = st + 1 == p.nstreams ? 0 : st + 1) {
                     if (dry >> st & 1u) continue;
-                    const int64_t v = (st ? p.items_remote : 0) + static_cast<int64_t>(atomicAdd(p.work + st, 1ull));
-                    if (v < (st ? p.items : p.items_remote)) return v;
+                    const int64_t v = p.stream_off[st] + static_cast<int64_t>(atomicAdd(p.work + st, 1ull));
+                    if (v < p.stream_off[st + 1]) return v;
                     dry |= 1u << st;
                 }
                 return p.items;
@@ -314,7 +324,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     m4d::ptx::mbar_arrive(&full_bar[s]);
                     break;
                 }
-                if (item < item_off[task]) task = 0;  // moved back to the remote stream
+                if (item < item_off[task]) task = 0;  // moved to an earlier stream
                 while (item_off[task + 1] <= item) ++task;  // items ascend within a stream: walk forward
                 const m4d_ts_task t = p.tasks[task];
                 const int4 ref = p.refs[task];
@@ -408,8 +418,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     if (p.dynamic && threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(p.exits, 1u) + 1u == gridDim.x) {  // last CTA out re-arms the cursor
-            p.work[0] = 0;
-            p.work[1] = 0;
+            for (int q = 0; q < p.nstreams; ++q) p.work[q] = 0;
             *p.exits = 0;
         }
     }
@@ -597,7 +606,9 @@ struct m4d_ts_plan {
     int nslots = 0;
     int64_t items = 0;
     int64_t items_remote = 0;
+    std::vector<int64_t> stream_off;  // nstreams + 1
     int remote_ctas = 0;
+    int remote_cap = 1 << 30;
     m4d_ts_task* d_tasks = nullptr;
     int4* d_refs = nullptr;
     int64_t* d_off = nullptr;
@@ -633,15 +644,25 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks_in, int ntask
                               int nslots, m4d_ts_plan** plan_out) {
     *plan_out = nullptr;
     if (ntasks > 0 && !tasks_in) return fail(M4D_ERR_USAGE, "null task array");
-    // Remote tasks first (stable): items [0, items_remote) form the NVLink stream.
+    // Tasks grouped into item streams: one per distinct non-zero `remote` id
+    // (the peer the partner tile is read from), ascending, then the local tasks.
+    std::vector<int> groups;
+    for (int t = 0; t < ntasks; ++t)
+        if (tasks_in[t].remote && std::find(groups.begin(), groups.end(), tasks_in[t].remote) == groups.end())
+            groups.push_back(tasks_in[t].remote);
+    std::sort(groups.begin(), groups.end());
+    if (static_cast<int>(groups.size()) >= kMaxStreams) return fail(M4D_ERR_USAGE, "more than %d peer groups", kMaxStreams - 1);
     std::vector<m4d_ts_task> sorted;
+    std::vector<int> stream_tasks(groups.size() + 2, 0);  // task prefix per stream
     sorted.reserve(ntasks > 0 ? ntasks : 0);
-    for (int pass = 0; pass < 2; ++pass)
+    for (size_t g = 0; g <= groups.size(); ++g) {
         for (int t = 0; t < ntasks; ++t)
-            if ((tasks_in[t].remote != 0) == (pass == 0)) sorted.push_back(tasks_in[t]);
+            if (g < groups.size() ? tasks_in[t].remote == groups[g] : tasks_in[t].remote == 0)
+                sorted.push_back(tasks_in[t]);
+        stream_tasks[g + 1] = static_cast<int>(sorted.size());
+    }
     const m4d_ts_task* tasks = sorted.data();
-    int nremote = 0;
-    while (nremote < ntasks && tasks[nremote].remote) ++nremote;
+    const int nremote = stream_tasks[groups.size()];
     if (block <= 0) return fail(M4D_ERR_USAGE, "block edge must be positive");
     if (ntasks < 0 || nslots < 0) return fail(M4D_ERR_USAGE, "negative task or slot count");
     const int64_t T64 = (block + kTile - 1) / kTile;
@@ -688,6 +709,7 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks_in, int ntask
     plan->nslots = nslots;
     plan->items = off[ntasks];
     plan->items_remote = off[nremote];
+    for (size_t g = 0; g < stream_tasks.size(); ++g) plan->stream_off.push_back(off[stream_tasks[g]]);
     auto cleanup = [&](int code) {
         m4d_ts_plan_destroy(plan);
         return code;
@@ -718,8 +740,8 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks_in, int ntask
             cudaSuccess ||
         (e = cudaMalloc(&plan->d_counters, sizeof(unsigned) * (nslots + 2))) != cudaSuccess ||
         (e = cudaMemset(plan->d_counters, 0, sizeof(unsigned) * (nslots + 2))) != cudaSuccess ||
-        (e = cudaMalloc(&plan->d_work, 2 * sizeof(unsigned long long))) != cudaSuccess ||
-        (e = cudaMemset(plan->d_work, 0, 2 * sizeof(unsigned long long))) != cudaSuccess)
+        (e = cudaMalloc(&plan->d_work, kMaxStreams * sizeof(unsigned long long))) != cudaSuccess ||
+        (e = cudaMemset(plan->d_work, 0, kMaxStreams * sizeof(unsigned long long))) != cudaSuccess)
         return cleanup(m4d::cuda_fail(e, "plan scratch"));
     if ((e = cudaFuncSetAttribute(ts_kernel_ldg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kSmemLdg))) != cudaSuccess ||
@@ -734,6 +756,7 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks_in, int ntask
     // items (M4D_TS_REMOTE_CTAS overrides, for the ablation in DESIGN.md).
     plan->remote_ctas = plan->items ? static_cast<int>((plan->sms * plan->items_remote + plan->items - 1) / plan->items) : 0;
     if (const char* v = getenv("M4D_TS_REMOTE_CTAS")) plan->remote_ctas = atoi(v);
+    if (const char* v = getenv("M4D_TS_REMOTE_CAP")) plan->remote_cap = atoi(v);
     *plan_out = plan;
     return M4D_OK;
 }
@@ -758,6 +781,9 @@ m4d_status m4d_ts_run(m4d_ts_plan* plan, double* block_sums, double* total, void
     p.items = plan->items;
     p.items_remote = plan->items_remote;
     p.remote_ctas = plan->remote_ctas;
+    p.remote_cap = plan->remote_cap;
+    p.nstreams = static_cast<int>(plan->stream_off.size()) - 1;
+    for (int q = 0; q <= p.nstreams; ++q) p.stream_off[q] = plan->stream_off[q];
     p.tile_sums = plan->d_tile_sums;
     p.block_done = plan->d_counters;
     p.all_done = plan->d_counters + plan->nslots;

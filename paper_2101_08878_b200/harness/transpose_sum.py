@@ -148,7 +148,7 @@ class TransposeSum:
                     self.tasks_paired += 1
                 else:
                     t.bt = self.remote_x_ptr(partner)
-                    t.remote = 1
+                    t.remote = 1 + partner % world  # item stream of the peer the tile is read from
                     self.tasks_single += 1
             tasks.append(t)
         arr = (native.TsTask * max(1, len(tasks)))(*tasks)
