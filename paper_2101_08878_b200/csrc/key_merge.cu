@@ -43,8 +43,9 @@ constexpr int kSlots = 1 << kSlotBits;
 constexpr int kChunk = kSlots * 3 / 4;
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr int kStage = 256;  // staged matches per warp per emit round
+constexpr int kJoinPer = 4;   // probe / build rows per thread per batch (4096 rows per batch)
 constexpr size_t kJoinSmem = kSlots * (sizeof(int64_t) + sizeof(uint32_t)) + (kJoinThreads / 32) * kStage * sizeof(uint32_t);
-static_assert(kSlotBits + 13 <= 32 && kJoinThreads * kRowsPerThread <= (1 << 13), "stage entry packing");
+static_assert(kSlotBits + 12 <= 32 && kJoinThreads * kJoinPer <= (1 << 12), "stage entry packing");
 
 __device__ __forceinline__ uint32_t bucket_of(int64_t key, int mode, int buckets, int log2b) {
     const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(key));
@@ -441,12 +442,14 @@ __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int bu
 
 // One CTA per partition: build an open-addressing table of the left rows in
 // shared memory (chunks of kChunk rows), then probe with the right rows in
-// batches of kJoinThreads * kRowsPerThread.  Per batch: (1) every thread
-// counts its matches (the walks are divergent but cheap), (2) a block scan
-// plus one global atomic reserves the batch's output range, (3) each thread
-// re-walks and records its matches as packed (slot, row) entries in its
-// warp's stage, (4) the warp emits the staged matches with all 32 lanes:
-// coalesced output stores and a full-width row-hash for the digest.
+// batches of kJoinThreads * kJoinPer.  The probe phase is warp-independent
+// (no block barriers): (1) each thread walks its rows' chains once, keeping
+// per row the first matching slot and the match count; (2) a warp scan plus
+// one global atomic per warp reserves the warp's output range; (3) each
+// thread writes its matches as packed (row, slot) entries into the warp's
+// stage (re-walking only rows with several matches); (4) the warp emits the
+// stage with all 32 lanes: coalesced output stores, full-width row hashes.
+// Indices are 32-bit offsets from the partition start.
 __global__ void __launch_bounds__(kJoinThreads, 1)
     join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
                 const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
@@ -456,77 +459,90 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
     int64_t* tkey = reinterpret_cast<int64_t*>(smem);
     uint32_t* tidx = reinterpret_cast<uint32_t*>(smem + kSlots * sizeof(int64_t));
     __shared__ unsigned long long red[kJoinThreads / 32][3];
-    __shared__ unsigned long long block_base;
-    const int part = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int T = kJoinThreads;
+    constexpr int kPer = kJoinPer;
+    constexpr uint32_t kMask = kSlots - 1;
     uint32_t* stage = tidx + kSlots + warp * kStage;
-    const int64_t b0 = loff[part], b1 = loff[part + 1];
-    const int64_t p0 = roff[part], p1 = roff[part + 1];
-    constexpr int kPer = kRowsPerThread;
+    const longlong2* brow = build + loff[blockIdx.x];
+    const longlong2* prow = probe + roff[blockIdx.x];
+    if (loff[blockIdx.x + 1] - loff[blockIdx.x] > INT32_MAX || roff[blockIdx.x + 1] - roff[blockIdx.x] > INT32_MAX)
+        __trap();  // partitions are < 2^31 rows (32-bit offsets); fail loudly rather than mis-join
+    const int bn = static_cast<int>(loff[blockIdx.x + 1] - loff[blockIdx.x]);
+    const int pn = static_cast<int>(roff[blockIdx.x + 1] - roff[blockIdx.x]);
     unsigned long long cnt = 0, hsum = 0, ksum = 0;
-    for (int64_t c0 = b0; c0 < b1; c0 += kChunk) {
-        const int64_t c1 = c0 + kChunk < b1 ? c0 + kChunk : b1;
-        for (int s = threadIdx.x; s < kSlots; s += blockDim.x) tidx[s] = kEmpty;
+    for (int c0 = 0; c0 < bn; c0 += kChunk) {
+        const int cn = bn - c0 < kChunk ? bn - c0 : kChunk;
+        const longlong2* crow = brow + c0;
+        if (c0) __syncthreads();  // every warp is done probing the previous chunk's table
+        for (int s = threadIdx.x; s < kSlots; s += T) tidx[s] = kEmpty;
         __syncthreads();
-        for (int64_t base = c0; base < c1; base += static_cast<int64_t>(blockDim.x) * kPer) {
+        for (int base = 0; base < cn; base += T * kPer) {
             int64_t k[kPer];
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {
-                const int64_t i = base + u * blockDim.x + threadIdx.x;
-                k[u] = i < c1 ? build[i].x : 0;
+                const int i = base + u * T + threadIdx.x;
+                k[u] = i < cn ? crow[i].x : 0;
             }
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {
-                const int64_t i = base + u * blockDim.x + threadIdx.x;
-                if (i >= c1) continue;
+                const int i = base + u * T + threadIdx.x;
+                if (i >= cn) break;  // rows ascend with u
                 uint32_t s = slot_of(k[u]);
-                while (atomicCAS(&tidx[s], kEmpty, static_cast<uint32_t>(i - c0)) != kEmpty) s = (s + 1) & (kSlots - 1);
+                while (atomicCAS(&tidx[s], kEmpty, static_cast<uint32_t>(i)) != kEmpty) s = (s + 1) & kMask;
                 tkey[s] = k[u];
             }
         }
         __syncthreads();
-        for (int64_t base = p0; base < p1; base += static_cast<int64_t>(blockDim.x) * kPer) {
+        for (int base = 0; base < pn; base += T * kPer) {
             int64_t r[kPer];
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {
-                const int64_t j = base + u * blockDim.x + threadIdx.x;
-                r[u] = j < p1 ? probe[j].x : 0;
+                const int j = base + u * T + threadIdx.x;
+                r[u] = j < pn ? prow[j].x : 0;
             }
-            uint32_t mine = 0;  // (1) count
+            uint32_t info[kPer];  // first matching slot | min(matches, 0xffff) << 16
+            uint32_t mine = 0;
 #pragma unroll
-            for (int u = 0; u < kPer; ++u) {
-                if (base + u * blockDim.x + threadIdx.x >= p1) continue;
-                for (uint32_t s = slot_of(r[u]); tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1)) mine += tkey[s] == r[u];
+            for (int u = 0; u < kPer; ++u) {  // (1) count
+                info[u] = 0;
+                if (base + u * T + static_cast<int>(threadIdx.x) >= pn) continue;
+                uint32_t c = 0, first = 0;
+                for (uint32_t s = slot_of(r[u]); tidx[s] != kEmpty; s = (s + 1) & kMask)
+                    if (tkey[s] == r[u]) {
+                        first = c ? first : s;
+                        ++c;
+                    }
+                info[u] = first | (c < 0xffffu ? c : 0xffffu) << 16;
+                mine += c;
             }
             uint32_t incl = mine;
+#pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
             const uint32_t warp_total = __shfl_sync(0xffffffffu, incl, 31);
-            if (lane == 31) red[warp][0] = warp_total;
-            __syncthreads();
-            if (threadIdx.x == 0) {  // (2) reserve
-                unsigned long long run = 0;
-                for (int w = 0; w < kJoinThreads / 32; ++w) {
-                    const unsigned long long t = red[w][0];
-                    red[w][0] = run;
-                    run += t;
-                }
-                block_base = run ? atomicAdd(cursor, run) : 0;
-            }
-            __syncthreads();
-            const unsigned long long wbase = block_base + red[warp][0];
-            __syncthreads();  // red / block_base are reused by the next batch
+            if (!warp_total) continue;  // warp-uniform
+            unsigned long long wbase = 0;  // (2) reserve
+            if (lane == 31) wbase = atomicAdd(cursor, static_cast<unsigned long long>(warp_total));
+            wbase = __shfl_sync(0xffffffffu, wbase, 31);
             const uint32_t my0 = incl - mine;
             for (uint32_t win = 0; win < warp_total; win += kStage) {  // warp-uniform rounds
                 if (mine && my0 < win + kStage && my0 + mine > win) {  // (3) stage
                     uint32_t e = my0;
 #pragma unroll
                     for (int u = 0; u < kPer; ++u) {
-                        if (base + u * blockDim.x + threadIdx.x >= p1) continue;
-                        const uint32_t loc = static_cast<uint32_t>(u * blockDim.x + threadIdx.x) << kSlotBits;
-                        for (uint32_t s = slot_of(r[u]); tidx[s] != kEmpty; s = (s + 1) & (kSlots - 1)) {
+                        const uint32_t c = info[u] >> 16;
+                        if (!c) continue;
+                        const uint32_t loc = static_cast<uint32_t>(u * T + threadIdx.x) << kSlotBits;
+                        const uint32_t first = info[u] & 0xffffu;
+                        if (c == 1) {
+                            if (e >= win && e < win + kStage) stage[e - win] = loc | first;
+                            ++e;
+                            continue;
+                        }
+                        for (uint32_t s = first; tidx[s] != kEmpty; s = (s + 1) & kMask) {
                             if (tkey[s] != r[u]) continue;
                             if (e >= win && e < win + kStage) stage[e - win] = loc | s;
                             ++e;
@@ -537,10 +553,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                 const uint32_t n = warp_total - win < kStage ? warp_total - win : kStage;
                 for (uint32_t q = lane; q < n; q += 32) {  // (4) emit, all lanes
                     const uint32_t ent = stage[q];
-                    const uint32_t s = ent & (kSlots - 1);
+                    const uint32_t s = ent & kMask;
                     const int64_t key = tkey[s];
-                    const int64_t l = build[c0 + tidx[s]].y;
-                    const int64_t rv = probe[base + (ent >> kSlotBits)].y;
+                    const int64_t l = crow[tidx[s]].y;
+                    const int64_t rv = prow[base + static_cast<int>(ent >> kSlotBits)].y;
                     const unsigned long long pos = wbase + win + q;
                     if (static_cast<int64_t>(pos) < capacity) {
                         ok[pos] = key;
@@ -554,7 +570,6 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                 __syncwarp();
             }
         }
-        __syncthreads();
     }
     for (int o = 16; o; o >>= 1) {
         cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
