@@ -422,20 +422,11 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
         raise RuntimeError("merge digest changed between steps")
     launches = km.launches
 
-    # per-phase device timing (partition / join) on this rank, one extra step
-    phase = {}
-    if dist.world == 1:
-        ev = [native.Event() for _ in range(4)]
-        ev[0].record(stream)
-        for side in range(2):
-            km._partition(km.inputs[side], km.n, 0, km.parts, km.parted[side], km.bounds[side])
-        ev[1].record(stream)
-        native.check(native.lib().m4d_hash_join(
-            km.parted[0].ptr, km.bounds[0].ptr, km.parted[1].ptr, km.bounds[1].ptr, km.parts, km.out[0].ptr,
-            km.out[1].ptr, km.out[2].ptr, km.out_capacity, km.result.ptr, stream.handle))
-        ev[2].record(stream)
-        ev[2].synchronize()
-        phase = {"partition_ms": ev[0].elapsed_ms(ev[1]), "join_ms": ev[1].elapsed_ms(ev[2])}
+    # per-phase timing on this rank: one extra step with a synchronise at each phase boundary
+    km.profile = True
+    loop.run_until_complete(km.run_global())
+    km.profile = False
+    phase = {k: round(v, 3) for k, v in km.phases.items()}
 
     alg = km.algorithmic_bytes()
     hbm_peak = float(peaks["hbm_gbs"])

@@ -15,7 +15,9 @@ B200 pipeline per rank (one CUDA stream, SoA device columns):
 1. world > 1: hash-partition both tables by owner rank (``m4d_partition``
    mode RANK) and move every peer's segment with the nvlink transport:
    device-frame rendezvous, i.e. the owner pulls the rows straight out of
-   the sender's HBM over NVLink (one message per column, counts first);
+   the sender's HBM over NVLink (one message per side and peer, counts
+   first).  The two sides are pipelined: side 1's rank partition runs while
+   side 0 is pulled, side 0's local partition while side 1 is pulled;
 2. hash-partition the rows this rank owns into ``parts`` local partitions
    of ~6K rows (mode LOCAL), small enough for a shared-memory hash table;
 3. ``m4d_hash_join``: one CTA per partition builds and probes, writes the
@@ -112,6 +114,8 @@ class KeyMerge:
         self.result = native.DeviceBuffer(device, 4 * 8)
         self.received = [0, 0]
         self.launches = 0
+        self.profile = False  # diagnostics: synchronise and stamp each phase (never in timed runs)
+        self.phases: dict[str, float] = {}
 
     # -- data -------------------------------------------------------------------------------
 
@@ -132,64 +136,95 @@ class KeyMerge:
                                                 self.scratch_bytes, self.stream.handle))
         self.launches += native.lib().m4d_partition_launches(buckets)
 
+    def _mark(self, name: str) -> None:
+        if self.profile:
+            import time
+
+            self.stream.synchronize()
+            now = time.perf_counter()
+            self.phases[name] = (now - self._t_last) * 1e3
+            self._t_last = now
+
     def _read_bounds(self, buf, count: int) -> list[int]:
         raw = native.to_host(buf.ptr, (count + 1) * 8, self.stream)
         return list(struct.unpack(f"<{count + 1}q", raw))
 
-    async def _shuffle(self) -> list[int]:
-        """Partition by owner rank and pull every peer's segments over NVLink."""
+    def _rank_split(self, side: int) -> list[int]:
+        """Partition one side by owner rank; returns the row bounds per destination (synchronises)."""
+        self._partition(self.inputs[side], self.n, 1, self.world, self.sendbuf[side], self.rank_bounds[side])
+        return self._read_bounds(self.rank_bounds[side], self.world)
+
+    def _post_side(self, side: int, sends: list[int], incoming: list[int]) -> list:
+        """Post one side's exchange: pulls of every peer's segment (device frames over NVLink)
+        into the source-major receive buffer, and this rank's segments for the peers."""
         from ..transport.base import DeviceView
 
         t, P, me = self.transport, self.world, self.rank
-        sends = []  # per side: row bounds per destination
-        for side in range(2):
-            self._partition(self.inputs[side], self.n, 1, P, self.sendbuf[side], self.rank_bounds[side])
-            sends.append(self._read_bounds(self.rank_bounds[side], P))
-        counts = [[sends[s][d + 1] - sends[s][d] for d in range(P)] for s in range(2)]
-        blob = struct.pack(f"<{2 * P}q", *counts[0], *counts[1])
-        table = [struct.unpack(f"<{2 * P}q", b) for b in await allgather(t, blob, EXCHANGE_TAG)]
-        incoming = [[table[src][side * P + me] for src in range(P)] for side in range(2)]
-        received = []
-        reqs = []
-        for side in range(2):
-            total = sum(incoming[side])
-            if total > self.recv[side].capacity:
-                self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096)
-            if total > self.parted[side].capacity:
-                self.parted[side] = _Pairs(self.device, int(total * 1.1) + 4096)
-            received.append(total)
-            at = 0
-            for src in range(P):  # receive layout: source-major, each source's rows contiguous
-                rows = incoming[side][src]
-                dst = self.recv[side].ptr + at * 16
-                if src == me:
-                    native.memcpy(dst, self.sendbuf[side].ptr + sends[side][me] * 16, rows * 16, self.stream)
-                elif rows:
-                    view = DeviceView(dst, rows * 16, self.device)
-                    reqs.append(t.post_recv(0, src, DATA_TAG + side, view, MemoryDomain.DEVICE))
-                at += rows
-            for dst_rank in range(P):
-                rows = counts[side][dst_rank]
-                if dst_rank == me or not rows:
-                    continue
-                view = DeviceView(self.sendbuf[side].ptr + sends[side][dst_rank] * 16, rows * 16, self.device)
+        total = sum(incoming)
+        if total > self.recv[side].capacity:
+            self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096)
+        if total > self.parted[side].capacity:
+            self.parted[side] = _Pairs(self.device, int(total * 1.1) + 4096)
+        reqs, at = [], 0
+        for src in range(P):  # receive layout: source-major, each source's rows contiguous
+            rows = incoming[src]
+            dst = self.recv[side].ptr + at * 16
+            if src == me:
+                native.memcpy(dst, self.sendbuf[side].ptr + sends[me] * 16, rows * 16, self.stream)
+            elif rows:
+                reqs.append(t.post_recv(0, src, DATA_TAG + side, DeviceView(dst, rows * 16, self.device),
+                                        MemoryDomain.DEVICE))
+            at += rows
+        for dst_rank in range(P):
+            rows = sends[dst_rank + 1] - sends[dst_rank]
+            if dst_rank != me and rows:
+                view = DeviceView(self.sendbuf[side].ptr + sends[dst_rank] * 16, rows * 16, self.device)
                 reqs.append(t.post_send(0, dst_rank, DATA_TAG + side, view, MemoryDomain.DEVICE))
-        # the send buffers were written on self.stream: make them visible before peers pull
-        self.stream.synchronize()
-        for r in reqs:
+        t.progress()  # match what already arrived: the pulls start now, on the transport's streams
+        return reqs
+
+    async def _exchange_side(self, side: int) -> tuple[list, int]:
+        t, P, me = self.transport, self.world, self.rank
+        sends = self._rank_split(side)  # synchronises: the send buffer is complete before peers pull
+        counts = [sends[d + 1] - sends[d] for d in range(P)]
+        table = [struct.unpack(f"<{P}q", b) for b in await allgather(t, struct.pack(f"<{P}q", *counts),
+                                                                         EXCHANGE_TAG + 2 + side)]
+        incoming = [table[src][me] for src in range(P)]
+        return self._post_side(side, sends, incoming), sum(incoming)
+
+    async def _shuffle_and_partition(self) -> list[int]:
+        """Owner-rank partition, NVLink exchange and local partition of both sides, pipelined:
+        side 1's rank partition runs while side 0's rows are pulled, and side 0's local
+        partition runs while side 1's rows are pulled."""
+        t = self.transport
+        reqs0, n0 = await self._exchange_side(0)
+        reqs1, n1 = await self._exchange_side(1)
+        self._mark("rank_partition_and_post_ms")
+        for r in reqs0:
             await await_request(t, r)
-        return received
+        self._mark("side0_exchange_wait_ms")
+        self._partition(self.recv[0], n0, 0, self.parts, self.parted[0], self.bounds[0])
+        for r in reqs1:
+            await await_request(t, r)
+        self._mark("side1_exchange_wait_ms")
+        self._partition(self.recv[1], n1, 0, self.parts, self.parted[1], self.bounds[1])
+        return [n0, n1]
 
     async def run(self) -> tuple[int, int, int]:
         """One full step (partition [+ shuffle] + join).  Returns this rank's digest."""
+        if self.profile:
+            import time
+
+            self.stream.synchronize()
+            self._t_last = time.perf_counter()
+            self.phases = {}
         if self.world > 1:
-            self.received = await self._shuffle()
-            tables = self.recv
+            self.received = await self._shuffle_and_partition()
         else:
             self.received = [self.n, self.n]
-            tables = self.inputs
-        for side in range(2):
-            self._partition(tables[side], self.received[side], 0, self.parts, self.parted[side], self.bounds[side])
+            for side in range(2):
+                self._partition(self.inputs[side], self.n, 0, self.parts, self.parted[side], self.bounds[side])
+        self._mark("local_partition_ms")
         while True:
             native.check(native.lib().m4d_hash_join(
                 self.parted[0].ptr, self.bounds[0].ptr, self.parted[1].ptr, self.bounds[1].ptr, self.parts,
@@ -197,6 +232,7 @@ class KeyMerge:
                 self.stream.handle))
             self.launches += 2
             raw = native.to_host(self.result.ptr, 32, self.stream)
+            self._mark("join_ms")
             produced, count, hsum, ksum = struct.unpack("<4Q", raw)
             if count <= self.out_capacity:
                 self.rows_out = count
