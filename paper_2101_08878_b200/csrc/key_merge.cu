@@ -236,6 +236,8 @@ __global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int
     constexpr int kW = kHistThreads / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lower = (1u << lane) - 1u;
+    int nbits = 0;
+    while ((1 << nbits) < buckets) ++nbits;
     for (int b = threadIdx.x; b < kTileBuckets; b += blockDim.x)
         gcur[b] = b < buckets ? static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]) : 0u;
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
@@ -263,7 +265,17 @@ __global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int
         for (int u = 0; u < kRowsPerThread; ++u) {
             const bool live = tile + w * 256 + u * 32 + lane < hi;
             bk[u] = live ? bucket_of(row[u].x, mode, buckets, log2b) : 0xffffffffu;
-            const unsigned peers = __match_any_sync(0xffffffffu, bk[u]);
+            // peers = lanes with the same bucket: one ballot per bucket bit (plus
+            // liveness), cheaper than MATCH.ANY's serialised match
+            unsigned peers = __ballot_sync(0xffffffffu, live);
+            peers = live ? peers : ~peers;
+#pragma unroll
+            for (int bit = 0; bit < 8; ++bit) {  // buckets <= 256
+                if (bit < nbits) {
+                    const unsigned v = __ballot_sync(0xffffffffu, (bk[u] >> bit) & 1u);
+                    peers &= (bk[u] >> bit) & 1u ? v : ~v;
+                }
+            }
             const int leader = __ffs(peers) - 1;
             uint32_t start = 0;
             if (live && lane == leader) {
