@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int
 // bounds) serves both passes, so no second histogram read is needed.  Both
 // passes keep their write frontier (CTAs x fan-out x 32 B) inside L2.
 
-__global__ void __launch_bounds__(kHistThreads) hist2_kernel(const int64_t* __restrict__ keys,
+__global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__ keys,
                                                              const int64_t* __restrict__ vals, int64_t n,
                                                              int64_t run, int log2b, int b1,
                                                              uint32_t* __restrict__ hist_top,
@@ -688,7 +688,7 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 4));
         M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
         M4D_CUDA_TRY(cudaMemsetAsync(hist_all, 0, buckets * sizeof(unsigned long long), s));
-        hist2_kernel<<<ctas, kHistThreads, buckets * sizeof(uint32_t), s>>>(keys, vals, n, run, log2b, b1, hist, hist_all);
+        hist2_kernel<<<ctas, 1024, buckets * sizeof(uint32_t), s>>>(keys, vals, n, run, log2b, b1, hist, hist_all);
         scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
         scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
         scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
