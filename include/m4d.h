@@ -160,6 +160,10 @@ m4d_status m4d_transport_cancel(m4d_transport* t, uint64_t req_id, int* cancelle
 /* Transport.purge_channel (sim.py:171-180): drop unmatched state of a channel id. */
 m4d_status m4d_transport_purge_channel(m4d_transport* t, uint32_t channel);
 int m4d_transport_peer_alive(const m4d_transport* t, int peer);
+/* Cap on the CTAs of one pull-kernel launch (default 296 = 2 per SM, which one
+ * in-flight message needs to reach the NVLink peak).  Lower it while pulls run
+ * beside compute kernels (the key_merge shuffle uses 64). */
+m4d_status m4d_transport_set_pull_ctas(m4d_transport* t, int max_ctas);
 m4d_status m4d_transport_stats_get(const m4d_transport* t, m4d_transport_stats* out);
 m4d_status m4d_transport_close(m4d_transport* t);
 

@@ -27,7 +27,7 @@ struct PullBatch {
     PullDesc d[kMaxPull];
     int n;
 };
-int launch_pull_batch(const PullBatch& batch, cudaStream_t stream);
+int launch_pull_batch(const PullBatch& batch, cudaStream_t stream, int max_ctas);
 
 inline int cuda_fail(cudaError_t err, const char* what) {
     return fail(M4D_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));

@@ -37,12 +37,14 @@ __global__ void __launch_bounds__(512) pull_kernel(m4d::PullBatch batch) {
 
 namespace m4d {
 
-int launch_pull_batch(const PullBatch& batch, cudaStream_t stream) {
+int launch_pull_batch(const PullBatch& batch, cudaStream_t stream, int max_ctas) {
     size_t total = 0;
     for (int k = 0; k < batch.n; ++k) total += batch.d[k].len;
     // 2 CTAs of 512 threads per SM saturate NVLink; tiny batches use fewer CTAs.
+    // max_ctas caps the grid so pulls can share the GPU with compute kernels.
+    const unsigned cap = static_cast<unsigned>(max_ctas > 0 ? max_ctas : 296);
     unsigned grid = static_cast<unsigned>((total + 8191) / 8192);
-    if (grid > 296) grid = 296;
+    if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
     pull_kernel<<<grid, 512, 0, stream>>>(batch);
     cudaError_t e = cudaGetLastError();

@@ -247,6 +247,7 @@ struct m4d_transport {
     std::vector<Copy> copies;
     std::vector<PendingPull> pending_pulls;
     bool use_ce = false;                                        // M4D_PULL_ENGINE=ce: copy engine only
+    int pull_ctas = 296;                                        // pull-kernel grid cap (M4D_PULL_CTAS / setter)
     std::vector<cudaEvent_t> spare_events;
     std::vector<m4d_completion> done;
     std::map<std::pair<int, uint64_t>, void*> ipc_maps;         // (pid, buffer id) -> mapped base
@@ -408,7 +409,7 @@ void flush_pulls(m4d_transport* t) {
             batch.n = 0;
             for (j = i; j < v.size() && batch.n < m4d::kMaxPull && via_kernel(v[j]); ++j)
                 batch.d[batch.n++] = m4d::PullDesc{v[j].src, v[j].recv->ptr, v[j].len};
-            if (m4d::launch_pull_batch(batch, s) != M4D_OK) e = cudaErrorLaunchFailure;
+            if (m4d::launch_pull_batch(batch, s, t->pull_ctas) != M4D_OK) e = cudaErrorLaunchFailure;
         }
         if (e == cudaSuccess) e = cudaEventRecord(ev, s);
         if (e != cudaSuccess) {
@@ -874,6 +875,7 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
         }
         if (e == cudaSuccess) t->stream = t->pull_streams[0];
         if (const char* eng = getenv("M4D_PULL_ENGINE")) t->use_ce = strcmp(eng, "ce") == 0;
+        if (const char* c = getenv("M4D_PULL_CTAS")) t->pull_ctas = atoi(c) > 0 ? atoi(c) : 296;
         if (e != cudaSuccess) {
             m4d_transport* raw = t.release();
             m4d_transport_close(raw);
@@ -1113,6 +1115,12 @@ int m4d_transport_mesh_ready(const m4d_transport* t) {
     for (int q = 0; q < t->world; ++q)
         if (q != t->rank && !t->peers[q].seg) return 0;
     return 1;
+}
+
+m4d_status m4d_transport_set_pull_ctas(m4d_transport* t, int max_ctas) {
+    if (max_ctas < 1) return fail(M4D_ERR_USAGE, "pull grid cap must be positive");
+    t->pull_ctas = max_ctas;
+    return M4D_OK;
 }
 
 int m4d_transport_peer_alive(const m4d_transport* t, int peer) {

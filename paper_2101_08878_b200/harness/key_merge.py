@@ -44,6 +44,8 @@ SEED_LEFT = 0x4C454654
 SEED_RIGHT = 0x52494748
 EXCHANGE_TAG = 900
 DATA_TAG = 910
+SHUFFLE_PULL_CTAS = 192  # total pull CTAs while the shuffle overlaps partition kernels, split over the
+                         # P-1 concurrent per-peer pulls (N=4: 64 each, 16.3 -> 14.2 ms; tools/km_pull_sweep.sh)
 _MASK64 = (1 << 64) - 1
 
 
@@ -197,6 +199,8 @@ class KeyMerge:
         side 1's rank partition runs while side 0's rows are pulled, and side 0's local
         partition runs while side 1's rows are pulled."""
         t = self.transport
+        if hasattr(t, "set_pull_ctas"):
+            t.set_pull_ctas(max(32, SHUFFLE_PULL_CTAS // (self.world - 1)))  # pulls share the GPU with partitioning
         reqs0, n0 = await self._exchange_side(0)
         reqs1, n1 = await self._exchange_side(1)
         self._mark("rank_partition_and_post_ms")
@@ -208,6 +212,8 @@ class KeyMerge:
             await await_request(t, r)
         self._mark("side1_exchange_wait_ms")
         self._partition(self.recv[1], n1, 0, self.parts, self.parted[1], self.bounds[1])
+        if hasattr(t, "set_pull_ctas"):
+            t.set_pull_ctas(296)
         return [n0, n1]
 
     async def run(self) -> tuple[int, int, int]:

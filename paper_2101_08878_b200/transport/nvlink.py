@@ -271,6 +271,10 @@ class NvlinkTransport(Transport):
         native.check(self._lib.m4d_transport_purge_channel(self._h, channel))
         self.progress()
 
+    def set_pull_ctas(self, max_ctas: int) -> None:
+        """Cap the SM pull kernel's grid (pulls sharing the GPU with compute kernels)."""
+        native.check(self._lib.m4d_transport_set_pull_ctas(self._h, int(max_ctas)))
+
     def peer_alive(self, peer: int) -> bool:
         return bool(self._lib.m4d_transport_peer_alive(self._h, peer))
 
