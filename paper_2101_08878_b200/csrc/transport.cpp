@@ -201,8 +201,14 @@ struct Copy {
     int peer;
     uint64_t send_id;
     uint64_t bytes;
-    cudaEvent_t ev;   // may be shared by the messages of one batched launch
-    bool owns_event;  // the last message of a launch returns the event to the pool
+};
+
+// One pull launch (or copy-engine copy) and the messages its event completes.
+// Launches on one stream finish in order, so only the oldest of each stream
+// is ever queried.
+struct Launch {
+    cudaEvent_t ev;
+    std::vector<Copy> msgs;
 };
 
 struct PendingPull {
@@ -244,7 +250,8 @@ struct m4d_transport {
     std::vector<Peer> peers;
     std::unordered_map<uint64_t, std::unique_ptr<Req>> reqs;  // live requests by id
     std::unordered_map<uint64_t, Req*> awaiting_fin;           // rendezvous sends by id
-    std::vector<Copy> copies;
+    std::vector<std::deque<Launch>> inflight;                   // per pull stream, launch order
+    size_t inflight_launches = 0;
     std::vector<PendingPull> pending_pulls;
     bool use_ce = false;                                        // M4D_PULL_ENGINE=ce: copy engine only
     int pull_ctas = 296;                                        // pull-kernel grid cap (M4D_PULL_CTAS / setter)
@@ -396,7 +403,8 @@ void flush_pulls(m4d_transport* t) {
     std::vector<PendingPull>& v = t->pending_pulls;
     size_t i = 0;
     while (i < v.size()) {
-        cudaStream_t s = t->pull_streams[t->next_stream++ % t->pull_streams.size()];
+        const size_t si = t->next_stream++ % t->pull_streams.size();
+        cudaStream_t s = t->pull_streams[si];
         cudaEvent_t ev = nullptr;
         cudaError_t e = take_event(&ev);
         size_t j = i + 1;
@@ -416,8 +424,11 @@ void flush_pulls(m4d_transport* t) {
             if (ev) t->spare_events.push_back(ev);
             fail_all(i, j, e);
         } else {
-            for (size_t k = i; k < j; ++k)
-                t->copies.push_back(Copy{v[k].recv, v[k].peer, v[k].send_id, v[k].len, ev, k + 1 == j});
+            Launch l{ev, {}};
+            l.msgs.reserve(j - i);
+            for (size_t k = i; k < j; ++k) l.msgs.push_back(Copy{v[k].recv, v[k].peer, v[k].send_id, v[k].len});
+            t->inflight[si].push_back(std::move(l));
+            ++t->inflight_launches;
         }
         i = j;
     }
@@ -673,32 +684,32 @@ int drain_peer(m4d_transport* t, int peer) {
         ++n;
     }
     if (n) ring.ctl->head.store(ring.cursor, std::memory_order_release);
-    flush_pulls(t);
     if (p.said_bye && !p.dead) fail_peer(t, peer, M4D_ERR_CLOSED, "closed the connection");
     return n;
 }
 
 int poll_copies(m4d_transport* t) {
     int n = 0;
-    for (size_t i = 0; i < t->copies.size();) {
-        Copy& c = t->copies[i];
-        cudaError_t e = cudaEventQuery(c.ev);
-        if (e == cudaErrorNotReady) {
-            ++i;
-            continue;
+    for (auto& q : t->inflight) {
+        while (!q.empty()) {
+            Launch& l = q.front();
+            const cudaError_t e = cudaEventQuery(l.ev);
+            if (e == cudaErrorNotReady) break;
+            if (e != cudaSuccess) m4d::cuda_fail(e, "rendezvous copy");
+            for (const Copy& c : l.msgs) {
+                if (e == cudaSuccess) {
+                    queue_fin(t, c.peer, c.send_id, M4D_OK, c.bytes);
+                    complete(t, c.recv, M4D_OK, c.bytes);
+                } else {
+                    queue_fin(t, c.peer, c.send_id, M4D_ERR_TRANSFER, 0);
+                    complete(t, c.recv, M4D_ERR_CUDA, 0);
+                }
+                ++n;
+            }
+            t->spare_events.push_back(l.ev);
+            q.pop_front();
+            --t->inflight_launches;
         }
-        if (e == cudaSuccess) {
-            queue_fin(t, c.peer, c.send_id, M4D_OK, c.bytes);
-            complete(t, c.recv, M4D_OK, c.bytes);
-        } else {
-            m4d::cuda_fail(e, "rendezvous copy");
-            queue_fin(t, c.peer, c.send_id, M4D_ERR_TRANSFER, 0);
-            complete(t, c.recv, M4D_ERR_CUDA, 0);
-        }
-        if (c.owns_event) t->spare_events.push_back(c.ev);
-        t->copies[i] = t->copies.back();
-        t->copies.pop_back();
-        ++n;
     }
     return n;
 }
@@ -712,6 +723,7 @@ void check_liveness(m4d_transport* t) {
         Peer& p = t->peers[q];
         if (p.seg->state.load(std::memory_order_acquire) == kStateClosed) {
             drain_peer(t, q);  // take what it sent before leaving
+            flush_pulls(t);
             fail_peer(t, q, M4D_ERR_CLOSED, "closed the connection");
         } else if (!pid_alive(p.pid)) {
             fail_peer(t, q, M4D_ERR_TRANSFER, "died");
@@ -874,6 +886,7 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
             if (e == cudaSuccess) t->pull_streams.push_back(st);
         }
         if (e == cudaSuccess) t->stream = t->pull_streams[0];
+        t->inflight.resize(t->pull_streams.size());
         if (const char* eng = getenv("M4D_PULL_ENGINE")) t->use_ce = strcmp(eng, "ce") == 0;
         if (const char* c = getenv("M4D_PULL_CTAS")) t->pull_ctas = atoi(c) > 0 ? atoi(c) : 296;
         if (e != cudaSuccess) {
@@ -990,7 +1003,10 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
         u->second.pop_front();
         if (u->second.empty()) p.unexpected.erase(u);
         deliver_unexpected(t, peer, raw, msg);
-        flush_pulls(t);
+        // Pulls matched here are launched in batches: a window of posted
+        // receives becomes a few multi-message launches, not one launch per
+        // post (the next progress() issues whatever is left).
+        if (t->pending_pulls.size() >= static_cast<size_t>(m4d::kMaxPull)) flush_pulls(t);
         flush_peer(t, peer);  // a truncation / empty-rendezvous FIN leaves now
     } else if (p.dead) {
         fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
@@ -1012,12 +1028,13 @@ int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
     map_missing_peers(t);
     // Copies first: a finished pull must send its FIN in this same call, or a
     // sender whose peer stops polling would wait forever.
-    if (!t->copies.empty()) poll_copies(t);
+    if (t->inflight_launches) poll_copies(t);
     for (int q = 0; q < t->world; ++q)
         if (q != t->rank) {
             drain_peer(t, q);
             flush_peer(t, q);
         }
+    flush_pulls(t);
     if (!t->reqs.empty()) check_liveness(t);
     int n = 0;
     const int avail = static_cast<int>(t->done.size());
@@ -1066,6 +1083,7 @@ m4d_status m4d_transport_purge_channel(m4d_transport* t, uint32_t channel) {
         if (q == t->rank) continue;
         Peer& p = t->peers[q];
         drain_peer(t, q);
+        flush_pulls(t);
         for (auto it = p.unexpected.begin(); it != p.unexpected.end();) {
             if ((it->first >> 32) == channel) {
                 for (auto& u : it->second)
@@ -1152,8 +1170,8 @@ m4d_status m4d_transport_close(m4d_transport* t) {
     if (t->me) t->me->state.store(kStateClosed, std::memory_order_release);
     if (!t->pull_streams.empty()) {
         for (cudaStream_t st : t->pull_streams) cudaStreamSynchronize(st);
-        for (Copy& c : t->copies)
-            if (c.owns_event) t->spare_events.push_back(c.ev);
+        for (auto& q : t->inflight)
+            for (Launch& l : q) t->spare_events.push_back(l.ev);
         for (cudaEvent_t e : t->spare_events) cudaEventDestroy(e);
         for (cudaStream_t st : t->pull_streams) cudaStreamDestroy(st);
     }

@@ -77,23 +77,43 @@ def verify_once(transport: Transport, peer: int, n: int, device: bool) -> None:
             raise AssertionError(f"p2p payload of {n} bytes differs")
 
 
+def _blank(transport: Transport, nbytes: int, device: bool):
+    if device:
+        from .. import native
+        from ..transport.nvlink import CudaRegion
+
+        region = CudaRegion(max(1, nbytes), transport.device)
+        native.check(native.lib().m4d_memset(region.ptr, 0x5A, max(1, nbytes), None))
+        native.check(native.lib().m4d_stream_sync(None))
+        return region
+    return bytearray(nbytes)
+
+
+def _slot(buf, device: bool, k: int, n: int):
+    return buf.window(k * n, n) if device else memoryview(buf)[k * n:(k + 1) * n]
+
+
 def osu_bw(transport: Transport, peer: int, n: int, window: int, iters: int, device: bool) -> float:
-    """Transport-layer bandwidth in GB/s (measured on rank 0; rank 1 mirrors)."""
+    """Transport-layer bandwidth in GB/s (measured on rank 0; rank 1 mirrors).
+
+    Every message of a window has its own source and destination region (the
+    OSU benchmark reuses one buffer, which lets concurrent pulls of identical
+    lines be served once and reports more than the link can carry)."""
     me = transport.rank
     dom = MemoryDomain.DEVICE if device else MemoryDomain.HOST
-    buf = _region(transport, pattern(n) if me == 0 else bytes(n), device)
+    buf = _blank(transport, n * window, device)
+    views = [_slot(buf, device, k, n) for k in range(window)]
     ack = bytearray(4)
-    view = _window(buf, device, n)
     start = None
     for it in range(iters + 1):  # iteration 0 is warm-up
         if it == 1:
             start = time.perf_counter()
         if me == 0:
-            reqs = [transport.post_send(0, peer, DATA_TAG, view, dom) for _ in range(window)]
+            reqs = [transport.post_send(0, peer, DATA_TAG, v, dom) for v in views]
             _wait(transport, *reqs)
             _wait(transport, transport.post_recv(0, peer, ACK_TAG, ack))
         else:
-            reqs = [transport.post_recv(0, peer, DATA_TAG, view, dom) for _ in range(window)]
+            reqs = [transport.post_recv(0, peer, DATA_TAG, v, dom) for v in views]
             _wait(transport, *reqs)
             _wait(transport, transport.post_send(0, peer, ACK_TAG, b"done"))
     elapsed = time.perf_counter() - start
