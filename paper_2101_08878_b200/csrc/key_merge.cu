@@ -35,7 +35,7 @@ namespace {
 constexpr int kHistThreads = 512;
 constexpr int kRowsPerThread = 8;        // rows each thread loads before using any (memory-level parallelism)
 constexpr int kMaxBuckets = 16384;       // single-pass partition limit (shared-memory counters)
-constexpr int kMaxParts = 1 << 15;       // two-pass LOCAL partition limit (128 KB of counters)
+constexpr int kMaxParts = 1 << 16;       // two-pass LOCAL partition limit (128 KB of 16-bit counters)
 constexpr int kSinglePassMax = 256;      // LOCAL above this: two passes (L2 write frontier)
 constexpr int kJoinThreads = 1024;
 constexpr int kSlotBits = 14;
@@ -348,14 +348,24 @@ __global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int
 // bounds) serves both passes, so no second histogram read is needed.  Both
 // passes keep their write frontier (CTAs x fan-out x 32 B) inside L2.
 
+// Full-id histogram in shared memory: 32-bit counters up to 32768 partitions;
+// for 65536, 16-bit counters packed two per word (128 KB, what a CTA can
+// hold).  A packed counter that would pass 65535 (one key repeated that often
+// inside one CTA's rows) flags the CTA, which then recounts its rows with
+// global atomics: exact under any skew.
+template <bool kPacked>
 __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__ keys,
-                                                             const int64_t* __restrict__ vals, int64_t n,
-                                                             int64_t run, int log2b, int b1,
-                                                             uint32_t* __restrict__ hist_top,
-                                                             unsigned long long* __restrict__ hist_all) {
-    extern __shared__ uint32_t h[];  // 2^log2b counters
+                                                     const int64_t* __restrict__ vals, int64_t n, int64_t run,
+                                                     int log2b, int b1, uint32_t* __restrict__ hist_top,
+                                                     unsigned long long* __restrict__ hist_all) {
+    extern __shared__ uint32_t h2[];  // 2^log2b 16-bit counters
+    __shared__ uint32_t top[256];
+    __shared__ int overflow;
     const int buckets = 1 << log2b;
-    for (int b = threadIdx.x; b < buckets; b += blockDim.x) h[b] = 0;
+    const int words = kPacked ? (buckets + 1) / 2 : buckets;
+    const int shift = log2b - b1;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) h2[w] = 0;
+    if (threadIdx.x == 0) overflow = 0;
     __syncthreads();
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
     for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
@@ -367,18 +377,42 @@ __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__
         }
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u)
-            if (base + u * blockDim.x + threadIdx.x < hi)
-                atomicAdd(&h[bucket_of(k[u], M4D_PART_LOCAL, buckets, log2b)], 1u);
+            if (base + u * blockDim.x + threadIdx.x < hi) {
+                const uint32_t b = bucket_of(k[u], M4D_PART_LOCAL, buckets, log2b);
+                if (kPacked) {
+                    const uint32_t half = (b & 1u) << 4;
+                    const uint32_t old = atomicAdd(&h2[b >> 1], 1u << half);
+                    if (((old >> half) & 0xffffu) == 0xffffu) overflow = 1;
+                } else {
+                    atomicAdd(&h2[b], 1u);
+                }
+            }
     }
     __syncthreads();
-    const int sub = 1 << (log2b - b1);
-    for (int b = threadIdx.x; b < buckets; b += blockDim.x)
-        if (h[b]) atomicAdd(hist_all + b, static_cast<unsigned long long>(h[b]));
-    for (int t = threadIdx.x; t < (1 << b1); t += blockDim.x) {
-        uint32_t c = 0;
-        for (int k = 0; k < sub; ++k) c += h[t * sub + k];
-        hist_top[static_cast<int64_t>(t) * gridDim.x + blockIdx.x] = c;
+    if (!overflow) {
+        auto count = [&](int b) -> uint32_t { return kPacked ? (h2[b >> 1] >> ((b & 1) << 4)) & 0xffffu : h2[b]; };
+        for (int b = threadIdx.x; b < buckets; b += blockDim.x) {
+            const uint32_t c = count(b);
+            if (c) atomicAdd(hist_all + b, static_cast<unsigned long long>(c));
+        }
+        for (int t = threadIdx.x; t < (1 << b1); t += blockDim.x) {
+            uint32_t c = 0;
+            for (int q = 0; q < (1 << shift); ++q) c += count(t << shift | q);
+            hist_top[static_cast<int64_t>(t) * gridDim.x + blockIdx.x] = c;
+        }
+        return;
     }
+    // rare skew path: exact recount with global atomics
+    for (int t = threadIdx.x; t < 256; t += blockDim.x) top[t] = 0;
+    __syncthreads();
+    for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const uint32_t b = bucket_of(key_at(keys, vals, i), M4D_PART_LOCAL, buckets, log2b);
+        atomicAdd(hist_all + b, 1ull);
+        atomicAdd(&top[b >> shift], 1u);
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < (1 << b1); t += blockDim.x)
+        hist_top[static_cast<int64_t>(t) * gridDim.x + blockIdx.x] = top[t];
 }
 
 __global__ void exclusive_scan_u64_kernel(const unsigned long long* __restrict__ v, int n, int64_t* __restrict__ out,
@@ -685,10 +719,14 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         unsigned long long* hist_all = reinterpret_cast<unsigned long long*>(base);
         base += (buckets * sizeof(unsigned long long) + 255) & ~size_t(255);
         longlong2* tmp = reinterpret_cast<longlong2*>(base);
-        M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 4));
+        const bool packed = buckets > (1 << 15);
+        const size_t hist_smem = packed ? (buckets + 1) / 2 * sizeof(uint32_t) : buckets * sizeof(uint32_t);
+        M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 2));
+        M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 2));
         M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
         M4D_CUDA_TRY(cudaMemsetAsync(hist_all, 0, buckets * sizeof(unsigned long long), s));
-        hist2_kernel<<<ctas, 1024, buckets * sizeof(uint32_t), s>>>(keys, vals, n, run, log2b, b1, hist, hist_all);
+        (packed ? hist2_kernel<true> : hist2_kernel<false>)<<<ctas, 1024, hist_smem, s>>>(keys, vals, n, run, log2b, b1,
+                                                                                        hist, hist_all);
         scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
         scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
         scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);

@@ -19,7 +19,7 @@ B200 pipeline per rank (one CUDA stream, SoA device columns):
    first).  The two sides are pipelined: side 1's rank partition runs while
    side 0 is pulled, side 0's local partition while side 1 is pulled;
 2. hash-partition the rows this rank owns into ``parts`` local partitions
-   of ~6K rows (mode LOCAL), small enough for a shared-memory hash table;
+   of ~1.5K rows (mode LOCAL), small enough for a shared-memory hash table;
 3. ``m4d_hash_join``: one CTA per partition builds and probes, writes the
    (key, lval, rval) rows and an order-independent digest (count, sum of
    row hashes, sum of keys, mod 2^64).
@@ -55,9 +55,10 @@ def merge_band(total: int, fraction: float) -> int:
 
 
 def choose_parts(rows: int) -> int:
-    """Power-of-two partition count with ~3K rows per partition (8192-slot shared tables)."""
+    """Power-of-two partition count with ~1.5K rows per partition (8192-slot shared tables,
+    load <= 0.19, two join CTAs per SM), at most 65536."""
     parts = 1
-    while parts < 32768 and rows / parts > 3000:
+    while parts < 65536 and rows / parts > 3100:
         parts *= 2
     return parts
 

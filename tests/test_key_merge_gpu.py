@@ -97,3 +97,37 @@ def test_large_config_properties():
     assert abs(got[0] / rows - 0.3) < 0.005
     assert got == oracle.key_merge_c(rows, 1, 0.3)
     assert ranks[0].received == [rows, rows]
+
+
+@pytest.mark.parametrize("buckets", [32768, 65536])
+def test_partition_bounds_under_extreme_skew(buckets):
+    """One key fills whole CTAs (>= 65536 equal rows each): the 16-bit shared histogram
+    overflows and the CTA falls back to exact global counting; bounds and the pair
+    permutation still match a numpy recount of the same bucket function."""
+    from paper_2101_08878_b200 import native
+
+    n = 3 * 65536
+    rng = np.random.default_rng(4)
+    keys = rng.integers(0, 1 << 40, n).astype(np.int64)
+    keys[: 2 * 65536] = 123456789  # the first two CTAs (65536 rows each) see one key only
+    vals = np.arange(n, dtype=np.int64)
+    lib = native.lib()
+    k_d, v_d = native.DeviceBuffer(0, n * 8), native.DeviceBuffer(0, n * 8)
+    native.memcpy(k_d.ptr, keys.ctypes.data, n * 8)
+    native.memcpy(v_d.ptr, vals.ctypes.data, n * 8)
+    out = native.DeviceBuffer(0, n * 16)
+    bounds = native.DeviceBuffer(0, (buckets + 1) * 8)
+    nbytes = lib.m4d_partition_scratch_bytes(n, buckets)
+    scratch = native.DeviceBuffer(0, nbytes)
+    native.check(lib.m4d_partition(k_d.ptr, v_d.ptr, n, 0, buckets, out.ptr, bounds.ptr, scratch.ptr, nbytes, None))
+    native.check(lib.m4d_device_sync(0))
+    got_b = np.frombuffer(native.to_host(bounds.ptr, (buckets + 1) * 8), dtype=np.int64)
+    pairs = np.frombuffer(native.to_host(out.ptr, n * 16), dtype=np.int64).reshape(n, 2)
+    h = oracle.splitmix64_np(keys.view(np.uint64))
+    bucket = ((h & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - int(np.log2(buckets)))).astype(np.int64)
+    want_b = np.concatenate([[0], np.cumsum(np.bincount(bucket, minlength=buckets))])
+    assert np.array_equal(got_b, want_b)
+    assert np.array_equal(np.sort(pairs[:, 1]), vals)  # a permutation of the rows
+    pb = bucket[pairs[:, 1]]
+    assert np.all(np.diff(pb) >= 0)  # grouped by bucket, in bucket order
+    assert np.array_equal(pairs[:, 0], keys[pairs[:, 1]])
