@@ -37,6 +37,8 @@ constexpr int kRowsPerThread = 8;        // rows each thread loads before using 
 constexpr int kMaxBuckets = 16384;       // single-pass partition limit (shared-memory counters)
 constexpr int kMaxParts = 1 << 16;       // two-pass LOCAL partition limit (128 KB of 16-bit counters)
 constexpr int kSinglePassMax = 256;      // LOCAL above this: two passes (L2 write frontier)
+constexpr int kMaxGroups = 8;            // pass-2 CTA groups per segment (per-group histograms)
+constexpr int kPass2Groups = 8;  // measured: pass 2 0.88 -> 0.81 ms at 1e8 rows (tools/km_pass2_groups.sh)
 constexpr int kJoinThreads = 1024;
 constexpr int kSlotBits = 14;
 constexpr int kSlots = 1 << kSlotBits;
@@ -356,12 +358,13 @@ __global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int
 template <bool kPacked>
 __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__ keys,
                                                      const int64_t* __restrict__ vals, int64_t n, int64_t run,
-                                                     int log2b, int b1, uint32_t* __restrict__ hist_top,
-                                                     unsigned long long* __restrict__ hist_all) {
+                                                     int log2b, int b1, int groups, uint32_t* __restrict__ hist_top,
+                                                     unsigned long long* __restrict__ hist_grp) {
     extern __shared__ uint32_t h2[];  // 2^log2b 16-bit counters
     __shared__ uint32_t top[256];
     __shared__ int overflow;
     const int buckets = 1 << log2b;
+    unsigned long long* hist_all = hist_grp + static_cast<int64_t>(blockIdx.x * groups / gridDim.x) * buckets;
     const int words = kPacked ? (buckets + 1) / 2 : buckets;
     const int shift = log2b - b1;
     for (int w = threadIdx.x; w < words; w += blockDim.x) h2[w] = 0;
@@ -415,6 +418,20 @@ __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__
         hist_top[static_cast<int64_t>(t) * gridDim.x + blockIdx.x] = top[t];
 }
 
+// hist_grp[g][b] -> counts of the groups before g (exclusive over g); hist_all[b] = total.
+__global__ void group_prefix_kernel(unsigned long long* __restrict__ hist_grp, int groups, int buckets,
+                                    unsigned long long* __restrict__ hist_all) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < buckets; b += gridDim.x * blockDim.x) {
+        unsigned long long run = 0;
+        for (int g = 0; g < groups; ++g) {
+            const unsigned long long c = hist_grp[static_cast<int64_t>(g) * buckets + b];
+            hist_grp[static_cast<int64_t>(g) * buckets + b] = run;
+            run += c;
+        }
+        hist_all[b] = run;
+    }
+}
+
 __global__ void exclusive_scan_u64_kernel(const unsigned long long* __restrict__ v, int n, int64_t* __restrict__ out,
                                           int64_t total) {
     // one CTA of 1024 threads; n <= 65536
@@ -453,15 +470,29 @@ __global__ void exclusive_scan_u64_kernel(const unsigned long long* __restrict__
     if (t == 0) out[n] = total;
 }
 
-__global__ void __launch_bounds__(1024) scatter_pass2_kernel(const longlong2* __restrict__ in,
-                                                             const int64_t* __restrict__ bounds, int log2b, int b1,
-                                                             longlong2* __restrict__ out) {
+// Pass 2: one CTA per (segment, group of pass-1 CTAs).  Within a segment the
+// rows of one group are contiguous, and the group's cursors start at the
+// partition bounds plus the counts of the earlier groups (from the per-group
+// histograms), so groups scatter independently and rows keep their order.
+// fan x groups CTAs instead of fan (256 CTAs of 1024 threads ran in 1.7
+// waves on 148 SMs).
+__global__ void __launch_bounds__(1024)
+    scatter_pass2_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ offs, int ctas, int64_t n,
+                         const unsigned long long* __restrict__ grp_before, int groups,
+                         const int64_t* __restrict__ bounds, int log2b, int b1, longlong2* __restrict__ out) {
     extern __shared__ uint32_t cursor[];  // 2^(log2b - b1)
     const int sub = 1 << (log2b - b1);
-    const int seg = blockIdx.x;
-    for (int k = threadIdx.x; k < sub; k += blockDim.x) cursor[k] = static_cast<uint32_t>(bounds[seg * sub + k]);
+    const int seg = blockIdx.x / groups, g = blockIdx.x % groups;
+    const int buckets = 1 << log2b;
+    for (int k = threadIdx.x; k < sub; k += blockDim.x) {
+        const int b = seg * sub + k;
+        cursor[k] = static_cast<uint32_t>(bounds[b] + static_cast<int64_t>(grp_before[static_cast<int64_t>(g) * buckets + b]));
+    }
     __syncthreads();
-    const int64_t lo = bounds[seg * sub], hi = bounds[(seg + 1) * sub];
+    const int k0 = (g * ctas + groups - 1) / groups, k1 = ((g + 1) * ctas + groups - 1) / groups;
+    const int64_t entries = static_cast<int64_t>(ctas) << b1;
+    const int64_t i0 = static_cast<int64_t>(seg) * ctas + k0, i1 = static_cast<int64_t>(seg) * ctas + k1;
+    const int64_t lo = i0 < entries ? offs[i0] : n, hi = i1 < entries ? offs[i1] : n;
     const uint32_t mask = sub - 1;
     for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
         longlong2 row[kRowsPerThread];
@@ -686,8 +717,8 @@ size_t m4d_partition_scratch_bytes(int64_t n, int buckets) {
     const int64_t entries = ctas * fan;
     const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
     size_t bytes = entries * sizeof(uint32_t) + entries * sizeof(int64_t) + (tiles + 1) * sizeof(int64_t) + 512;
-    if (buckets > kSinglePassMax)  // global histogram + pass-1 pairs
-        bytes += buckets * sizeof(unsigned long long) + 256 + static_cast<size_t>(n) * 16 + 256;
+    if (buckets > kSinglePassMax)  // per-group + global histograms, pass-1 pairs
+        bytes += (kMaxGroups + 1) * (buckets * sizeof(unsigned long long) + 256) + static_cast<size_t>(n) * 16 + 256;
     return bytes;
 }
 
@@ -718,15 +749,22 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         base += ((entries + tiles + 1) * sizeof(int64_t) + 255) & ~size_t(255);
         unsigned long long* hist_all = reinterpret_cast<unsigned long long*>(base);
         base += (buckets * sizeof(unsigned long long) + 255) & ~size_t(255);
+        unsigned long long* hist_grp = reinterpret_cast<unsigned long long*>(base);
+        base += (kMaxGroups * buckets * sizeof(unsigned long long) + 255) & ~size_t(255);
         longlong2* tmp = reinterpret_cast<longlong2*>(base);
+        static const int groups = [] {
+            const char* v = getenv("M4D_PASS2_GROUPS");
+            const int g = v ? atoi(v) : kPass2Groups;
+            return g < 1 ? 1 : g > kMaxGroups ? kMaxGroups : g;
+        }();
         const bool packed = buckets > (1 << 15);
         const size_t hist_smem = packed ? (buckets + 1) / 2 * sizeof(uint32_t) : buckets * sizeof(uint32_t);
         M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 2));
         M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 2));
         M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
-        M4D_CUDA_TRY(cudaMemsetAsync(hist_all, 0, buckets * sizeof(unsigned long long), s));
+        M4D_CUDA_TRY(cudaMemsetAsync(hist_grp, 0, groups * buckets * sizeof(unsigned long long), s));
         (packed ? hist2_kernel<true> : hist2_kernel<false>)<<<ctas, 1024, hist_smem, s>>>(keys, vals, n, run, log2b, b1,
-                                                                                        hist, hist_all);
+                                                                                        groups, hist, hist_grp);
         scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
         scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
         scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
@@ -734,9 +772,10 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         M4D_CUDA_TRY(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           static_cast<int>(kTileSmem)));
         tile_scatter_kernel<<<ctas, kHistThreads, kTileSmem, s>>>(keys, vals, n, run, M4D_PART_LOCAL, fan, b1, offs, tmp);
+        group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, groups, buckets, hist_all);
         exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
-        scatter_pass2_kernel<<<fan, 1024, (buckets >> b1) * sizeof(uint32_t), s>>>(
-            tmp, bounds, log2b, b1, reinterpret_cast<longlong2*>(out_pairs));
+        scatter_pass2_kernel<<<fan * groups, 1024, (buckets >> b1) * sizeof(uint32_t), s>>>(
+            tmp, offs, ctas, n, hist_grp, groups, bounds, log2b, b1, reinterpret_cast<longlong2*>(out_pairs));
         M4D_CUDA_TRY(cudaGetLastError());
         return M4D_OK;
     }
@@ -770,7 +809,7 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
     return M4D_OK;
 }
 
-int m4d_partition_launches(int buckets) { return buckets > kSinglePassMax ? 8 : 6; }
+int m4d_partition_launches(int buckets) { return buckets > kSinglePassMax ? 9 : 6; }
 
 m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const int64_t* rpairs,
                          const int64_t* rbounds, int parts, int64_t* out_keys, int64_t* out_lvals,
