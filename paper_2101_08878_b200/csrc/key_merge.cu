@@ -40,14 +40,19 @@ constexpr int kSinglePassMax = 256;      // LOCAL above this: two passes (L2 wri
 constexpr int kMaxGroups = 8;            // pass-2 CTA groups per segment (per-group histograms)
 constexpr int kPass2Groups = 8;  // measured: pass 2 0.88 -> 0.81 ms at 1e8 rows (tools/km_pass2_groups.sh)
 constexpr int kJoinThreads = 1024;
-constexpr int kSlotBits = 14;
+constexpr int kSlotBits = 14;                 // 16384 chain heads
 constexpr int kSlots = 1 << kSlotBits;
-constexpr int kChunk = kSlots * 3 / 4;
+constexpr int kChunk = 12288;                 // build rows per table (keys + links in shared memory)
+constexpr int kIdxBits = 14;                  // build row index within a chunk
 constexpr uint32_t kEmpty = 0xffffffffu;
+constexpr uint16_t kNil = 0xffffu;
 constexpr int kStage = 256;  // staged matches per warp per emit round
 constexpr int kJoinPer = 4;   // probe / build rows per thread per batch (4096 rows per batch)
-constexpr size_t kJoinSmem = kSlots * (sizeof(int64_t) + sizeof(uint32_t)) + (kJoinThreads / 32) * kStage * sizeof(uint32_t);
-static_assert(kSlotBits + 12 <= 32 && kJoinThreads * kJoinPer <= (1 << 12), "stage entry packing");
+constexpr size_t kJoinSmem = kSlots * sizeof(uint32_t) + kChunk * (sizeof(int64_t) + sizeof(uint16_t)) +
+                             (kJoinThreads / 32) * kStage * sizeof(uint32_t);
+static_assert(kChunk < (1 << kIdxBits) && kIdxBits + 12 <= 32 && kJoinThreads * kJoinPer <= (1 << 12),
+              "stage entry packing");
+static_assert(kJoinSmem <= 227 * 1024, "join shared memory");
 
 __device__ __forceinline__ uint32_t bucket_of(int64_t key, int mode, int buckets, int log2b) {
     const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(key));
@@ -517,30 +522,35 @@ __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int bu
         bounds[b] = b < buckets ? offsets[static_cast<int64_t>(b) * ctas] : total;
 }
 
-// One CTA per partition: build an open-addressing table of the left rows in
-// shared memory (chunks of kChunk rows), then probe with the right rows in
-// batches of kJoinThreads * kJoinPer.  The probe phase is warp-independent
-// (no block barriers): (1) each thread walks its rows' chains once, keeping
-// per row the first matching slot and the match count; (2) a warp scan plus
-// one global atomic per warp reserves the warp's output range; (3) each
-// thread writes its matches as packed (row, slot) entries into the warp's
-// stage (re-walking only rows with several matches); (4) the warp emits the
-// stage with all 32 lanes: coalesced output stores, full-width row hashes.
+// One CTA per partition: a chained hash table of the left rows in shared
+// memory (chunks of kChunk rows): 16384 chain heads, the chunk's keys and one
+// 16-bit link per row.  Inserting is one atomicExch per row (no probing
+// loops); a probe walks only the rows that share its head, Poisson(rows /
+// 16384) long, so lanes of a warp finish together (linear probing at the same
+// load ran ~6 divergent steps per warp for ~1.2 per row).  The right rows
+// stream through in batches of kJoinThreads * kJoinPer, warp-independently:
+// (1) each thread walks its rows' chains once, keeping per row the first
+// matching build row and the match count; (2) a warp scan plus one global
+// atomic per warp reserves the warp's output range; (3) each thread writes its
+// matches as packed (probe row, build row) entries into the warp's stage
+// (re-walking only rows with several matches); (4) the warp emits the stage
+// with all 32 lanes: coalesced output stores, full-width row hashes.
 // Indices are 32-bit offsets from the partition start.
 __global__ void __launch_bounds__(kJoinThreads, 1)
     join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
                 const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
                 int64_t* __restrict__ ol, int64_t* __restrict__ orr, int64_t capacity,
                 unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ digest) {
-    extern __shared__ unsigned char smem[];
-    int64_t* tkey = reinterpret_cast<int64_t*>(smem);
-    uint32_t* tidx = reinterpret_cast<uint32_t*>(smem + kSlots * sizeof(int64_t));
+    extern __shared__ __align__(16) unsigned char smem[];
+    int64_t* bkey = reinterpret_cast<int64_t*>(smem);                                   // [kChunk]
+    uint32_t* head = reinterpret_cast<uint32_t*>(smem + kChunk * sizeof(int64_t));      // [kSlots]
+    uint16_t* link = reinterpret_cast<uint16_t*>(head + kSlots);                        // [kChunk]
+    uint32_t* stage_all = reinterpret_cast<uint32_t*>(link + kChunk);
     __shared__ unsigned long long red[kJoinThreads / 32][3];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int T = kJoinThreads;
     constexpr int kPer = kJoinPer;
-    constexpr uint32_t kMask = kSlots - 1;
-    uint32_t* stage = tidx + kSlots + warp * kStage;
+    uint32_t* stage = stage_all + warp * kStage;
     const longlong2* brow = build + loff[blockIdx.x];
     const longlong2* prow = probe + roff[blockIdx.x];
     if (loff[blockIdx.x + 1] - loff[blockIdx.x] > INT32_MAX || roff[blockIdx.x + 1] - roff[blockIdx.x] > INT32_MAX)
@@ -552,7 +562,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
         const int cn = bn - c0 < kChunk ? bn - c0 : kChunk;
         const longlong2* crow = brow + c0;
         if (c0) __syncthreads();  // every warp is done probing the previous chunk's table
-        for (int s = threadIdx.x; s < kSlots; s += T) tidx[s] = kEmpty;
+        for (int s = threadIdx.x; s < kSlots; s += T) head[s] = kEmpty;
         __syncthreads();
         for (int base = 0; base < cn; base += T * kPer) {
             int64_t k[kPer];
@@ -565,9 +575,9 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
             for (int u = 0; u < kPer; ++u) {
                 const int i = base + u * T + threadIdx.x;
                 if (i >= cn) break;  // rows ascend with u
-                uint32_t s = slot_of(k[u]);
-                while (atomicCAS(&tidx[s], kEmpty, static_cast<uint32_t>(i)) != kEmpty) s = (s + 1) & kMask;
-                tkey[s] = k[u];
+                bkey[i] = k[u];
+                const uint32_t old = atomicExch(&head[slot_of(k[u])], static_cast<uint32_t>(i));
+                link[i] = old == kEmpty ? kNil : static_cast<uint16_t>(old);
             }
         }
         __syncthreads();
@@ -578,16 +588,17 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                 const int j = base + u * T + threadIdx.x;
                 r[u] = j < pn ? prow[j].x : 0;
             }
-            uint32_t info[kPer];  // first matching slot | min(matches, 0xffff) << 16
+            uint32_t info[kPer];  // first matching build row | min(matches, 0xffff) << 16
             uint32_t mine = 0;
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {  // (1) count
                 info[u] = 0;
                 if (base + u * T + static_cast<int>(threadIdx.x) >= pn) continue;
                 uint32_t c = 0, first = 0;
-                for (uint32_t s = slot_of(r[u]); tidx[s] != kEmpty; s = (s + 1) & kMask)
-                    if (tkey[s] == r[u]) {
-                        first = c ? first : s;
+                const uint32_t h0 = head[slot_of(r[u])];
+                for (uint32_t i = h0 == kEmpty ? kNil : h0; i != kNil; i = link[i])
+                    if (bkey[i] == r[u]) {
+                        first = c ? first : i;
                         ++c;
                     }
                 info[u] = first | (c < 0xffffu ? c : 0xffffu) << 16;
@@ -612,16 +623,16 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                     for (int u = 0; u < kPer; ++u) {
                         const uint32_t c = info[u] >> 16;
                         if (!c) continue;
-                        const uint32_t loc = static_cast<uint32_t>(u * T + threadIdx.x) << kSlotBits;
+                        const uint32_t loc = static_cast<uint32_t>(u * T + threadIdx.x) << kIdxBits;
                         const uint32_t first = info[u] & 0xffffu;
                         if (c == 1) {
                             if (e >= win && e < win + kStage) stage[e - win] = loc | first;
                             ++e;
                             continue;
                         }
-                        for (uint32_t s = first; tidx[s] != kEmpty; s = (s + 1) & kMask) {
-                            if (tkey[s] != r[u]) continue;
-                            if (e >= win && e < win + kStage) stage[e - win] = loc | s;
+                        for (uint32_t i = first; i != kNil; i = link[i]) {
+                            if (bkey[i] != r[u]) continue;
+                            if (e >= win && e < win + kStage) stage[e - win] = loc | i;
                             ++e;
                         }
                     }
@@ -630,10 +641,10 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                 const uint32_t n = warp_total - win < kStage ? warp_total - win : kStage;
                 for (uint32_t q = lane; q < n; q += 32) {  // (4) emit, all lanes
                     const uint32_t ent = stage[q];
-                    const uint32_t s = ent & kMask;
-                    const int64_t key = tkey[s];
-                    const int64_t l = crow[tidx[s]].y;
-                    const int64_t rv = prow[base + static_cast<int>(ent >> kSlotBits)].y;
+                    const uint32_t i = ent & ((1u << kIdxBits) - 1);
+                    const int64_t key = bkey[i];
+                    const int64_t l = crow[i].y;
+                    const int64_t rv = prow[base + static_cast<int>(ent >> kIdxBits)].y;
                     const unsigned long long pos = wbase + win + q;
                     if (static_cast<int64_t>(pos) < capacity) {
                         ok[pos] = key;
