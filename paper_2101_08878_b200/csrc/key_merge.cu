@@ -42,7 +42,7 @@ constexpr int kPass2Groups = 8;  // measured: pass 2 0.88 -> 0.81 ms at 1e8 rows
 constexpr int kJoinThreads = 1024;
 constexpr int kSlotBits = 14;                 // 16384 chain heads
 constexpr int kSlots = 1 << kSlotBits;
-constexpr int kChunk = 12288;                 // build rows per table (keys + links in shared memory)
+constexpr int kChunk = 13000;                 // build rows per table (keys + links in shared memory)
 constexpr int kIdxBits = 14;                  // build row index within a chunk
 constexpr uint32_t kEmpty = 0xffffffffu;
 constexpr uint16_t kNil = 0xffffu;

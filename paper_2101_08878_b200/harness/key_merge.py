@@ -58,7 +58,7 @@ def choose_parts(rows: int) -> int:
     """Power-of-two partition count with ~1.5K rows per partition (8192-slot shared tables,
     load <= 0.19, two join CTAs per SM), at most 65536."""
     parts = 1
-    while parts < 65536 and rows / parts > 6200:
+    while parts < 65536 and rows / parts > 12400:
         parts *= 2
     return parts
 
