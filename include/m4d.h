@@ -221,8 +221,21 @@ int m4d_ts_launches_per_run(const m4d_ts_plan* plan);
 
 enum {
     M4D_PART_LOCAL = 0,  /* bucket = (h & 0xffffffff) >> (32 - log2 buckets), h = splitmix64(key) */
-    M4D_PART_RANK = 1    /* bucket = owner rank = (uint32(h >> 32) * buckets) >> 32               */
+    M4D_PART_RANK = 1,   /* bucket = owner rank = (uint32(h >> 32) * buckets) >> 32               */
+    M4D_PART_OWNER_COARSE = 2  /* bucket = owner rank * C + the top log2 C bits of the LOCAL id
+                                  (m4d_partition_owner_coarse only) */
 };
+
+/* Largest power of two C with world * C <= 256 (the owner+coarse fan-out). */
+int m4d_owner_coarse_count(int world);
+/* One pass that both routes rows to their owner rank (as M4D_PART_RANK with
+ * `world` buckets) and performs the owner's first local pass: bucket = owner *
+ * coarse + the top log2(coarse) bits of the LOCAL partition id (coarse a power
+ * of two, world * coarse <= 256).  bounds[] gets world * coarse + 1 entries;
+ * scratch as m4d_partition_scratch_bytes(n, world * coarse). */
+m4d_status m4d_partition_owner_coarse(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
+                                      int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
+                                      void* stream);
 
 /* Table generator: keys[i] = band + splitmix64(seed + row0 + i) % total,
  * vals[i] = row0 + i (the global row index). */
@@ -239,6 +252,17 @@ size_t m4d_partition_scratch_bytes(int64_t n, int buckets);
 m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
                          int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
                          void* stream);
+/* Receiver side of an M4D_PART_OWNER_COARSE exchange: in_pairs holds `sources`
+ * segments, each made of `coarse` runs in coarse-bucket order; runs_host (host
+ * memory, int64[coarse][sources][2]) gives each run's [start, end) row in
+ * in_pairs.  Writes the rows split into `buckets` LOCAL partitions (power of
+ * two <= 32768, coarse dividing it) to out_pairs and bounds[buckets + 1]
+ * (device); within a partition rows keep source order.  Launches sources + 3
+ * kernels. */
+m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t* runs_host, int coarse, int sources,
+                              int buckets, int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
+                              void* stream);
+size_t m4d_partition_runs_scratch_bytes(int sources, int buckets, int coarse);
 /* Kernel launches (plus memsets) one m4d_partition call issues for that bucket count. */
 int m4d_partition_launches(int buckets);
 /* Inner join of partitioned build (left) and probe (right) pair arrays,

@@ -54,10 +54,15 @@ static_assert(kChunk < (1 << kIdxBits) && kIdxBits + 12 <= 32 && kJoinThreads * 
               "stage entry packing");
 static_assert(kJoinSmem <= 227 * 1024, "join shared memory");
 
+// mode LOCAL: log2b bits of the low word; RANK: owner of `buckets` ranks;
+// OWNER_COARSE: owner of buckets >> log2b ranks, then log2b low-word bits.
 __device__ __forceinline__ uint32_t bucket_of(int64_t key, int mode, int buckets, int log2b) {
     const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(key));
+    const uint32_t low = log2b ? static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) : 0u;
     if (mode == M4D_PART_RANK) return __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(buckets));
-    return log2b ? static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) : 0u;
+    if (mode == M4D_PART_OWNER_COARSE)
+        return __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(buckets >> log2b)) << log2b | low;
+    return low;
 }
 
 // Shared-table slot: a 32-bit multiplicative hash of the folded key (cheap;
@@ -516,6 +521,69 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
+// Receiver side of the owner+coarse exchange (M4D_PART_OWNER_COARSE): S
+// source segments, each holding C coarse runs in bucket order, are split into
+// the final 2^log2b partitions.  Per-source full-id histograms (one pass over
+// the keys) give every (coarse run, source) CTA its cursors: partition bounds
+// plus the counts of earlier sources, so rows stay source-ordered.
+__global__ void __launch_bounds__(1024) hist_fine_kernel(const longlong2* __restrict__ in, int64_t lo, int64_t hi,
+                                                         int64_t run, int log2b,
+                                                         unsigned long long* __restrict__ out) {
+    extern __shared__ uint32_t h[];
+    const int buckets = 1 << log2b;
+    for (int b = threadIdx.x; b < buckets; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    const int64_t a = lo + blockIdx.x * run, z = a + run < hi ? a + run : hi;
+    for (int64_t base = a; base < z; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+        int64_t k[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            k[u] = i < z ? in[i].x : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u)
+            if (base + u * blockDim.x + threadIdx.x < z)
+                atomicAdd(&h[bucket_of(k[u], M4D_PART_LOCAL, buckets, log2b)], 1u);
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < buckets; b += blockDim.x)
+        if (h[b]) atomicAdd(out + b, static_cast<unsigned long long>(h[b]));
+}
+
+__global__ void __launch_bounds__(1024)
+    runs_pass2_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ runs, int sources,
+                      const unsigned long long* __restrict__ src_before, const int64_t* __restrict__ bounds,
+                      int log2b, int cbits, longlong2* __restrict__ out) {
+    extern __shared__ uint32_t cursor[];  // 2^(log2b - cbits)
+    const int sub = 1 << (log2b - cbits);
+    const int c = blockIdx.x / sources, src = blockIdx.x % sources;
+    const int buckets = 1 << log2b;
+    for (int k = threadIdx.x; k < sub; k += blockDim.x) {
+        const int b = c * sub + k;
+        cursor[k] = static_cast<uint32_t>(bounds[b] +
+                                          static_cast<int64_t>(src_before[static_cast<int64_t>(src) * buckets + b]));
+    }
+    __syncthreads();
+    const int64_t lo = runs[2 * blockIdx.x], hi = runs[2 * blockIdx.x + 1];
+    const uint32_t mask = sub - 1;
+    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+        longlong2 row[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            if (i < hi) row[u] = __ldcs(in + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            if (base + u * blockDim.x + threadIdx.x >= hi) continue;
+            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(row[u].x));
+            const uint32_t b2 = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) & mask;
+            out[atomicAdd(&cursor[b2], 1u)] = row[u];
+        }
+    }
+}
+
 __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int buckets, int ctas, int64_t total,
                                      int64_t* __restrict__ bounds) {
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= buckets; b += gridDim.x * blockDim.x)
@@ -698,6 +766,55 @@ int log2_exact(int v) {
 
 using m4d::fail;
 
+static int partition_ctas(int64_t n) {
+    // <= 2 resident CTAs per SM: the scatter's L2 write frontier must fit (see top).
+    const int64_t per = 65536;
+    int64_t c = (n + per - 1) / per;
+    if (c < 1) c = 1;
+    if (c > 148 * 2) c = 148 * 2;
+    return static_cast<int>(c);
+}
+
+static int pass1_bits(int log2b) { return log2b > 8 ? 8 : log2b; }
+
+// Single-pass partition (hist -> scan -> scatter) into `buckets` buckets; the
+// bucket function gets (mode, buckets, log2b) as bucket_of documents.
+static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
+                                   int log2b, int64_t* out_pairs, int64_t* bounds, void* scratch,
+                                   size_t scratch_bytes, cudaStream_t s) {
+    if (scratch_bytes < m4d_partition_scratch_bytes(n, buckets)) return fail(M4D_ERR_USAGE, "partition scratch too small");
+    const int ctas = partition_ctas(n);
+    const int64_t run = (n + ctas - 1) / ctas;
+    if (buckets > kMaxBuckets) return fail(M4D_ERR_USAGE, "bucket count %d above the single-pass limit", buckets);
+    const int64_t entries = static_cast<int64_t>(ctas) * buckets;
+    const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
+    uint32_t* hist = static_cast<uint32_t*>(scratch);
+    int64_t* offs = reinterpret_cast<int64_t*>(static_cast<char*>(scratch) + ((entries * sizeof(uint32_t) + 255) & ~size_t(255)));
+    int64_t* tile_sums = offs + entries;
+    int64_t* total = tile_sums + tiles;
+    const size_t hist_smem = buckets * sizeof(uint32_t);
+    const size_t cur_smem = buckets * sizeof(uint32_t);
+    // (per device; cheap enough to repeat on every call)
+    M4D_CUDA_TRY(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
+    M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
+    hist_kernel<<<ctas, kHistThreads, hist_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, hist);
+    scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
+    scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
+    scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
+    if (buckets <= kTileBuckets) {
+        M4D_CUDA_TRY(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(kTileSmem)));
+        tile_scatter_kernel<<<ctas, kHistThreads, kTileSmem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+                                                                  reinterpret_cast<longlong2*>(out_pairs));
+    } else {
+        scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+                                                            reinterpret_cast<longlong2*>(out_pairs));
+    }
+    bucket_bounds_kernel<<<(buckets + 256) / 256, 256, 0, s>>>(offs, buckets, ctas, n, bounds);
+    M4D_CUDA_TRY(cudaGetLastError());
+    return M4D_OK;
+}
+
 extern "C" {
 
 m4d_status m4d_merge_generate(int64_t* keys, int64_t* vals, int64_t row0, int64_t count, uint64_t total,
@@ -711,16 +828,11 @@ m4d_status m4d_merge_generate(int64_t* keys, int64_t* vals, int64_t row0, int64_
     return M4D_OK;
 }
 
-static int partition_ctas(int64_t n) {
-    // <= 2 resident CTAs per SM: the scatter's L2 write frontier must fit (see top).
-    const int64_t per = 65536;
-    int64_t c = (n + per - 1) / per;
-    if (c < 1) c = 1;
-    if (c > 148 * 2) c = 148 * 2;
-    return static_cast<int>(c);
+int m4d_owner_coarse_count(int world) {
+    int c = 1;
+    while (world > 0 && world * c * 2 <= 256) c *= 2;
+    return c;
 }
-
-static int pass1_bits(int log2b) { return log2b > 8 ? 8 : log2b; }
 
 size_t m4d_partition_scratch_bytes(int64_t n, int buckets) {
     const int64_t ctas = partition_ctas(n);
@@ -736,6 +848,7 @@ size_t m4d_partition_scratch_bytes(int64_t n, int buckets) {
 m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
                          int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes, void* stream) {
     if (n < 0 || n >= (int64_t(1) << 32)) return fail(M4D_ERR_USAGE, "partition of %lld rows outside [0, 2^32)", (long long)n);
+    if (mode == M4D_PART_OWNER_COARSE) return fail(M4D_ERR_USAGE, "owner+coarse partitions go through m4d_partition_owner_coarse");
     const int log2b = log2_exact(buckets);
     const bool two_pass = mode == M4D_PART_LOCAL && buckets > kSinglePassMax;
     if (n < 0 || buckets < 1 || buckets > (mode == M4D_PART_LOCAL ? kMaxParts : kMaxBuckets))
@@ -790,32 +903,59 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         M4D_CUDA_TRY(cudaGetLastError());
         return M4D_OK;
     }
-    if (buckets > kMaxBuckets) return fail(M4D_ERR_USAGE, "bucket count %d above the single-pass limit", buckets);
-    const int64_t entries = static_cast<int64_t>(ctas) * buckets;
-    const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
-    uint32_t* hist = static_cast<uint32_t*>(scratch);
-    int64_t* offs = reinterpret_cast<int64_t*>(static_cast<char*>(scratch) + ((entries * sizeof(uint32_t) + 255) & ~size_t(255)));
-    int64_t* tile_sums = offs + entries;
-    int64_t* total = tile_sums + tiles;
-    const size_t hist_smem = buckets * sizeof(uint32_t);
-    const size_t cur_smem = buckets * sizeof(uint32_t);
-    // (per device; cheap enough to repeat on every call)
-    M4D_CUDA_TRY(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
-    M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
-    hist_kernel<<<ctas, kHistThreads, hist_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, hist);
-    scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
-    scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
-    scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
-    if (buckets <= kTileBuckets) {
-        M4D_CUDA_TRY(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kTileSmem)));
-        tile_scatter_kernel<<<ctas, kHistThreads, kTileSmem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
-                                                                  reinterpret_cast<longlong2*>(out_pairs));
-    } else {
-        scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
-                                                            reinterpret_cast<longlong2*>(out_pairs));
+    return partition_single(keys, vals, n, mode, buckets, log2b, out_pairs, bounds, scratch, scratch_bytes, s);
+}
+
+m4d_status m4d_partition_owner_coarse(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
+                                      int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
+                                      void* stream) {
+    if (n < 0 || n >= (int64_t(1) << 32)) return fail(M4D_ERR_USAGE, "partition of %lld rows outside [0, 2^32)", (long long)n);
+    if (world < 1 || world > 256) return fail(M4D_ERR_USAGE, "owner count %d outside [1, 256]", world);
+    const int cbits = log2_exact(coarse);
+    if (cbits < 0 || world * coarse > 256) return fail(M4D_ERR_USAGE, "coarse count %d invalid for %d owners", coarse, world);
+    return partition_single(keys, vals, n, M4D_PART_OWNER_COARSE, world * coarse, cbits, out_pairs, bounds, scratch,
+                            scratch_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t m4d_partition_runs_scratch_bytes(int sources, int buckets, int coarse) {
+    if (sources < 1 || buckets < 1 || coarse < 1) return 0;
+    return (static_cast<size_t>(sources) + 1) * buckets * sizeof(unsigned long long) +
+           2 * static_cast<size_t>(coarse) * sources * sizeof(int64_t) + 1024;
+}
+
+m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t* runs_host, int coarse, int sources,
+                              int buckets, int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
+                              void* stream) {
+    const int log2b = log2_exact(buckets), cbits = log2_exact(coarse);
+    if (n < 0 || n >= (int64_t(1) << 32)) return fail(M4D_ERR_USAGE, "partition of %lld rows outside [0, 2^32)", (long long)n);
+    if (log2b < 0 || buckets > (1 << 15)) return fail(M4D_ERR_USAGE, "partition count %d must be a power of two <= 32768", buckets);
+    if (cbits < 0 || coarse > buckets || coarse > 256) return fail(M4D_ERR_USAGE, "coarse run count %d invalid", coarse);
+    if (sources < 1 || sources > 256) return fail(M4D_ERR_USAGE, "source count %d outside [1, 256]", sources);
+    if (scratch_bytes < m4d_partition_runs_scratch_bytes(sources, buckets, coarse))
+        return fail(M4D_ERR_USAGE, "partition scratch too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* base = static_cast<char*>(scratch);
+    unsigned long long* src_cnt = reinterpret_cast<unsigned long long*>(base);       // [sources][buckets]
+    unsigned long long* hist_all = src_cnt + static_cast<int64_t>(sources) * buckets;  // [buckets]
+    int64_t* runs = reinterpret_cast<int64_t*>(hist_all + buckets);                   // [coarse * sources][2]
+    const size_t run_bytes = 2 * static_cast<size_t>(coarse) * sources * sizeof(int64_t);
+    M4D_CUDA_TRY(cudaMemcpyAsync(runs, runs_host, run_bytes, cudaMemcpyHostToDevice, s));
+    M4D_CUDA_TRY(cudaMemsetAsync(src_cnt, 0, static_cast<size_t>(sources) * buckets * sizeof(unsigned long long), s));
+    M4D_CUDA_TRY(cudaFuncSetAttribute(hist_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (1 << 15) * 4));
+    for (int src = 0; src < sources; ++src) {
+        const int64_t lo = runs_host[2 * src], hi = runs_host[2 * ((coarse - 1) * sources + src) + 1];
+        if (hi <= lo) continue;
+        const int grid = partition_ctas(hi - lo);
+        const int64_t run = (hi - lo + grid - 1) / grid;
+        hist_fine_kernel<<<grid, 1024, buckets * sizeof(uint32_t), s>>>(reinterpret_cast<const longlong2*>(in_pairs),
+                                                                         lo, hi, run, log2b,
+                                                                         src_cnt + static_cast<int64_t>(src) * buckets);
     }
-    bucket_bounds_kernel<<<(buckets + 256) / 256, 256, 0, s>>>(offs, buckets, ctas, n, bounds);
+    group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(src_cnt, sources, buckets, hist_all);
+    exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
+    runs_pass2_kernel<<<coarse * sources, 1024, (buckets >> cbits) * sizeof(uint32_t), s>>>(
+        reinterpret_cast<const longlong2*>(in_pairs), runs, sources, src_cnt, bounds, log2b, cbits,
+        reinterpret_cast<longlong2*>(out_pairs));
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }

@@ -44,8 +44,8 @@ SEED_LEFT = 0x4C454654
 SEED_RIGHT = 0x52494748
 EXCHANGE_TAG = 900
 DATA_TAG = 910
-SHUFFLE_PULL_CTAS = 192  # total pull CTAs while the shuffle overlaps partition kernels, split over the
-                         # P-1 concurrent per-peer pulls (N=4: 64 each, 16.3 -> 14.2 ms; tools/km_pull_sweep.sh)
+SHUFFLE_PULL_CTAS = 192  # pull-kernel grid while the shuffle overlaps partition kernels (the transport
+                         # batches the per-peer messages of a side into one launch)
 _MASK64 = (1 << 64) - 1
 
 
@@ -107,9 +107,13 @@ class KeyMerge:
         self.recv = [_Pairs(device, slack), _Pairs(device, slack)] if world > 1 else None
         self.parted = [_Pairs(device, slack), _Pairs(device, slack)]
         self.bounds = [native.DeviceBuffer(device, (max(self.parts, world) + 1) * 8) for _ in range(2)]
-        self.rank_bounds = [native.DeviceBuffer(device, (world + 1) * 8) for _ in range(2)]
-        scratch = max(native.lib().m4d_partition_scratch_bytes(slack, self.parts),
-                      native.lib().m4d_partition_scratch_bytes(self.n, max(world, 1)))
+        lib = native.lib()
+        # owner + coarse buckets of the sender pass (SoA input -> P * C runs; C | parts)
+        self.coarse = min(lib.m4d_owner_coarse_count(world), self.parts) if world > 1 else 1
+        self.rank_bounds = [native.DeviceBuffer(device, (world * self.coarse + 1) * 8) for _ in range(2)]
+        scratch = max(lib.m4d_partition_scratch_bytes(slack, self.parts),
+                      lib.m4d_partition_scratch_bytes(self.n, max(world, 1) * self.coarse),
+                      lib.m4d_partition_runs_scratch_bytes(max(world, 1), self.parts, self.coarse))
         self.scratch = native.DeviceBuffer(device, scratch)
         self.scratch_bytes = scratch
         self.out_capacity = int(fraction * self.n * 1.25) + 65536
@@ -152,10 +156,16 @@ class KeyMerge:
         raw = native.to_host(buf.ptr, (count + 1) * 8, self.stream)
         return list(struct.unpack(f"<{count + 1}q", raw))
 
-    def _rank_split(self, side: int) -> list[int]:
-        """Partition one side by owner rank; returns the row bounds per destination (synchronises)."""
-        self._partition(self.inputs[side], self.n, 1, self.world, self.sendbuf[side], self.rank_bounds[side])
-        return self._read_bounds(self.rank_bounds[side], self.world)
+    def _owner_split(self, side: int) -> list[int]:
+        """One pass over one side's columns: rows grouped by (owner rank, top bits of their
+        local partition), i.e. routed to their owner and already through the owner's first
+        local pass.  Returns the P * C + 1 bucket bounds (synchronises)."""
+        P, C = self.world, self.coarse
+        native.check(native.lib().m4d_partition_owner_coarse(
+            self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.sendbuf[side].ptr,
+            self.rank_bounds[side].ptr, self.scratch.ptr, self.scratch_bytes, self.stream.handle))
+        self.launches += native.lib().m4d_partition_launches(P * C)
+        return self._read_bounds(self.rank_bounds[side], P * C)
 
     def _post_side(self, side: int, sends: list[int], incoming: list[int]) -> list:
         """Post one side's exchange: pulls of every peer's segment (device frames over NVLink)
@@ -186,33 +196,53 @@ class KeyMerge:
         t.progress()  # match what already arrived: the pulls start now, on the transport's streams
         return reqs
 
-    async def _exchange_side(self, side: int) -> tuple[list, int]:
-        t, P, me = self.transport, self.world, self.rank
-        sends = self._rank_split(side)  # synchronises: the send buffer is complete before peers pull
-        counts = [sends[d + 1] - sends[d] for d in range(P)]
-        table = [struct.unpack(f"<{P}q", b) for b in await allgather(t, struct.pack(f"<{P}q", *counts),
-                                                                         EXCHANGE_TAG + 2 + side)]
-        incoming = [table[src][me] for src in range(P)]
-        return self._post_side(side, sends, incoming), sum(incoming)
+    async def _exchange_side(self, side: int):
+        """Owner pass, run-table exchange and posting of one side's transfers."""
+        t, P, me, C = self.transport, self.world, self.rank, self.coarse
+        b = self._owner_split(side)  # synchronises: the send buffer is complete before peers pull
+        rel = [b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)]
+        table = [struct.unpack(f"<{P * (C + 1)}q", blob)
+                 for blob in await allgather(t, struct.pack(f"<{P * (C + 1)}q", *rel), EXCHANGE_TAG + 2 + side)]
+        runs_in = [table[src][me * (C + 1):(me + 1) * (C + 1)] for src in range(P)]  # my runs in each source
+        incoming = [r[C] for r in runs_in]
+        sends = [b[d * C] for d in range(P)] + [b[P * C]]
+        return self._post_side(side, sends, incoming), runs_in
+
+    def _finish_side(self, side: int, runs_in: list) -> int:
+        """Split the received source segments (each C coarse runs) into the local partitions."""
+        import numpy as np
+
+        P, C = self.world, self.coarse
+        starts = np.cumsum([0] + [r[C] for r in runs_in])
+        runs = np.empty((C, P, 2), dtype=np.int64)
+        for src, r in enumerate(runs_in):
+            for c in range(C):
+                runs[c, src] = (starts[src] + r[c], starts[src] + r[c + 1])
+        total = int(starts[-1])
+        native.check(native.lib().m4d_partition_runs(self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts,
+                                                     self.parted[side].ptr, self.bounds[side].ptr, self.scratch.ptr,
+                                                     self.scratch_bytes, self.stream.handle))
+        self.launches += P + 3
+        return total
 
     async def _shuffle_and_partition(self) -> list[int]:
-        """Owner-rank partition, NVLink exchange and local partition of both sides, pipelined:
-        side 1's rank partition runs while side 0's rows are pulled, and side 0's local
-        partition runs while side 1's rows are pulled."""
+        """Owner pass, NVLink exchange and local partition of both sides, pipelined: side 1's
+        owner pass runs while side 0's rows are pulled, and side 0's local partition while
+        side 1's rows are pulled."""
         t = self.transport
         if hasattr(t, "set_pull_ctas"):
-            t.set_pull_ctas(max(32, SHUFFLE_PULL_CTAS // (self.world - 1)))  # pulls share the GPU with partitioning
-        reqs0, n0 = await self._exchange_side(0)
-        reqs1, n1 = await self._exchange_side(1)
-        self._mark("rank_partition_and_post_ms")
+            t.set_pull_ctas(SHUFFLE_PULL_CTAS)  # the pulls share the GPU with the partition kernels
+        reqs0, runs0 = await self._exchange_side(0)
+        reqs1, runs1 = await self._exchange_side(1)
+        self._mark("owner_partition_and_post_ms")
         for r in reqs0:
             await await_request(t, r)
         self._mark("side0_exchange_wait_ms")
-        self._partition(self.recv[0], n0, 0, self.parts, self.parted[0], self.bounds[0])
+        n0 = self._finish_side(0, runs0)
         for r in reqs1:
             await await_request(t, r)
         self._mark("side1_exchange_wait_ms")
-        self._partition(self.recv[1], n1, 0, self.parts, self.parted[1], self.bounds[1])
+        n1 = self._finish_side(1, runs1)
         if hasattr(t, "set_pull_ctas"):
             t.set_pull_ctas(296)
         return [n0, n1]

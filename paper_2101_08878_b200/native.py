@@ -147,6 +147,12 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_partition_scratch_bytes": (_size, [_i64, ctypes.c_int]),
     "m4d_partition": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
                                      _c_void_p, _c_void_p, _size, _c_void_p]),
+    "m4d_partition_runs": (ctypes.c_int, [_c_void_p, _i64, _c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
+    "m4d_partition_runs_scratch_bytes": (_size, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "m4d_owner_coarse_count": (ctypes.c_int, [ctypes.c_int]),
+    "m4d_partition_owner_coarse": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                                  _c_void_p, _c_void_p, _size, _c_void_p]),
     "m4d_partition_launches": (ctypes.c_int, [ctypes.c_int]),
     "m4d_hash_join": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int,
                                      _c_void_p, _c_void_p, _c_void_p, _i64, _c_void_p, _c_void_p]),
