@@ -131,3 +131,34 @@ def test_partition_bounds_under_extreme_skew(buckets):
     pb = bucket[pairs[:, 1]]
     assert np.all(np.diff(pb) >= 0)  # grouped by bucket, in bucket order
     assert np.array_equal(pairs[:, 0], keys[pairs[:, 1]])
+
+
+@pytest.mark.parametrize("world,coarse", [(3, 64), (8, 32), (2, 1)])
+def test_owner_coarse_partition_matches_numpy(world, coarse):
+    """m4d_partition_owner_coarse: bucket = owner * C + top log2 C bits of the local id."""
+    from paper_2101_08878_b200 import native
+
+    n = 300_001
+    keys = np.random.default_rng(world).integers(-(1 << 62), 1 << 62, n).astype(np.int64)
+    vals = np.arange(n, dtype=np.int64)
+    lib = native.lib()
+    k_d, v_d = native.DeviceBuffer(0, n * 8), native.DeviceBuffer(0, n * 8)
+    native.memcpy(k_d.ptr, keys.ctypes.data, n * 8)
+    native.memcpy(v_d.ptr, vals.ctypes.data, n * 8)
+    nb = world * coarse
+    out, bounds = native.DeviceBuffer(0, n * 16), native.DeviceBuffer(0, (nb + 1) * 8)
+    nbytes = lib.m4d_partition_scratch_bytes(n, nb)
+    scratch = native.DeviceBuffer(0, nbytes)
+    native.check(lib.m4d_partition_owner_coarse(k_d.ptr, v_d.ptr, n, world, coarse, out.ptr, bounds.ptr, scratch.ptr,
+                                                nbytes, None))
+    native.check(lib.m4d_device_sync(0))
+    got_b = np.frombuffer(native.to_host(bounds.ptr, (nb + 1) * 8), dtype=np.int64)
+    pairs = np.frombuffer(native.to_host(out.ptr, n * 16), dtype=np.int64).reshape(n, 2)
+    h = oracle.splitmix64_np(keys.view(np.uint64))
+    owner = ((h >> np.uint64(32)) * np.uint64(world)) >> np.uint64(32)
+    cbits = int(np.log2(coarse))
+    low = ((h & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - cbits)) if cbits else np.zeros(n, np.uint64)
+    bucket = (owner * np.uint64(coarse) + low).astype(np.int64)
+    want_b = np.concatenate([[0], np.cumsum(np.bincount(bucket, minlength=nb))])
+    assert np.array_equal(got_b, want_b)
+    assert np.all(np.diff(bucket[pairs[:, 1]]) >= 0) and np.array_equal(np.sort(pairs[:, 1]), vals)
