@@ -16,8 +16,31 @@
 //
 // Reference interface replaced: Transport.post_send / post_recv / progress
 // (pkg/src/commshim/transport/base.py:267-284).
+//
+// Framed composites (the messaging layer's wire protocol done natively):
+//
+//   send_framed(handle, kind, channel, peer, tag, header, frames, max_chunk, req_id)
+//   recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id)
+//   take_framed(req_id) -> (outcome, header bytes, payload bytearray | None, detail)
+//
+// kind 0 is send_payload/recv_payload (messaging.py:295-320 of the reference:
+// a <QBB transfer header, then the payload in max_chunk slices, one tag);
+// kind 1 is write_message/read_message (:325-388: a <I count + n x <QBB
+// header on MESSAGE_TAG, then frame i in slices on tag 16 + i mod 2^15).  The
+// composite posts exactly the transport messages the Python functions post,
+// in the same order, so either side may use either path.  A receive
+// composite reads the header, and for host frames posts the slice receives
+// into one buffer itself; anything else (device frames, a malformed or EOS
+// header) completes it early with the header bytes so Python finishes the
+// message the generic way and raises the generic errors.  Sub-requests carry
+// ids with kSubBit set and never reach Python.
 #define PY_SSIZE_T_CLEAN
 #include <Python.h>
+
+#include <cstring>
+#include <memory>
+#include <unordered_map>
+#include <vector>
 
 #include "m4d.h"
 
@@ -34,6 +57,158 @@ post_recv_fn g_recv = nullptr;
 progress_fn g_progress = nullptr;
 
 constexpr int kBatch = 64;
+constexpr uint64_t kSubBit = 1ull << 62;
+constexpr int kTagMessage = 1;        // messaging.MESSAGE_TAG
+constexpr int kDataTagBase = 16;      // messaging.DATA_TAG_BASE
+constexpr int kDataTagSpan = 1 << 15;
+constexpr uint32_t kEos = 0xffffffffu;
+constexpr size_t kMaxFrames = 1024;
+constexpr size_t kMsgHeaderCap = 4 + kMaxFrames * 10;
+
+enum Outcome { kComplete = 0, kHeaderOnly = 1, kEndOfStream = 2, kShortChunk = 3 };
+
+struct Framed {
+    uint64_t id = 0;
+    m4d_transport* t = nullptr;
+    int kind = 0, peer = 0;
+    uint32_t channel = 0, tag = 0;
+    uint64_t max_chunk = 1;
+    bool recv = false;
+    std::vector<uint8_t> header;
+    uint64_t header_got = 0;
+    std::vector<uint8_t> payload;
+    std::vector<Py_buffer> views;  // send: exporters held until the sends complete
+    int pending = 0;
+    int status = M4D_OK;
+    int outcome = kComplete;
+    long long detail[3] = {0, 0, 0};  // short chunk: offset, expected, actual
+    bool done = false;
+    std::vector<std::pair<uint64_t, uint64_t>> expect;  // per sub id: (offset, piece)
+    std::unordered_map<uint64_t, size_t> sub_slot;
+};
+
+std::unordered_map<uint64_t, std::shared_ptr<Framed>> g_framed;   // composite id -> state
+std::unordered_map<uint64_t, std::shared_ptr<Framed>> g_by_sub;   // sub id -> composite
+std::unordered_map<m4d_transport*, std::vector<m4d_completion>> g_ready;  // finished composites, per transport
+uint64_t g_next_sub = 1;
+
+void release_views(Framed& f) {
+    for (Py_buffer& v : f.views) PyBuffer_Release(&v);
+    f.views.clear();
+}
+
+void finish(const std::shared_ptr<Framed>& f, int status, bool inline_done, m4d_completion* now) {
+    if (f->done) return;
+    f->done = true;
+    f->status = status;
+    release_views(*f);
+    m4d_completion c{f->id, status, f->recv ? 1 : 0, f->payload.size()};
+    if (!f->recv) g_framed.erase(f->id);  // a send composite has no result to take
+    if (inline_done && now) *now = c;
+    else g_ready[f->t].push_back(c);
+}
+
+// A composite that finished while its own post call was still running is
+// reported by that call, not by progress().
+void unqueue(const std::shared_ptr<Framed>& f) {
+    auto it = g_ready.find(f->t);
+    if (it == g_ready.end()) return;
+    auto& v = it->second;
+    for (size_t i = 0; i < v.size(); ++i)
+        if (v[i].req_id == f->id) {
+            v.erase(v.begin() + static_cast<long>(i));
+            break;
+        }
+}
+
+void on_sub(const std::shared_ptr<Framed>& f, uint64_t sub, int status, uint64_t bytes);
+
+// Posts one sub-request; an inline completion is handled at once.
+int post_sub(const std::shared_ptr<Framed>& f, bool send, uint32_t tag, void* ptr, uint64_t len, uint64_t offset) {
+    const uint64_t sub = kSubBit | g_next_sub++;
+    m4d_completion now;
+    g_by_sub[sub] = f;
+    f->sub_slot[sub] = f->expect.size();
+    f->expect.emplace_back(offset, len);
+    ++f->pending;
+    const m4d_status st = send ? g_send(f->t, f->channel, f->peer, tag, ptr, len, 0, 0, sub, &now)
+                               : g_recv(f->t, f->channel, f->peer, tag, ptr, len, 0, 0, sub, &now);
+    if (st != M4D_OK) {
+        g_by_sub.erase(sub);
+        --f->pending;
+        return st;
+    }
+    if (now.status != -1) {
+        g_by_sub.erase(sub);
+        on_sub(f, sub, now.status, now.bytes);
+    }
+    return M4D_OK;
+}
+
+int data_tag(size_t i) { return kDataTagBase + static_cast<int>(i % kDataTagSpan); }
+
+// The receive composite's header arrived: post the slice receives (host frames) or stop early.
+void on_header(const std::shared_ptr<Framed>& f, uint64_t got) {
+    f->header_got = got;
+    f->header.resize(got);
+    std::vector<std::pair<uint64_t, int>> frames;  // (length, tag)
+    if (f->kind == 0) {
+        if (got != 10 || f->header[9] != 0) { f->outcome = kHeaderOnly; return; }
+        uint64_t len;
+        std::memcpy(&len, f->header.data(), 8);
+        frames.emplace_back(len, static_cast<int>(f->tag));
+    } else {
+        if (got < 4) { f->outcome = kHeaderOnly; return; }
+        uint32_t count;
+        std::memcpy(&count, f->header.data(), 4);
+        if (count == kEos) { f->outcome = kEndOfStream; return; }
+        if (count > kMaxFrames || got != 4 + 10ull * count) { f->outcome = kHeaderOnly; return; }
+        for (uint32_t i = 0; i < count; ++i) {
+            const uint8_t* m = f->header.data() + 4 + 10 * i;
+            uint64_t len;
+            std::memcpy(&len, m, 8);
+            if (m[9] != 0) { f->outcome = kHeaderOnly; return; }  // a device frame: Python allocates it
+            frames.emplace_back(len, data_tag(i));
+        }
+    }
+    uint64_t total = 0;
+    for (auto& fr : frames) total += fr.first;
+    f->payload.resize(total);
+    f->outcome = kComplete;
+    uint64_t at = 0;
+    for (auto& fr : frames) {
+        for (uint64_t off = 0; off < fr.first; off += f->max_chunk) {
+            const uint64_t piece = fr.first - off < f->max_chunk ? fr.first - off : f->max_chunk;
+            const int st = post_sub(f, false, static_cast<uint32_t>(fr.second), f->payload.data() + at + off, piece, off);
+            if (st != M4D_OK) { f->status = st; return; }
+            if (f->done) return;
+        }
+        at += fr.first;
+    }
+}
+
+void on_sub(const std::shared_ptr<Framed>& f, uint64_t sub, int status, uint64_t bytes) {
+    --f->pending;
+    const size_t slot = f->sub_slot[sub];
+    f->sub_slot.erase(sub);
+    if (f->done) return;
+    if (status != M4D_OK) {
+        finish(f, status, false, nullptr);
+        return;
+    }
+    if (f->recv && slot == 0) {  // the header
+        ++f->pending;  // guard: slices completing inline must not finish the composite early
+        on_header(f, bytes);
+        --f->pending;
+        if (f->status != M4D_OK) { finish(f, f->status, false, nullptr); return; }
+    } else if (f->recv && bytes != f->expect[slot].second && f->outcome == kComplete) {
+        f->outcome = kShortChunk;
+        f->detail[0] = static_cast<long long>(f->expect[slot].first);
+        f->detail[1] = static_cast<long long>(f->expect[slot].second);
+        f->detail[2] = static_cast<long long>(bytes);
+    }
+    if (!f->pending && !f->done) finish(f, M4D_OK, false, nullptr);
+}
 
 PyObject* bind(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     if (nargs != 3) {
@@ -116,6 +291,15 @@ PyObject* progress(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
         const int n = g_progress(t, batch, kBatch);
         if (n > 0 && !out && !(out = PyList_New(0))) return nullptr;
         for (int k = 0; k < n; ++k) {
+            if (batch[k].req_id & kSubBit) {
+                auto it = g_by_sub.find(batch[k].req_id);
+                if (it != g_by_sub.end()) {
+                    std::shared_ptr<Framed> f = it->second;
+                    g_by_sub.erase(it);
+                    on_sub(f, batch[k].req_id, batch[k].status, batch[k].bytes);
+                }
+                continue;
+            }
             PyObject* item = Py_BuildValue("(KiK)", static_cast<unsigned long long>(batch[k].req_id), batch[k].status,
                                            static_cast<unsigned long long>(batch[k].bytes));
             if (!item || PyList_Append(out, item) != 0) {
@@ -127,8 +311,149 @@ PyObject* progress(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
         }
         if (n < kBatch) break;
     }
+    auto ready = g_ready.find(t);
+    if (ready != g_ready.end() && !ready->second.empty()) {
+        if (!out && !(out = PyList_New(0))) return nullptr;
+        for (const m4d_completion& c : ready->second) {
+            PyObject* item = Py_BuildValue("(KiK)", static_cast<unsigned long long>(c.req_id), c.status,
+                                           static_cast<unsigned long long>(c.bytes));
+            if (!item || PyList_Append(out, item) != 0) {
+                Py_XDECREF(item);
+                Py_DECREF(out);
+                return nullptr;
+            }
+            Py_DECREF(item);
+        }
+        ready->second.clear();
+    }
     if (!out) Py_RETURN_NONE;
     return out;
+}
+
+PyObject* inline_result(const std::shared_ptr<Framed>& f) {
+    if (!f->done) Py_RETURN_NONE;
+    return Py_BuildValue("(iK)", f->status, static_cast<unsigned long long>(f->payload.size()));
+}
+
+// recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id)
+PyObject* recv_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+    if (nargs != 7 || !g_recv) {
+        PyErr_SetString(PyExc_TypeError, "recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id)");
+        return nullptr;
+    }
+    auto f = std::make_shared<Framed>();
+    f->t = static_cast<m4d_transport*>(PyLong_AsVoidPtr(args[0]));
+    f->kind = static_cast<int>(PyLong_AsLong(args[1]));
+    f->channel = static_cast<uint32_t>(PyLong_AsUnsignedLong(args[2]));
+    f->peer = static_cast<int>(PyLong_AsLong(args[3]));
+    f->tag = static_cast<uint32_t>(PyLong_AsUnsignedLong(args[4]));
+    f->max_chunk = PyLong_AsUnsignedLongLong(args[5]);
+    f->id = PyLong_AsUnsignedLongLong(args[6]);
+    if (PyErr_Occurred()) return nullptr;
+    if (f->max_chunk < 1) f->max_chunk = 1;
+    f->recv = true;
+    f->header.resize(f->kind == 0 ? 10 : kMsgHeaderCap);
+    g_framed[f->id] = f;
+    const int st = post_sub(f, false, f->tag, f->header.data(), f->header.size(), 0);
+    if (st != M4D_OK) {
+        g_framed.erase(f->id);
+        PyErr_SetObject(PyExc_OSError, PyLong_FromLong(st));
+        return nullptr;
+    }
+    if (!f->pending && !f->done) finish(f, f->status, true, nullptr);
+    if (f->done) unqueue(f);  // completed inline: reported here, not through progress()
+    return inline_result(f);
+}
+
+// send_framed(handle, kind, channel, peer, tag, header, frames, max_chunk, req_id)
+PyObject* send_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+    if (nargs != 9 || !g_send) {
+        PyErr_SetString(PyExc_TypeError, "send_framed(handle, kind, channel, peer, tag, header, frames, max_chunk, req_id)");
+        return nullptr;
+    }
+    auto f = std::make_shared<Framed>();
+    f->t = static_cast<m4d_transport*>(PyLong_AsVoidPtr(args[0]));
+    f->kind = static_cast<int>(PyLong_AsLong(args[1]));
+    f->channel = static_cast<uint32_t>(PyLong_AsUnsignedLong(args[2]));
+    f->peer = static_cast<int>(PyLong_AsLong(args[3]));
+    f->tag = static_cast<uint32_t>(PyLong_AsUnsignedLong(args[4]));
+    f->max_chunk = PyLong_AsUnsignedLongLong(args[7]);
+    f->id = PyLong_AsUnsignedLongLong(args[8]);
+    if (PyErr_Occurred()) return nullptr;
+    if (f->max_chunk < 1) f->max_chunk = 1;
+    PyObject* frames = args[6];
+    if (!PyTuple_Check(frames)) {
+        PyErr_SetString(PyExc_TypeError, "frames must be a tuple of buffers");
+        return nullptr;
+    }
+    const Py_ssize_t nf = PyTuple_GET_SIZE(frames);
+    f->views.resize(static_cast<size_t>(nf) + 1);
+    Py_ssize_t got = 0;
+    auto fail_views = [&]() {
+        for (Py_ssize_t i = 0; i < got; ++i) PyBuffer_Release(&f->views[static_cast<size_t>(i)]);
+        f->views.clear();
+        return nullptr;
+    };
+    if (PyObject_GetBuffer(args[5], &f->views[0], PyBUF_SIMPLE) != 0) { f->views.clear(); return nullptr; }
+    got = 1;
+    for (Py_ssize_t i = 0; i < nf; ++i, ++got)
+        if (PyObject_GetBuffer(PyTuple_GET_ITEM(frames, i), &f->views[static_cast<size_t>(i) + 1], PyBUF_SIMPLE) != 0)
+            return fail_views();
+    g_framed[f->id] = f;
+    f->pending = 1;  // guard: the composite cannot finish while its sends are still being posted
+    const uint32_t header_tag = f->kind == 0 ? f->tag : static_cast<uint32_t>(kTagMessage);
+    int st = post_sub(f, true, header_tag, f->views[0].buf, static_cast<uint64_t>(f->views[0].len), 0);
+    for (Py_ssize_t i = 0; i < nf && st == M4D_OK && !f->done; ++i) {
+        const Py_buffer& v = f->views[static_cast<size_t>(i) + 1];
+        const uint32_t tag = f->kind == 0 ? f->tag : static_cast<uint32_t>(data_tag(static_cast<size_t>(i)));
+        const uint64_t len = static_cast<uint64_t>(v.len);
+        for (uint64_t off = 0; off < len && st == M4D_OK && !f->done; off += f->max_chunk) {
+            const uint64_t piece = len - off < f->max_chunk ? len - off : f->max_chunk;
+            st = post_sub(f, true, tag, static_cast<uint8_t*>(v.buf) + off, piece, off);
+        }
+    }
+    --f->pending;
+    if (st != M4D_OK && !f->done) {
+        if (f->pending) {
+            f->status = st;  // the remaining posted parts still complete; report the failure then
+        } else {
+            g_framed.erase(f->id);
+            release_views(*f);
+            PyErr_SetObject(PyExc_OSError, PyLong_FromLong(st));
+            return nullptr;
+        }
+    }
+    if (!f->pending && !f->done) finish(f, f->status, true, nullptr);
+    if (f->done) unqueue(f);
+    return inline_result(f);
+}
+
+// take_framed(req_id) -> (outcome, header, payload bytearray | None, (offset, expected, actual))
+PyObject* take_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+    if (nargs != 1) {
+        PyErr_SetString(PyExc_TypeError, "take_framed(req_id)");
+        return nullptr;
+    }
+    const uint64_t id = PyLong_AsUnsignedLongLong(args[0]);
+    if (PyErr_Occurred()) return nullptr;
+    auto it = g_framed.find(id);
+    if (it == g_framed.end()) {
+        PyErr_SetString(PyExc_KeyError, "no framed result for this request");
+        return nullptr;
+    }
+    std::shared_ptr<Framed> f = it->second;
+    g_framed.erase(it);
+    PyObject* payload = nullptr;
+    if (f->outcome == kComplete) {
+        payload = PyByteArray_FromStringAndSize(reinterpret_cast<const char*>(f->payload.data()),
+                                                static_cast<Py_ssize_t>(f->payload.size()));
+        if (!payload) return nullptr;
+    } else {
+        Py_INCREF(Py_None);
+        payload = Py_None;
+    }
+    return Py_BuildValue("(iy#N(LLL))", f->outcome, reinterpret_cast<const char*>(f->header.data()),
+                         static_cast<Py_ssize_t>(f->header_got), payload, f->detail[0], f->detail[1], f->detail[2]);
 }
 
 PyMethodDef methods[] = {
@@ -138,6 +463,12 @@ PyMethodDef methods[] = {
      "post(handle, is_send, channel, peer, tag, data, domain, device_len, req_id)"},
     {"progress", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(progress)), METH_FASTCALL,
      "progress(handle) -> [(req_id, status, bytes)] or None"},
+    {"recv_framed", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(recv_framed)), METH_FASTCALL,
+     "recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id) -> None | (status, bytes)"},
+    {"send_framed", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(send_framed)), METH_FASTCALL,
+     "send_framed(handle, kind, channel, peer, tag, header, frames, max_chunk, req_id) -> None | (status, bytes)"},
+    {"take_framed", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(take_framed)), METH_FASTCALL,
+     "take_framed(req_id) -> (outcome, header, payload | None, (offset, expected, actual))"},
     {nullptr, nullptr, 0, nullptr},
 };
 

@@ -39,6 +39,18 @@ from .base import (
     as_view,
 )
 
+class _Extent:
+    """Length-only stand-in for the payload view of a framed composite request."""
+
+    __slots__ = ("n",)
+
+    def __init__(self, n: int):
+        self.n = n
+
+    def __len__(self) -> int:
+        return self.n
+
+
 _Config = native.TransportConfigC
 Completion = native.Completion
 Stats = native.TransportStats
@@ -210,6 +222,46 @@ class NvlinkTransport(Transport):
         else:
             self._apply(req, done[0], done[1])
         return self._track(req)
+
+    # -- framed composites (messaging wire protocol done natively, csrc/pyfast.cpp) -------------
+
+    def post_send_framed(self, kind: int, channel: int, peer: int, tag: int, header: bytes, bodies: tuple,
+                         max_chunk: int) -> TransferRequest:
+        """One request for a whole host-frame transfer: ``header`` then every body in
+        ``max_chunk`` slices (kind 0: send_payload, all on ``tag``; kind 1: write_message,
+        header on ``tag``, body i on data tag 16 + i)."""
+        self._check_route(channel, peer)
+        total = len(header) + sum(len(b) for b in bodies)
+        req = TransferRequest(self, "send", channel, peer, tag, _Extent(total), MemoryDomain.HOST)
+        try:
+            done = self._fast.send_framed(self._h, kind, channel, peer, tag, header, bodies, max_chunk, req.id)
+        except OSError as exc:
+            raise native.error_for(exc.args[0], native.last_error()) from None
+        if done is None:
+            self._live[req.id] = req
+        else:
+            self._apply(req, done[0], total if done[0] == native.OK else 0)
+        return self._track(req)
+
+    def post_recv_framed(self, kind: int, channel: int, peer: int, tag: int, max_chunk: int) -> TransferRequest:
+        """One request that receives a whole framed transfer (see :meth:`take_framed`)."""
+        self._check_route(channel, peer)
+        req = TransferRequest(self, "recv", channel, peer, tag, _Extent(0), MemoryDomain.HOST)
+        try:
+            done = self._fast.recv_framed(self._h, kind, channel, peer, tag, max_chunk, req.id)
+        except OSError as exc:
+            raise native.error_for(exc.args[0], native.last_error()) from None
+        if done is None:
+            self._live[req.id] = req
+        else:
+            self._apply(req, done[0], done[1])
+        return self._track(req)
+
+    def take_framed(self, req: TransferRequest):
+        """(outcome, header bytes, payload bytearray or None, (offset, expected, actual)) of a
+        finished receive composite: outcome 0 = all host frames received, 1 = header only (the
+        caller finishes the transfer), 2 = end of stream, 3 = a slice came short."""
+        return self._fast.take_framed(req.id)
 
     def post_send(self, channel: int, peer: int, tag: int, data,
                   domain: MemoryDomain = MemoryDomain.HOST) -> TransferRequest:
