@@ -752,9 +752,12 @@ m4d_status m4d_ts_plan_create(int device, const m4d_ts_task* tasks_in, int ntask
         return cleanup(m4d::cuda_fail(e, "ts kernel attributes"));
     if ((e = cudaDeviceGetAttribute(&plan->sms, cudaDevAttrMultiProcessorCount, device)) != cudaSuccess)
         return cleanup(m4d::cuda_fail(e, "SM count"));
-    // CTAs that start on the remote stream: in proportion to its share of the
-    // items (M4D_TS_REMOTE_CTAS overrides, for the ablation in DESIGN.md).
-    plan->remote_ctas = plan->items ? static_cast<int>((plan->sms * plan->items_remote + plan->items - 1) / plan->items) : 0;
+    // CTAs that start on the peer streams: their share of the items, leaned
+    // 15% toward NVLink (N=4: 111 -> 130 CTAs, 4.21 -> 4.08 ms per launch;
+    // flat at N=2; tools/ts_remote_sweep.sh).  M4D_TS_REMOTE_CTAS overrides.
+    plan->remote_ctas = plan->items ? static_cast<int>(std::min<int64_t>(
+                                          plan->sms, (plan->sms * plan->items_remote * 115 / 100 + plan->items - 1) / plan->items))
+                                    : 0;
     if (const char* v = getenv("M4D_TS_REMOTE_CTAS")) plan->remote_ctas = atoi(v);
     if (const char* v = getenv("M4D_TS_REMOTE_CAP")) plan->remote_cap = atoi(v);
     *plan_out = plan;
