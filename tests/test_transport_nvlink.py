@@ -267,3 +267,47 @@ def test_requests_transition_exactly_once(pair):
     assert [b[0] for b in bufs] == list(range(50))
     assert t0.metrics.sends_completed == 50 and t1.metrics.recvs_completed == 50
     assert t0.metrics.staged_bytes == 0 and t1.metrics.staged_bytes == 0
+
+
+DYING_PEER = """
+import sys, time
+sys.path.insert(0, sys.argv[1])
+from paper_2101_08878_b200.transport import TransportConfig, transport_init
+t = transport_init(2, 1, TransportConfig(kind="nvlink", session=sys.argv[2], device=-1, connect_timeout=20))
+t.wait_ready()
+print("ready", flush=True)
+time.sleep(60)  # killed by the test
+"""
+
+
+def test_peer_death_fails_pending_receives_and_sends():
+    """A peer killed mid-run (no close): its pid probe fails the pending receive and a
+    queued send with TransferError and later posts with CommClosedError (the socket
+    transport's peer-death handling, tcp.py:420-438 of the reference)."""
+    import signal
+    import subprocess
+    import sys
+    import time
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    session = new_session()
+    child = subprocess.Popen([sys.executable, "-c", DYING_PEER, root, session], stdout=subprocess.PIPE, text=True)
+    try:
+        t0 = transport_init(2, 0, TransportConfig(kind="nvlink", session=session, device=-1, connect_timeout=20))
+        t0.wait_ready()
+        assert child.stdout.readline().strip() == "ready"
+        recv = t0.post_recv(0, 1, 5, bytearray(8))
+        big = t0.post_send(0, 1, 6, bytes(32 << 20))  # larger than the ring: stays queued
+        child.send_signal(signal.SIGKILL)
+        child.wait(timeout=10)
+        deadline = time.monotonic() + 10
+        while (recv.pending or big.pending) and time.monotonic() < deadline:
+            t0.progress()
+        assert recv.failed and isinstance(recv.error, TransferError)
+        assert big.failed and isinstance(big.error, TransferError)
+        late = t0.post_recv(0, 1, 5, bytearray(8))
+        assert late.failed and isinstance(late.error, (CommClosedError, TransferError))
+        t0.close()
+    finally:
+        if child.poll() is None:
+            child.kill()
