@@ -1135,6 +1135,11 @@ int m4d_transport_mesh_ready(const m4d_transport* t) {
     return 1;
 }
 
+m4d_status m4d_transport_set_pull_engine(m4d_transport* t, int copy_engine) {
+    t->use_ce = copy_engine != 0;
+    return M4D_OK;
+}
+
 m4d_status m4d_transport_set_pull_ctas(m4d_transport* t, int max_ctas) {
     if (max_ctas < 1) return fail(M4D_ERR_USAGE, "pull grid cap must be positive");
     t->pull_ctas = max_ctas;

@@ -44,8 +44,6 @@ SEED_LEFT = 0x4C454654
 SEED_RIGHT = 0x52494748
 EXCHANGE_TAG = 900
 DATA_TAG = 910
-SHUFFLE_PULL_CTAS = 192  # pull-kernel grid while the shuffle overlaps partition kernels (the transport
-                         # batches the per-peer messages of a side into one launch)
 _MASK64 = (1 << 64) - 1
 
 
@@ -230,8 +228,9 @@ class KeyMerge:
         owner pass runs while side 0's rows are pulled, and side 0's local partition while
         side 1's rows are pulled."""
         t = self.transport
-        if hasattr(t, "set_pull_ctas"):
-            t.set_pull_ctas(SHUFFLE_PULL_CTAS)  # the pulls share the GPU with the partition kernels
+        engine = getattr(t, "pull_copy_engine", None)
+        if engine is not None:
+            t.set_pull_engine(True)  # copy-engine pulls: every SM stays on the partition kernels
         reqs0, runs0 = await self._exchange_side(0)
         reqs1, runs1 = await self._exchange_side(1)
         self._mark("owner_partition_and_post_ms")
@@ -243,8 +242,8 @@ class KeyMerge:
             await await_request(t, r)
         self._mark("side1_exchange_wait_ms")
         n1 = self._finish_side(1, runs1)
-        if hasattr(t, "set_pull_ctas"):
-            t.set_pull_ctas(296)
+        if engine is not None:
+            t.set_pull_engine(engine)
         return [n0, n1]
 
     async def run(self) -> tuple[int, int, int]:

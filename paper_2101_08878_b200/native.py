@@ -141,6 +141,7 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_transport_purge_channel": (ctypes.c_int, [_c_void_p, ctypes.c_uint32]),
     "m4d_transport_peer_alive": (ctypes.c_int, [_c_void_p, ctypes.c_int]),
     "m4d_transport_set_pull_ctas": (ctypes.c_int, [_c_void_p, ctypes.c_int]),
+    "m4d_transport_set_pull_engine": (ctypes.c_int, [_c_void_p, ctypes.c_int]),
     "m4d_transport_stats_get": (ctypes.c_int, [_c_void_p, ctypes.POINTER(TransportStats)]),
     "m4d_transport_close": (ctypes.c_int, [_c_void_p]),
     "m4d_merge_generate": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, _i64, _u64, _u64, _u64, _c_void_p]),

@@ -182,6 +182,7 @@ class NvlinkTransport(Transport):
         self._h = handle.value
         self._lib = native.lib()
         self._fast = native.fast()
+        self.pull_copy_engine = os.environ.get("M4D_PULL_ENGINE") == "ce"
         self._live: dict[int, TransferRequest] = {}
         self._pool = _RegionPool(device) if device >= 0 else None
         self.connect_timeout = config.connect_timeout
@@ -322,6 +323,11 @@ class NvlinkTransport(Transport):
     def purge_channel(self, channel: int) -> None:
         native.check(self._lib.m4d_transport_purge_channel(self._h, channel))
         self.progress()
+
+    def set_pull_engine(self, copy_engine: bool) -> None:
+        """Rendezvous pulls on the copy engines only (True) or SM copy kernels (False)."""
+        native.check(self._lib.m4d_transport_set_pull_engine(self._h, int(bool(copy_engine))))
+        self.pull_copy_engine = bool(copy_engine)
 
     def set_pull_ctas(self, max_ctas: int) -> None:
         """Cap the SM pull kernel's grid (pulls sharing the GPU with compute kernels)."""
