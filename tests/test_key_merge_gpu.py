@@ -162,3 +162,15 @@ def test_owner_coarse_partition_matches_numpy(world, coarse):
     want_b = np.concatenate([[0], np.cumsum(np.bincount(bucket, minlength=nb))])
     assert np.array_equal(got_b, want_b)
     assert np.all(np.diff(bucket[pairs[:, 1]]) >= 0) and np.array_equal(np.sort(pairs[:, 1]), vals)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("fraction", [0.0, 0.3, 1.0])
+def test_spec_application_oracle(world, fraction):
+    """SPEC.md acceptance (application oracles): 10^4 rows per worker, fraction in {0, 0.3, 1},
+    workers in {1, 2, 4}: the global digest equals the brute-force join of the oracle."""
+    rows = 10_000
+    _, got = run_world(rows, world, fraction)
+    assert got == oracle.key_merge_c(rows, world, fraction)
+    if fraction == 0.0:
+        assert got[0] == 0
