@@ -229,15 +229,17 @@ __global__ void __launch_bounds__(kHistThreads) scatter_kernel(const int64_t* __
 // of the tile to its global position, so every global store belongs to a
 // contiguous run (about 16 rows = 256 B per bucket per tile) and DRAM sees
 // full sectors.  Rows keep their input order within a bucket (deterministic).
-constexpr int kTileRows = kHistThreads * kRowsPerThread;  // 4096
 constexpr int kTileBuckets = 256;
-constexpr size_t kTileSmem = kTileRows * sizeof(longlong2) + kTileRows + (kHistThreads / 32) * kTileBuckets * 2;
+template <int kT>
+constexpr size_t tile_smem() { return kT * kRowsPerThread * (sizeof(longlong2) + 1) + (kT / 32) * kTileBuckets * 2; }
 
-__global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int64_t* __restrict__ keys,
+template <int kT>
+__global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile_scatter_kernel(const int64_t* __restrict__ keys,
                                                                        const int64_t* __restrict__ vals, int64_t n,
                                                                        int64_t run, int mode, int buckets, int log2b,
                                                                        const int64_t* __restrict__ offsets,
                                                                        longlong2* __restrict__ out) {
+    constexpr int kTileRows = kT * kRowsPerThread;
     extern __shared__ __align__(16) unsigned char tsm[];
     longlong2* stage = reinterpret_cast<longlong2*>(tsm);
     uint8_t* sbucket = tsm + kTileRows * sizeof(longlong2);
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kHistThreads, 2) tile_scatter_kernel(const int
     __shared__ uint32_t gcur[kTileBuckets];
     __shared__ uint32_t tstart[kTileBuckets + 1];
     __shared__ uint32_t scan_tmp[kTileBuckets / 32];
-    constexpr int kW = kHistThreads / 32;
+    constexpr int kW = kT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const unsigned lower = (1u << lane) - 1u;
     int nbits = 0;
@@ -766,13 +768,51 @@ int log2_exact(int v) {
 
 using m4d::fail;
 
+// Threads per tile-scatter CTA (M4D_TILE_THREADS = 256 | 512 | 1024, default 256): sets the
+// resident CTAs per SM (2048 / threads, at most 4) and so the partition grid.
+static int tile_threads() {
+    static const int t = [] {
+        const char* v = getenv("M4D_TILE_THREADS");
+        const int x = v ? atoi(v) : 256;  // measured: 1.02 / 1.12 / 1.35 ms at 256 / 512 / 1024 (1e8 rows)
+        return x == 512 || x == 1024 ? x : 256;
+    }();
+    return t;
+}
+
 static int partition_ctas(int64_t n) {
-    // <= 2 resident CTAs per SM: the scatter's L2 write frontier must fit (see top).
-    const int64_t per = 65536;
+    // One wave of the tile scatter (its L2 write frontier must fit, see top).
+    const int per_sm = tile_threads() >= 1024 ? 1 : tile_threads() >= 512 ? 2 : 4;
+    const int64_t per = 65536 * 2 / per_sm;
     int64_t c = (n + per - 1) / per;
     if (c < 1) c = 1;
-    if (c > 148 * 2) c = 148 * 2;
+    if (c > 148 * per_sm) c = 148 * per_sm;
     return static_cast<int>(c);
+}
+
+static cudaError_t launch_tile_scatter(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
+                                       int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
+                                       longlong2* out) {
+    cudaError_t e = cudaSuccess;
+    switch (tile_threads()) {
+        case 256:
+            e = cudaFuncSetAttribute(tile_scatter_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tile_smem<256>()));
+            if (e == cudaSuccess)
+                tile_scatter_kernel<256><<<ctas, 256, tile_smem<256>(), s>>>(keys, vals, n, run, mode, buckets, log2b, offs, out);
+            break;
+        case 1024:
+            e = cudaFuncSetAttribute(tile_scatter_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tile_smem<1024>()));
+            if (e == cudaSuccess)
+                tile_scatter_kernel<1024><<<ctas, 1024, tile_smem<1024>(), s>>>(keys, vals, n, run, mode, buckets, log2b, offs, out);
+            break;
+        default:
+            e = cudaFuncSetAttribute(tile_scatter_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(tile_smem<512>()));
+            if (e == cudaSuccess)
+                tile_scatter_kernel<512><<<ctas, 512, tile_smem<512>(), s>>>(keys, vals, n, run, mode, buckets, log2b, offs, out);
+    }
+    return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 static int pass1_bits(int log2b) { return log2b > 8 ? 8 : log2b; }
@@ -802,10 +842,8 @@ static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int
     scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
     scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
     if (buckets <= kTileBuckets) {
-        M4D_CUDA_TRY(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kTileSmem)));
-        tile_scatter_kernel<<<ctas, kHistThreads, kTileSmem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
-                                                                  reinterpret_cast<longlong2*>(out_pairs));
+        M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs,
+                                         reinterpret_cast<longlong2*>(out_pairs)));
     } else {
         scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
                                                             reinterpret_cast<longlong2*>(out_pairs));
@@ -893,9 +931,7 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
         scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
         // pass 1: by the top b1 bits of the partition id (mode LOCAL with 2^b1 buckets == those bits)
-        M4D_CUDA_TRY(cudaFuncSetAttribute(tile_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(kTileSmem)));
-        tile_scatter_kernel<<<ctas, kHistThreads, kTileSmem, s>>>(keys, vals, n, run, M4D_PART_LOCAL, fan, b1, offs, tmp);
+        M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, M4D_PART_LOCAL, fan, b1, offs, tmp));
         group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, groups, buckets, hist_all);
         exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
         scatter_pass2_kernel<<<fan * groups, 1024, (buckets >> b1) * sizeof(uint32_t), s>>>(
