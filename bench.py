@@ -515,6 +515,9 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
     # the public comm path (send_payload / recv_payload, Listing 2/3) with device frames
     pp = {sz: p2p.pingpong(t, 1 - dist.rank, sz, 1000 if sz < (1 << 20) else 50, True)
           for sz in sorted({1, min(4 << 20, args.max_size), args.max_size})}
+    # host frames (Dask control messages; the reference arm's frames): transport and comm path at 1 B
+    host_lat = p2p.osu_latency(t, 1 - dist.rank, 1, 2000, False)
+    host_pp = p2p.pingpong(t, 1 - dist.rank, 1, 2000, False)
     t.close()
     cpu = None
     if dist.rank == 0 and not args.skip_cpu:
@@ -535,6 +538,8 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
         "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
         "config": {"workload": "p2p", "sizes": [r["size"] for r in rows], "window": 64},
         "latency_1B_us": rows[0]["osu_latency_us"], "sweep": rows,
+        "host_frames_1B": {"osu_latency_us": host_lat,
+                           "comm_path_latency_us": host_pp["mean_s"] * 1e6 if host_pp else None},
         "comm_path": {str(k): {"latency_us": v["mean_s"] * 1e6, "GBps": v["throughput_Bps"] / 1e9}
                       for k, v in pp.items() if v},
         "gpu_launches": None,
