@@ -456,6 +456,28 @@ PyObject* take_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
                          static_cast<Py_ssize_t>(f->header_got), payload, f->detail[0], f->detail[1], f->detail[2]);
 }
 
+// forget(handle): drop the composite state of a transport that is closing.
+PyObject* forget(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+    if (nargs != 1) {
+        PyErr_SetString(PyExc_TypeError, "forget(handle)");
+        return nullptr;
+    }
+    auto* t = static_cast<m4d_transport*>(PyLong_AsVoidPtr(args[0]));
+    if (PyErr_Occurred()) return nullptr;
+    for (auto it = g_by_sub.begin(); it != g_by_sub.end();)
+        it = it->second->t == t ? g_by_sub.erase(it) : std::next(it);
+    for (auto it = g_framed.begin(); it != g_framed.end();) {
+        if (it->second->t == t) {
+            release_views(*it->second);
+            it = g_framed.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    g_ready.erase(t);
+    Py_RETURN_NONE;
+}
+
 PyMethodDef methods[] = {
     {"bind", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(bind)), METH_FASTCALL,
      "bind(post_send, post_recv, progress): C-ABI function addresses from the ctypes loader"},
@@ -467,6 +489,8 @@ PyMethodDef methods[] = {
      "recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id) -> None | (status, bytes)"},
     {"send_framed", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(send_framed)), METH_FASTCALL,
      "send_framed(handle, kind, channel, peer, tag, header, frames, max_chunk, req_id) -> None | (status, bytes)"},
+    {"forget", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(forget)), METH_FASTCALL,
+     "forget(handle): drop the composite state of a closing transport"},
     {"take_framed", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(take_framed)), METH_FASTCALL,
      "take_framed(req_id) -> (outcome, header, payload | None, (offset, expected, actual))"},
     {nullptr, nullptr, 0, nullptr},

@@ -351,6 +351,7 @@ class NvlinkTransport(Transport):
 
     def close(self) -> None:
         if getattr(self, "_h", None):
+            self._fast.forget(self._h)
             self._lib.m4d_transport_close(self._h)
             self._h = None
 
