@@ -482,6 +482,28 @@ __global__ void exclusive_scan_u64_kernel(const unsigned long long* __restrict__
     if (t == 0) out[n] = total;
 }
 
+// Second-level scatter of rows [lo, hi) of `in` by the low bits of their local
+// partition id, through per-partition cursors in shared memory.
+__device__ __forceinline__ void scatter_by_low_bits(const longlong2* __restrict__ in, int64_t lo, int64_t hi,
+                                                    uint32_t* cursor, int log2b, uint32_t mask,
+                                                    longlong2* __restrict__ out) {
+    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+        longlong2 row[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            if (i < hi) row[u] = __ldcs(in + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            if (base + u * blockDim.x + threadIdx.x >= hi) continue;
+            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(row[u].x));
+            const uint32_t b2 = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) & mask;
+            out[atomicAdd(&cursor[b2], 1u)] = row[u];
+        }
+    }
+}
+
 // Pass 2: one CTA per (segment, group of pass-1 CTAs).  Within a segment the
 // rows of one group are contiguous, and the group's cursors start at the
 // partition bounds plus the counts of the earlier groups (from the per-group
@@ -505,22 +527,7 @@ __global__ void __launch_bounds__(1024)
     const int64_t entries = static_cast<int64_t>(ctas) << b1;
     const int64_t i0 = static_cast<int64_t>(seg) * ctas + k0, i1 = static_cast<int64_t>(seg) * ctas + k1;
     const int64_t lo = i0 < entries ? offs[i0] : n, hi = i1 < entries ? offs[i1] : n;
-    const uint32_t mask = sub - 1;
-    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
-        longlong2 row[kRowsPerThread];
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            const int64_t i = base + u * blockDim.x + threadIdx.x;
-            if (i < hi) row[u] = __ldcs(in + i);
-        }
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            if (base + u * blockDim.x + threadIdx.x >= hi) continue;
-            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(row[u].x));
-            const uint32_t b2 = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) & mask;
-            out[atomicAdd(&cursor[b2], 1u)] = row[u];
-        }
-    }
+    scatter_by_low_bits(in, lo, hi, cursor, log2b, static_cast<uint32_t>(sub - 1), out);
 }
 
 // Receiver side of the owner+coarse exchange (M4D_PART_OWNER_COARSE): S
@@ -568,22 +575,7 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     const int64_t lo = runs[2 * blockIdx.x], hi = runs[2 * blockIdx.x + 1];
-    const uint32_t mask = sub - 1;
-    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
-        longlong2 row[kRowsPerThread];
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            const int64_t i = base + u * blockDim.x + threadIdx.x;
-            if (i < hi) row[u] = __ldcs(in + i);
-        }
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            if (base + u * blockDim.x + threadIdx.x >= hi) continue;
-            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(row[u].x));
-            const uint32_t b2 = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) & mask;
-            out[atomicAdd(&cursor[b2], 1u)] = row[u];
-        }
-    }
+    scatter_by_low_bits(in, lo, hi, cursor, log2b, static_cast<uint32_t>(sub - 1), out);
 }
 
 __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int buckets, int ctas, int64_t total,
