@@ -97,3 +97,43 @@ def test_native_receive_reports_the_generic_protocol_errors():
         loop.run_until_complete(main())
     finally:
         close_all(ts)
+
+
+def test_failed_chunk_withdraws_the_chunks_posted_ahead():
+    """Chunks are posted CHUNK_WINDOW ahead; when one fails, those still unmatched are
+    withdrawn, so the next transfer on the same key is not swallowed by a stale receive.
+    (A sender that breaks the chunk plan corrupts the stream in either design; this pins
+    the clean-up, not protocol recovery.)"""
+    from paper_2101_08878_b200.errors import TruncationError
+    from paper_2101_08878_b200.loop import sleep
+
+    loop, ts, tables = nvlink_world(2)
+    t0, t1 = ts
+    t1.post_recv_framed = None  # the per-chunk path is the one that posts ahead
+    ch0, ch1 = tables[0].lookup(1), tables[1].lookup(0)
+    state = {"failed": False}
+
+    async def main():
+        async def bad_then_good_writer():
+            hdr = (300).to_bytes(8, "little") + bytes([0, 0])
+            await await_request(t0, t0.post_send(ch0.id, 1, 60, hdr))
+            await await_request(t0, t0.post_send(ch0.id, 1, 60, b"a" * 100))
+            await await_request(t0, t0.post_send(ch0.id, 1, 60, b"b" * 150))  # longer than the 100-byte slice
+            while not state["failed"]:
+                await sleep(0)
+            await send_payload(t0, ch0, 60, make_frame(b"good" * 60), max_chunk=100)
+
+        async def reader():
+            with pytest.raises(TruncationError):
+                await recv_payload(t1, ch1, 60, max_chunk=100)
+            assert not t1.has_pending(ch1.id)  # the third slice's receive was withdrawn
+            state["failed"] = True
+            frame = await recv_payload(t1, ch1, 60, max_chunk=100)
+            assert frame.to_bytes() == b"good" * 60
+
+        await gather(bad_then_good_writer(), reader())
+
+    try:
+        loop.run_until_complete(main())
+    finally:
+        close_all(ts)
