@@ -233,6 +233,58 @@ constexpr int kTileBuckets = 256;
 template <int kT>
 constexpr size_t tile_smem() { return kT * kRowsPerThread * (sizeof(longlong2) + 1) + (kT / 32) * kTileBuckets * 2; }
 
+// Tile scatter, steps 1-2 for one warp: load its rows of the tile and rank each
+// row among the warp's rows of the same bucket (peers found with one ballot per
+// bucket bit, cheaper than MATCH.ANY's serialised match); the leader of each
+// peer group advances the warp's bucket counter wb[b].  kFull: all rows of the
+// tile exist; kBits: compile-time bucket bits (0 = nbits at run time).
+template <bool kFull, int kBits>
+__device__ __forceinline__ void load_and_rank(const int64_t* __restrict__ keys, const int64_t* __restrict__ vals,
+                                              int64_t tile, int rem, int w, int lane, int mode, int buckets, int log2b,
+                                              int nbits, uint16_t* wb, longlong2 (&row)[kRowsPerThread],
+                                              uint32_t (&bk)[kRowsPerThread], uint16_t (&off)[kRowsPerThread]) {
+    const unsigned lower = (1u << lane) - 1u;
+#pragma unroll
+    for (int u = 0; u < kRowsPerThread; ++u) {
+        const int r = w * 256 + u * 32 + lane;
+        if (kFull || r < rem) {
+            const int64_t i = tile + r;
+            if (vals) {
+                row[u].x = __ldcs(keys + i);
+                row[u].y = __ldcs(vals + i);
+            } else {
+                row[u] = __ldcs(reinterpret_cast<const longlong2*>(keys) + i);
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kRowsPerThread; ++u) {
+        const bool live = kFull || w * 256 + u * 32 + lane < rem;
+        bk[u] = live ? bucket_of(row[u].x, mode, buckets, log2b) : 0xffffffffu;
+        unsigned peers = 0xffffffffu;
+        if (!kFull) {
+            peers = __ballot_sync(0xffffffffu, live);
+            peers = live ? peers : ~peers;
+        }
+#pragma unroll
+        for (int bit = 0; bit < 8; ++bit) {  // buckets <= 256
+            if (kBits ? bit < kBits : bit < nbits) {
+                const unsigned v = __ballot_sync(0xffffffffu, (bk[u] >> bit) & 1u);
+                peers &= (bk[u] >> bit) & 1u ? v : ~v;
+            }
+        }
+        const int leader = __ffs(peers) - 1;
+        uint32_t start = 0;
+        if (live && lane == leader) {
+            start = wb[bk[u]];
+            wb[bk[u]] = static_cast<uint16_t>(start + __popc(peers));
+        }
+        start = __shfl_sync(0xffffffffu, start, leader);
+        off[u] = static_cast<uint16_t>(start + __popc(peers & lower));
+        __syncwarp();
+    }
+}
+
 template <int kT>
 __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile_scatter_kernel(const int64_t* __restrict__ keys,
                                                                        const int64_t* __restrict__ vals, int64_t n,
@@ -249,57 +301,26 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
     __shared__ uint32_t scan_tmp[kTileBuckets / 32];
     constexpr int kW = kT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const unsigned lower = (1u << lane) - 1u;
     int nbits = 0;
     while ((1 << nbits) < buckets) ++nbits;
     for (int b = threadIdx.x; b < kTileBuckets; b += blockDim.x)
         gcur[b] = b < buckets ? static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]) : 0u;
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
     for (int64_t tile = lo; tile < hi; tile += kTileRows) {
-        // 1. load: warp w owns rows [tile + 256 w, tile + 256 w + 256)
+        // 1-2. load (warp w owns rows [tile + 256 w, tile + 256 w + 256)) and rank each
+        // row among the warp's rows of its bucket.  Full tiles and 256 buckets (the
+        // common case) run without per-row bounds or bit-count checks.
         longlong2 row[kRowsPerThread];
         uint32_t bk[kRowsPerThread];
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            const int64_t i = tile + w * 256 + u * 32 + lane;
-            if (i < hi) {
-                if (vals) {
-                    row[u].x = __ldcs(keys + i);
-                    row[u].y = __ldcs(vals + i);
-                } else {
-                    row[u] = __ldcs(reinterpret_cast<const longlong2*>(keys) + i);
-                }
-            }
-        }
-        for (int b = lane; b < kTileBuckets; b += 32) wbase[w * kTileBuckets + b] = 0;
-        __syncwarp();
-        // 2. warp multisplit: rank of each row among the warp's rows of its bucket
         uint16_t off[kRowsPerThread];
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            const bool live = tile + w * 256 + u * 32 + lane < hi;
-            bk[u] = live ? bucket_of(row[u].x, mode, buckets, log2b) : 0xffffffffu;
-            // peers = lanes with the same bucket: one ballot per bucket bit (plus
-            // liveness), cheaper than MATCH.ANY's serialised match
-            unsigned peers = __ballot_sync(0xffffffffu, live);
-            peers = live ? peers : ~peers;
-#pragma unroll
-            for (int bit = 0; bit < 8; ++bit) {  // buckets <= 256
-                if (bit < nbits) {
-                    const unsigned v = __ballot_sync(0xffffffffu, (bk[u] >> bit) & 1u);
-                    peers &= (bk[u] >> bit) & 1u ? v : ~v;
-                }
-            }
-            const int leader = __ffs(peers) - 1;
-            uint32_t start = 0;
-            if (live && lane == leader) {
-                start = wbase[w * kTileBuckets + bk[u]];
-                wbase[w * kTileBuckets + bk[u]] = static_cast<uint16_t>(start + __popc(peers));
-            }
-            start = __shfl_sync(0xffffffffu, start, leader);
-            off[u] = static_cast<uint16_t>(start + __popc(peers & lower));
-            __syncwarp();
-        }
+        uint16_t* wb = wbase + w * kTileBuckets;
+        for (int b = lane; b < kTileBuckets; b += 32) wb[b] = 0;
+        __syncwarp();
+        const int rem = hi - tile < kTileRows ? static_cast<int>(hi - tile) : kTileRows;
+        if (rem == kTileRows && nbits == 8)
+            load_and_rank<true, 8>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, nbits, wb, row, bk, off);
+        else
+            load_and_rank<false, 0>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, nbits, wb, row, bk, off);
         __syncthreads();
         // 3. per-bucket tile totals, exclusive over buckets; warp bases within each bucket
         uint32_t total = 0;
