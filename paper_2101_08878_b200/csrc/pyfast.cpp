@@ -64,6 +64,7 @@ constexpr int kDataTagSpan = 1 << 15;
 constexpr uint32_t kEos = 0xffffffffu;
 constexpr size_t kMaxFrames = 1024;
 constexpr size_t kMsgHeaderCap = 4 + kMaxFrames * 10;
+constexpr uint64_t kFramedLimit = 1u << 20;  // messaging.FRAMED_SEND_LIMIT
 
 enum Outcome { kComplete = 0, kHeaderOnly = 1, kEndOfStream = 2, kShortChunk = 3 };
 
@@ -173,6 +174,9 @@ void on_header(const std::shared_ptr<Framed>& f, uint64_t got) {
     }
     uint64_t total = 0;
     for (auto& fr : frames) total += fr.first;
+    // Bulk transfers are received slice by slice from Python (as the send side posts
+    // them): one native call posting and assembling megabytes would stall the loop.
+    if (total > kFramedLimit) { f->outcome = kHeaderOnly; return; }
     f->payload.resize(total);
     f->outcome = kComplete;
     uint64_t at = 0;
