@@ -241,6 +241,22 @@ m4d_status m4d_partition_owner_coarse(const int64_t* keys, const int64_t* vals, 
                                       int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
                                       void* stream);
 
+/* The same owner+coarse partition split in two calls so the shuffle can be
+ * fused into the scatter (replaces the shuffle of the reference's merge,
+ * "hash-shuffles rows to their owner").
+ * m4d_partition_owner_plan: histogram + offsets (kept in `scratch`) and
+ * bounds[world * coarse + 1] (device), exactly as m4d_partition_owner_coarse.
+ * m4d_partition_owner_push: the scatter of that plan (same keys, vals, n,
+ * scratch), writing owner d's rows -- its `coarse` runs back to back, the
+ * layout m4d_partition_owner_coarse gives segment d -- to the device address
+ * seg_dest[d] (host array of `world` addresses, world <= 64): a peer B200's
+ * receive buffer mapped through CUDA IPC, so the rows cross NVLink as the
+ * kernel's own stores and no separate exchange step exists. */
+m4d_status m4d_partition_owner_plan(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
+                                    int64_t* bounds, void* scratch, size_t scratch_bytes, void* stream);
+m4d_status m4d_partition_owner_push(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
+                                    const uint64_t* seg_dest, void* scratch, size_t scratch_bytes, void* stream);
+
 /* Table generator: keys[i] = band + splitmix64(seed + row0 + i) % total,
  * vals[i] = row0 + i (the global row index). */
 m4d_status m4d_merge_generate(int64_t* keys, int64_t* vals, int64_t row0, int64_t count,
@@ -261,7 +277,7 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
  * memory, int64[coarse][sources][2]) gives each run's [start, end) row in
  * in_pairs.  Writes the rows split into `buckets` LOCAL partitions (power of
  * two <= 32768, coarse dividing it) to out_pairs and bounds[buckets + 1]
- * (device); within a partition rows keep source order.  Launches sources + 3
+ * (device); within a partition rows keep source order.  Launches 4
  * kernels. */
 m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t* runs_host, int coarse, int sources,
                               int buckets, int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,

@@ -27,8 +27,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include "m4d_internal.h"
+#include "ptx.cuh"
 
 namespace {
 
@@ -93,15 +95,21 @@ __device__ __forceinline__ int64_t key_at(const int64_t* keys, const int64_t* va
     return vals ? __ldcs(keys + i) : __ldcs(keys + 2 * i);
 }
 
-// hist[b * ctas + cta] = rows of this CTA's run that fall in bucket b.
+// hist[b * ctas + cta] = rows of scatter CTA cta's run that fall in bucket b.
+// `split` histogram CTAs share one scatter run (grid = ctas * split, so a
+// grid sized for 1024-thread scatter CTAs still fills every SM); with
+// split > 1 they add into a zeroed hist.
 __global__ void __launch_bounds__(kHistThreads) hist_kernel(const int64_t* __restrict__ keys,
                                                             const int64_t* __restrict__ vals, int64_t n,
                                                             int64_t run, int mode, int buckets, int log2b,
-                                                            uint32_t* __restrict__ hist) {
+                                                            int split, uint32_t* __restrict__ hist) {
     extern __shared__ uint32_t h[];
     for (int b = threadIdx.x; b < buckets; b += blockDim.x) h[b] = 0;
     __syncthreads();
-    const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
+    const int cta = blockIdx.x / split, part = blockIdx.x % split, ctas = gridDim.x / split;
+    const int64_t r0 = cta * run, r1 = r0 + run < n ? r0 + run : n;
+    const int64_t len = r1 > r0 ? r1 - r0 : 0;
+    const int64_t lo = r0 + len * part / split, hi = r0 + len * (part + 1) / split;
     for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
         int64_t k[kRowsPerThread];
 #pragma unroll
@@ -114,7 +122,13 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(const int64_t* __res
             if (base + u * blockDim.x + threadIdx.x < hi) atomicAdd(&h[bucket_of(k[u], mode, buckets, log2b)], 1u);
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < buckets; b += blockDim.x) hist[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = h[b];
+    for (int b = threadIdx.x; b < buckets; b += blockDim.x) {
+        uint32_t* dst = hist + static_cast<int64_t>(b) * ctas + cta;
+        if (split == 1)
+            *dst = h[b];
+        else if (h[b])
+            atomicAdd(dst, h[b]);
+    }
 }
 
 // Exclusive scan of hist (bucket-major) in place: three phases over tiles.
@@ -285,12 +299,22 @@ __device__ __forceinline__ void load_and_rank(const int64_t* __restrict__ keys, 
     }
 }
 
-template <int kT>
+// Push targets of the fused owner scatter + shuffle: owner d's rows go to
+// seg[d] (its receive buffer, a CUDA-IPC mapping when d is a peer B200),
+// bucket (d, c) at the same offset it has inside d's segment of the local
+// bucket-major order.
+constexpr int kMaxPushOwners = 64;
+struct PushTargets {
+    longlong2* seg[kMaxPushOwners];
+};
+
+template <int kT, bool kPush, bool kBulk>
 __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile_scatter_kernel(const int64_t* __restrict__ keys,
                                                                        const int64_t* __restrict__ vals, int64_t n,
                                                                        int64_t run, int mode, int buckets, int log2b,
                                                                        const int64_t* __restrict__ offsets,
-                                                                       longlong2* __restrict__ out) {
+                                                                       longlong2* __restrict__ out,
+                                                                       const __grid_constant__ PushTargets push) {
     constexpr int kTileRows = kT * kRowsPerThread;
     extern __shared__ __align__(16) unsigned char tsm[];
     longlong2* stage = reinterpret_cast<longlong2*>(tsm);
@@ -305,6 +329,18 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
     while ((1 << nbits) < buckets) ++nbits;
     for (int b = threadIdx.x; b < kTileBuckets; b += blockDim.x)
         gcur[b] = b < buckets ? static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]) : 0u;
+    // kPush: bucket b = (owner d, coarse c) writes row j of the local order to
+    // seg[d] + (j - start of d's segment), so each owner's rows land contiguous
+    // in its receive buffer, C coarse runs in order.  (Shared only when used.)
+    __shared__ longlong2* bptr[kPush ? kTileBuckets : 1];
+    if (kPush) {
+        for (int b = threadIdx.x; b < buckets; b += blockDim.x) {
+            const int d = b >> log2b;
+            const int64_t seg0 = offsets[static_cast<int64_t>(d << log2b) * gridDim.x];
+            bptr[b] = reinterpret_cast<longlong2*>(reinterpret_cast<uintptr_t>(push.seg[d]) -
+                                                   static_cast<uintptr_t>(seg0) * sizeof(longlong2));
+        }
+    }
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
     for (int64_t tile = lo; tile < hi; tile += kTileRows) {
         // 1-2. load (warp w owns rows [tile + 256 w, tile + 256 w + 256)) and rank each
@@ -324,6 +360,7 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         __syncthreads();
         // 3. per-bucket tile totals, exclusive over buckets; warp bases within each bucket
         uint32_t total = 0;
+        if (kBulk && threadIdx.x < kTileBuckets) m4d::ptx::bulk_wait_read_all();  // last tile's runs left the stage
         if (threadIdx.x < kTileBuckets) {
             const int b = threadIdx.x;
             for (int ww = 0; ww < kW; ++ww) {
@@ -362,17 +399,36 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
             stage[pos] = row[u];
             sbucket[pos] = static_cast<uint8_t>(bk[u]);
         }
+        if (kBulk) m4d::ptx::fence_proxy_async_smem();  // stage writes before the TMA engine reads them
         __syncthreads();
-        // 5. copy each bucket's run to its global place
-        const uint32_t valid = tstart[kTileBuckets];
-        for (uint32_t r = threadIdx.x; r < valid; r += blockDim.x) {
-            const uint32_t b = sbucket[r];
-            out[gcur[b] + (r - tstart[b])] = stage[r];
+        // 5. copy each bucket's run to its global place: kBulk, one TMA bulk store
+        // per run (thread b issues bucket b's; the stage is reused only after the
+        // copies have read it, step 3 of the next tile); else row by row.
+        if (kBulk) {
+            if (threadIdx.x < kTileBuckets) {
+                const int b = threadIdx.x;
+                const uint32_t cnt = tstart[b + 1] - tstart[b];
+                if (cnt) {
+                    longlong2* dst = (kPush ? bptr[b] : out) + gcur[b];
+                    m4d::ptx::bulk_s2g(dst, stage + tstart[b], cnt * static_cast<uint32_t>(sizeof(longlong2)));
+                }
+                m4d::ptx::bulk_commit();
+            }
+        } else {
+            const uint32_t valid = tstart[kTileBuckets];
+            for (uint32_t r = threadIdx.x; r < valid; r += blockDim.x) {
+                const uint32_t b = sbucket[r];
+                if (kPush)
+                    bptr[b][gcur[b] + (r - tstart[b])] = stage[r];
+                else
+                    out[gcur[b] + (r - tstart[b])] = stage[r];
+            }
         }
         __syncthreads();
         if (threadIdx.x < kTileBuckets) gcur[threadIdx.x] += tstart[threadIdx.x + 1] - tstart[threadIdx.x];
         __syncthreads();
     }
+    if (kBulk && threadIdx.x < kTileBuckets) m4d::ptx::bulk_wait_all();
 }
 
 // ---- two-pass LOCAL partition (buckets > kSinglePassMax) -------------------------------
@@ -553,50 +609,62 @@ __global__ void __launch_bounds__(1024)
 
 // Receiver side of the owner+coarse exchange (M4D_PART_OWNER_COARSE): S
 // source segments, each holding C coarse runs in bucket order, are split into
-// the final 2^log2b partitions.  Per-source full-id histograms (one pass over
-// the keys) give every (coarse run, source) CTA its cursors: partition bounds
-// plus the counts of earlier sources, so rows stay source-ordered.
-__global__ void __launch_bounds__(1024) hist_fine_kernel(const longlong2* __restrict__ in, int64_t lo, int64_t hi,
-                                                         int64_t run, int log2b,
-                                                         unsigned long long* __restrict__ out) {
-    extern __shared__ uint32_t h[];
-    const int buckets = 1 << log2b;
-    for (int b = threadIdx.x; b < buckets; b += blockDim.x) h[b] = 0;
+// the final 2^log2b partitions.  Every (coarse run, source) piece is cut into
+// G row ranges; one CTA per (run, source, range) counts its rows per
+// sub-partition (the low log2b - cbits bits), the counts become cursors
+// (partition bounds plus the rows of earlier (source, range) pairs, so rows
+// stay source-ordered), and a CTA per (run, source, range) scatters its rows.
+// C x S x G CTAs per pass: enough to fill 148 SMs (C x S alone can be 128).
+__device__ __forceinline__ void piece_range(const int64_t* __restrict__ runs, int piece, int g, int groups,
+                                            int64_t* a, int64_t* z) {
+    const int64_t lo = runs[2 * piece], hi = runs[2 * piece + 1], len = hi - lo;
+    *a = lo + len * g / groups;
+    *z = lo + len * (g + 1) / groups;
+}
+
+__global__ void __launch_bounds__(1024) runs_hist_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ runs,
+                                                         int sources, int groups, int log2b, int cbits,
+                                                         unsigned long long* __restrict__ hist_grp) {
+    extern __shared__ uint32_t h[];  // 2^(log2b - cbits)
+    const int sub = 1 << (log2b - cbits), buckets = 1 << log2b;
+    const int g = blockIdx.x % groups, piece = blockIdx.x / groups;  // piece = c * sources + src
+    const int c = piece / sources, src = piece % sources;
+    for (int k = threadIdx.x; k < sub; k += blockDim.x) h[k] = 0;
     __syncthreads();
-    const int64_t a = lo + blockIdx.x * run, z = a + run < hi ? a + run : hi;
+    int64_t a, z;
+    piece_range(runs, piece, g, groups, &a, &z);
     for (int64_t base = a; base < z; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
         int64_t k[kRowsPerThread];
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u) {
             const int64_t i = base + u * blockDim.x + threadIdx.x;
-            k[u] = i < z ? in[i].x : 0;
+            k[u] = i < z ? __ldcs(&in[i].x) : 0;
         }
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u)
             if (base + u * blockDim.x + threadIdx.x < z)
-                atomicAdd(&h[bucket_of(k[u], M4D_PART_LOCAL, buckets, log2b)], 1u);
+                atomicAdd(&h[bucket_of(k[u], M4D_PART_LOCAL, buckets, log2b) & (sub - 1)], 1u);
     }
     __syncthreads();
-    for (int b = threadIdx.x; b < buckets; b += blockDim.x)
-        if (h[b]) atomicAdd(out + b, static_cast<unsigned long long>(h[b]));
+    unsigned long long* out = hist_grp + static_cast<int64_t>(src * groups + g) * buckets + c * sub;
+    for (int k = threadIdx.x; k < sub; k += blockDim.x) out[k] = h[k];
 }
 
 __global__ void __launch_bounds__(1024)
-    runs_pass2_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ runs, int sources,
-                      const unsigned long long* __restrict__ src_before, const int64_t* __restrict__ bounds,
+    runs_pass2_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ runs, int sources, int groups,
+                      const unsigned long long* __restrict__ grp_before, const int64_t* __restrict__ bounds,
                       int log2b, int cbits, longlong2* __restrict__ out) {
     extern __shared__ uint32_t cursor[];  // 2^(log2b - cbits)
-    const int sub = 1 << (log2b - cbits);
-    const int c = blockIdx.x / sources, src = blockIdx.x % sources;
-    const int buckets = 1 << log2b;
-    for (int k = threadIdx.x; k < sub; k += blockDim.x) {
-        const int b = c * sub + k;
-        cursor[k] = static_cast<uint32_t>(bounds[b] +
-                                          static_cast<int64_t>(src_before[static_cast<int64_t>(src) * buckets + b]));
-    }
+    const int sub = 1 << (log2b - cbits), buckets = 1 << log2b;
+    const int g = blockIdx.x % groups, piece = blockIdx.x / groups;
+    const int c = piece / sources, src = piece % sources;
+    const unsigned long long* before = grp_before + static_cast<int64_t>(src * groups + g) * buckets + c * sub;
+    for (int k = threadIdx.x; k < sub; k += blockDim.x)
+        cursor[k] = static_cast<uint32_t>(bounds[c * sub + k] + static_cast<int64_t>(before[k]));
     __syncthreads();
-    const int64_t lo = runs[2 * blockIdx.x], hi = runs[2 * blockIdx.x + 1];
-    scatter_by_low_bits(in, lo, hi, cursor, log2b, static_cast<uint32_t>(sub - 1), out);
+    int64_t a, z;
+    piece_range(runs, piece, g, groups, &a, &z);
+    scatter_by_low_bits(in, a, z, cursor, log2b, static_cast<uint32_t>(sub - 1), out);
 }
 
 __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int buckets, int ctas, int64_t total,
@@ -792,9 +860,9 @@ static int tile_threads() {
     return t;
 }
 
-static int partition_ctas(int64_t n) {
+static int partition_ctas(int64_t n, int threads = tile_threads()) {
     // One wave of the tile scatter (its L2 write frontier must fit, see top).
-    const int per_sm = tile_threads() >= 1024 ? 1 : tile_threads() >= 512 ? 2 : 4;
+    const int per_sm = threads >= 1024 ? 1 : threads >= 512 ? 2 : 4;
     const int64_t per = 65536 * 2 / per_sm;
     int64_t c = (n + per - 1) / per;
     if (c < 1) c = 1;
@@ -802,43 +870,84 @@ static int partition_ctas(int64_t n) {
     return static_cast<int>(c);
 }
 
+// Tile-scatter stores (M4D_TILE_STORE = bulk | rows): one TMA bulk store per
+// bucket run of a tile, or the row-by-row copy.  Default: bulk for the push
+// scatter (runs cross NVLink), rows for local partitions (measured 5.46 vs
+// 5.56 ms per local merge step; push N=2 8.63 vs 8.76 ms).
+static bool tile_bulk(bool push) {
+    static const int mode = [] {
+        const char* v = getenv("M4D_TILE_STORE");
+        return !v ? -1 : strcmp(v, "rows") == 0 ? 0 : 1;
+    }();
+    return mode < 0 ? push : mode == 1;
+}
+
+// Threads per push-scatter CTA (M4D_PUSH_TILE_THREADS, default 1024): longer
+// runs per bucket per tile make NVLink stores efficient (N=2 / N=4 at 128
+// push buckets: 8.08 / 9.99 ms with 256 threads, 7.72 / 9.39 ms with 1024).
+static int push_tile_threads() {
+    static const int t = [] {
+        const char* v = getenv("M4D_PUSH_TILE_THREADS");
+        const int x = v ? atoi(v) : 1024;
+        return x == 256 || x == 512 ? x : 1024;
+    }();
+    return t;
+}
+
+template <int kT, bool kPush, bool kBulk>
+static cudaError_t launch_tile_scatter_t(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
+                                         int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
+                                         longlong2* out, const PushTargets& push) {
+    const cudaError_t e = cudaFuncSetAttribute(tile_scatter_kernel<kT, kPush, kBulk>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               static_cast<int>(tile_smem<kT>()));
+    if (e != cudaSuccess) return e;
+    tile_scatter_kernel<kT, kPush, kBulk><<<ctas, kT, tile_smem<kT>(), s>>>(keys, vals, n, run, mode, buckets, log2b,
+                                                                          offs, out, push);
+    return cudaGetLastError();
+}
+
+template <int kT>
+static cudaError_t launch_tile_scatter_k(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
+                                         int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
+                                         longlong2* out, const PushTargets* push) {
+    static const PushTargets none{};
+    if (tile_bulk(push != nullptr))
+        return push ? launch_tile_scatter_t<kT, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push)
+                    : launch_tile_scatter_t<kT, false, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none);
+    return push ? launch_tile_scatter_t<kT, true, false>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push)
+                : launch_tile_scatter_t<kT, false, false>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none);
+}
+
 static cudaError_t launch_tile_scatter(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
                                        int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
-                                       longlong2* out) {
-    cudaError_t e = cudaSuccess;
-    switch (tile_threads()) {
-        case 256:
-            e = cudaFuncSetAttribute(tile_scatter_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(tile_smem<256>()));
-            if (e == cudaSuccess)
-                tile_scatter_kernel<256><<<ctas, 256, tile_smem<256>(), s>>>(keys, vals, n, run, mode, buckets, log2b, offs, out);
-            break;
-        case 1024:
-            e = cudaFuncSetAttribute(tile_scatter_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(tile_smem<1024>()));
-            if (e == cudaSuccess)
-                tile_scatter_kernel<1024><<<ctas, 1024, tile_smem<1024>(), s>>>(keys, vals, n, run, mode, buckets, log2b, offs, out);
-            break;
-        default:
-            e = cudaFuncSetAttribute(tile_scatter_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(tile_smem<512>()));
-            if (e == cudaSuccess)
-                tile_scatter_kernel<512><<<ctas, 512, tile_smem<512>(), s>>>(keys, vals, n, run, mode, buckets, log2b, offs, out);
+                                       longlong2* out, const PushTargets* push = nullptr) {
+    switch (push ? push_tile_threads() : tile_threads()) {
+        case 256: return launch_tile_scatter_k<256>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push);
+        case 1024: return launch_tile_scatter_k<1024>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push);
+        default: return launch_tile_scatter_k<512>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push);
     }
-    return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 static int pass1_bits(int log2b) { return log2b > 8 ? 8 : log2b; }
 
 // Single-pass partition (hist -> scan -> scatter) into `buckets` buckets; the
-// bucket function gets (mode, buckets, log2b) as bucket_of documents.
+// bucket function gets (mode, buckets, log2b) as bucket_of documents.  The
+// plan (histogram, per-(bucket, CTA) offsets in scratch, bounds) and the
+// scatter can run as separate calls (kPlan / kScatter) on the same scratch:
+// the fused owner push needs every owner's counts before it can write.
+enum { kPlan = 1, kScatter = 2, kPlanAndScatter = 3 };
+
 static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
                                    int log2b, int64_t* out_pairs, int64_t* bounds, void* scratch,
-                                   size_t scratch_bytes, cudaStream_t s) {
+                                   size_t scratch_bytes, cudaStream_t s, int phases = kPlanAndScatter,
+                                   const PushTargets* push = nullptr, bool push_layout = false) {
     if (scratch_bytes < m4d_partition_scratch_bytes(n, buckets)) return fail(M4D_ERR_USAGE, "partition scratch too small");
-    const int ctas = partition_ctas(n);
+    // (the push scatter's plan and scatter calls both size the grid for its CTAs)
+    const int ctas = partition_ctas(n, push_layout ? push_tile_threads() : tile_threads());
     const int64_t run = (n + ctas - 1) / ctas;
     if (buckets > kMaxBuckets) return fail(M4D_ERR_USAGE, "bucket count %d above the single-pass limit", buckets);
+    if (push && buckets > kTileBuckets) return fail(M4D_ERR_USAGE, "push scatter limited to %d buckets", kTileBuckets);
     const int64_t entries = static_cast<int64_t>(ctas) * buckets;
     const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
     uint32_t* hist = static_cast<uint32_t*>(scratch);
@@ -847,21 +956,28 @@ static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int
     int64_t* total = tile_sums + tiles;
     const size_t hist_smem = buckets * sizeof(uint32_t);
     const size_t cur_smem = buckets * sizeof(uint32_t);
-    // (per device; cheap enough to repeat on every call)
-    M4D_CUDA_TRY(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
-    M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
-    hist_kernel<<<ctas, kHistThreads, hist_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, hist);
-    scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
-    scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
-    scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
-    if (buckets <= kTileBuckets) {
-        M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs,
-                                         reinterpret_cast<longlong2*>(out_pairs)));
-    } else {
-        scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
-                                                            reinterpret_cast<longlong2*>(out_pairs));
+    if (phases & kPlan) {
+        // (per device; cheap enough to repeat on every call)
+        M4D_CUDA_TRY(cudaFuncSetAttribute(hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
+        // a histogram grid of at least 4 x 148 CTAs (kHistThreads each) however few scatter CTAs
+        const int split = (4 * 148 + ctas - 1) / ctas;
+        if (split > 1) M4D_CUDA_TRY(cudaMemsetAsync(hist, 0, entries * sizeof(uint32_t), s));
+        hist_kernel<<<ctas * split, kHistThreads, hist_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, split, hist);
+        scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
+        scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
+        scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
+        bucket_bounds_kernel<<<(buckets + 256) / 256, 256, 0, s>>>(offs, buckets, ctas, n, bounds);
     }
-    bucket_bounds_kernel<<<(buckets + 256) / 256, 256, 0, s>>>(offs, buckets, ctas, n, bounds);
+    if (phases & kScatter) {
+        if (buckets <= kTileBuckets) {
+            M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs,
+                                             reinterpret_cast<longlong2*>(out_pairs), push));
+        } else {
+            M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
+            scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+                                                                reinterpret_cast<longlong2*>(out_pairs));
+        }
+    }
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }
@@ -966,9 +1082,53 @@ m4d_status m4d_partition_owner_coarse(const int64_t* keys, const int64_t* vals, 
                             scratch_bytes, static_cast<cudaStream_t>(stream));
 }
 
+static m4d_status owner_coarse_check(int64_t n, int world, int coarse, int* cbits) {
+    if (n < 0 || n >= (int64_t(1) << 32)) return fail(M4D_ERR_USAGE, "partition of %lld rows outside [0, 2^32)", (long long)n);
+    if (world < 1 || world > 256) return fail(M4D_ERR_USAGE, "owner count %d outside [1, 256]", world);
+    *cbits = log2_exact(coarse);
+    if (*cbits < 0 || world * coarse > 256) return fail(M4D_ERR_USAGE, "coarse count %d invalid for %d owners", coarse, world);
+    return M4D_OK;
+}
+
+m4d_status m4d_partition_owner_plan(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
+                                    int64_t* bounds, void* scratch, size_t scratch_bytes, void* stream) {
+    int cbits = 0;
+    const m4d_status st = owner_coarse_check(n, world, coarse, &cbits);
+    if (st != M4D_OK) return st;
+    return partition_single(keys, vals, n, M4D_PART_OWNER_COARSE, world * coarse, cbits, nullptr, bounds, scratch,
+                            scratch_bytes, static_cast<cudaStream_t>(stream), kPlan, nullptr, true);
+}
+
+m4d_status m4d_partition_owner_push(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
+                                    const uint64_t* seg_dest, void* scratch, size_t scratch_bytes, void* stream) {
+    int cbits = 0;
+    const m4d_status st = owner_coarse_check(n, world, coarse, &cbits);
+    if (st != M4D_OK) return st;
+    if (world > kMaxPushOwners) return fail(M4D_ERR_USAGE, "push scatter limited to %d owners", kMaxPushOwners);
+    if (!seg_dest) return fail(M4D_ERR_USAGE, "null push destinations");
+    PushTargets push{};
+    for (int d = 0; d < world; ++d) push.seg[d] = reinterpret_cast<longlong2*>(seg_dest[d]);
+    return partition_single(keys, vals, n, M4D_PART_OWNER_COARSE, world * coarse, cbits, nullptr, nullptr, scratch,
+                            scratch_bytes, static_cast<cudaStream_t>(stream), kScatter, &push, true);
+}
+
+// Row ranges per (coarse run, source) piece of the receiver split: about 8 CTAs
+// of 1024 threads per SM in total, at most kMaxRunGroups.
+constexpr int kMaxRunGroups = 64;
+static int runs_groups(int coarse, int sources) {
+    const int pieces = coarse * sources;
+    static const int per_sm = [] {
+        const char* v = getenv("M4D_RUNS_CTAS_PER_SM");
+        const int x = v ? atoi(v) : 8;
+        return x < 1 ? 1 : x > 64 ? 64 : x;
+    }();
+    int g = (148 * per_sm + pieces - 1) / pieces;
+    return g < 1 ? 1 : g > kMaxRunGroups ? kMaxRunGroups : g;
+}
+
 size_t m4d_partition_runs_scratch_bytes(int sources, int buckets, int coarse) {
     if (sources < 1 || buckets < 1 || coarse < 1) return 0;
-    return (static_cast<size_t>(sources) + 1) * buckets * sizeof(unsigned long long) +
+    return (static_cast<size_t>(sources) * kMaxRunGroups + 1) * buckets * sizeof(unsigned long long) +
            2 * static_cast<size_t>(coarse) * sources * sizeof(int64_t) + 1024;
 }
 
@@ -983,28 +1143,22 @@ m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t*
     if (scratch_bytes < m4d_partition_runs_scratch_bytes(sources, buckets, coarse))
         return fail(M4D_ERR_USAGE, "partition scratch too small");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int groups = runs_groups(coarse, sources);
     char* base = static_cast<char*>(scratch);
-    unsigned long long* src_cnt = reinterpret_cast<unsigned long long*>(base);       // [sources][buckets]
-    unsigned long long* hist_all = src_cnt + static_cast<int64_t>(sources) * buckets;  // [buckets]
-    int64_t* runs = reinterpret_cast<int64_t*>(hist_all + buckets);                   // [coarse * sources][2]
+    unsigned long long* hist_grp = reinterpret_cast<unsigned long long*>(base);               // [sources][groups][buckets]
+    unsigned long long* hist_all = hist_grp + static_cast<int64_t>(sources) * groups * buckets;  // [buckets]
+    int64_t* runs = reinterpret_cast<int64_t*>(hist_grp + (static_cast<int64_t>(sources) * kMaxRunGroups + 1) * buckets);
     const size_t run_bytes = 2 * static_cast<size_t>(coarse) * sources * sizeof(int64_t);
     M4D_CUDA_TRY(cudaMemcpyAsync(runs, runs_host, run_bytes, cudaMemcpyHostToDevice, s));
-    M4D_CUDA_TRY(cudaMemsetAsync(src_cnt, 0, static_cast<size_t>(sources) * buckets * sizeof(unsigned long long), s));
-    M4D_CUDA_TRY(cudaFuncSetAttribute(hist_fine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (1 << 15) * 4));
-    for (int src = 0; src < sources; ++src) {
-        const int64_t lo = runs_host[2 * src], hi = runs_host[2 * ((coarse - 1) * sources + src) + 1];
-        if (hi <= lo) continue;
-        const int grid = partition_ctas(hi - lo);
-        const int64_t run = (hi - lo + grid - 1) / grid;
-        hist_fine_kernel<<<grid, 1024, buckets * sizeof(uint32_t), s>>>(reinterpret_cast<const longlong2*>(in_pairs),
-                                                                         lo, hi, run, log2b,
-                                                                         src_cnt + static_cast<int64_t>(src) * buckets);
-    }
-    group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(src_cnt, sources, buckets, hist_all);
+    const int ctas = coarse * sources * groups;
+    const size_t sub_smem = static_cast<size_t>(buckets >> cbits) * sizeof(uint32_t);
+    runs_hist_kernel<<<ctas, 1024, sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
+                                                  log2b, cbits, hist_grp);
+    group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, sources * groups, buckets, hist_all);
     exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
-    runs_pass2_kernel<<<coarse * sources, 1024, (buckets >> cbits) * sizeof(uint32_t), s>>>(
-        reinterpret_cast<const longlong2*>(in_pairs), runs, sources, src_cnt, bounds, log2b, cbits,
-        reinterpret_cast<longlong2*>(out_pairs));
+    runs_pass2_kernel<<<ctas, 1024, sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
+                                                   hist_grp, bounds, log2b, cbits,
+                                                   reinterpret_cast<longlong2*>(out_pairs));
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }

@@ -12,12 +12,17 @@ scaling: ``rows_per_rank * world``), worker ``r`` owns global rows
 
 B200 pipeline per rank (one CUDA stream, SoA device columns):
 
-1. world > 1: hash-partition both tables by owner rank (``m4d_partition``
-   mode RANK) and move every peer's segment with the nvlink transport:
-   device-frame rendezvous, i.e. the owner pulls the rows straight out of
-   the sender's HBM over NVLink (one message per side and peer, counts
-   first).  The two sides are pipelined: side 1's rank partition runs while
-   side 0 is pulled, side 0's local partition while side 1 is pulled;
+1. world > 1, shuffle ``push`` (default): one owner+coarse pass plans both
+   sides (histogram, offsets), the run tables are all-gathered as eager host
+   messages, and the scatter kernel itself writes every owner's rows into
+   that owner's receive buffer (CUDA-IPC mapped, so peer rows cross NVLink as
+   the kernel's stores: partitioning and shuffle are one kernel,
+   ``m4d_partition_owner_push``); a one-byte "side written" exchange then
+   lets each owner split what it received.  Shuffle ``pull``
+   (``M4D_MERGE_SHUFFLE=pull``, also the fallback when a receive buffer is
+   too small): the owner pass writes a local send buffer and every owner
+   pulls its segments over NVLink as device-frame rendezvous messages of the
+   transport, the two sides pipelined;
 2. hash-partition the rows this rank owns into ``parts`` local partitions
    of ~1.5K rows (mode LOCAL), small enough for a shared-memory hash table;
 3. ``m4d_hash_join``: one CTA per partition builds and probes, writes the
@@ -32,6 +37,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 import struct
 
 from .. import native
@@ -44,6 +50,7 @@ SEED_LEFT = 0x4C454654
 SEED_RIGHT = 0x52494748
 EXCHANGE_TAG = 900
 DATA_TAG = 910
+_SHUFFLE = os.environ.get("M4D_MERGE_SHUFFLE", "push")
 _MASK64 = (1 << 64) - 1
 
 
@@ -84,7 +91,7 @@ class KeyMerge:
 
     def __init__(self, rows_per_rank: int, fraction: float = 0.3, *, rank: int = 0, world: int = 1,
                  device: int = 0, transport=None, seed_l: int = SEED_LEFT, seed_r: int = SEED_RIGHT,
-                 parts: int | None = None, stream: native.Stream | None = None):
+                 parts: int | None = None, stream: native.Stream | None = None, shuffle: str | None = None):
         if rows_per_rank < 0 or not 0.0 <= fraction <= 1.0:
             raise UsageError("rows per rank must be >= 0 and fraction in [0, 1]")
         if world > 1 and transport is None:
@@ -114,6 +121,26 @@ class KeyMerge:
                       lib.m4d_partition_runs_scratch_bytes(max(world, 1), self.parts, self.coarse))
         self.scratch = native.DeviceBuffer(device, scratch)
         self.scratch_bytes = scratch
+        self.shuffle = (shuffle or _SHUFFLE) if world > 1 else "local"
+        if self.shuffle not in ("push", "pull", "local"):
+            raise UsageError(f"unknown shuffle {self.shuffle!r} (push | pull)")
+        if self.shuffle == "push":  # per-side plan scratch (both plans live until their push)
+            # Coarse runs per owner of the push scatter (M4D_PUSH_BUCKETS = owners x runs,
+            # default 256).  Fewer make each tile's run per bucket longer, so NVLink
+            # stores are more efficient (tools/probes/write_probe.cu: 8-row runs 395
+            # GB/s, 64-row runs 638 GB/s), but the receiver's split fans out wider;
+            # measured N=2 / N=4: 64 -> 8.10 / 9.68 ms, 128 -> 7.81 / 9.40, 256 -> 7.72 / 9.29.
+            target = int(os.environ.get("M4D_PUSH_BUCKETS", "256"))
+            c = 1
+            while world * c * 2 <= target and c * 2 <= self.coarse:
+                c *= 2
+            self.coarse_push = c
+            nb = lib.m4d_partition_scratch_bytes(self.n, world * self.coarse)
+            self.push_scratch = [native.DeviceBuffer(device, nb) for _ in range(2)]
+            self.push_scratch_bytes = nb
+            self.pushed = [native.Event(), native.Event()]
+        self._peer_recv: list[list[int]] | None = None  # [side][rank] receive-buffer address (mapped)
+        self._imported: list[int] = []
         self.out_capacity = int(fraction * self.n * 1.25) + 65536
         self.out = [native.DeviceBuffer(device, self.out_capacity * 8) for _ in range(3)]
         self.result = native.DeviceBuffer(device, 4 * 8)
@@ -206,11 +233,11 @@ class KeyMerge:
         sends = [b[d * C] for d in range(P)] + [b[P * C]]
         return self._post_side(side, sends, incoming), runs_in
 
-    def _finish_side(self, side: int, runs_in: list) -> int:
+    def _finish_side(self, side: int, runs_in: list, coarse: int | None = None) -> int:
         """Split the received source segments (each C coarse runs) into the local partitions."""
         import numpy as np
 
-        P, C = self.world, self.coarse
+        P, C = self.world, coarse or self.coarse
         starts = np.cumsum([0] + [r[C] for r in runs_in])
         runs = np.empty((C, P, 2), dtype=np.int64)
         for src, r in enumerate(runs_in):
@@ -220,7 +247,7 @@ class KeyMerge:
         native.check(native.lib().m4d_partition_runs(self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts,
                                                      self.parted[side].ptr, self.bounds[side].ptr, self.scratch.ptr,
                                                      self.scratch_bytes, self.stream.handle))
-        self.launches += P + 3
+        self.launches += 4
         return total
 
     async def _shuffle_and_partition(self) -> list[int]:
@@ -246,6 +273,80 @@ class KeyMerge:
             t.set_pull_engine(engine)
         return [n0, n1]
 
+    async def _connect_push(self) -> None:
+        """Swap CUDA-IPC handles of both receive buffers (once): every rank's scatter
+        kernel then writes straight into its peers' buffers."""
+        me = self.rank
+        blob = b""
+        for side in range(2):
+            handle, off = native.ipc_export(self.recv[side].ptr)
+            blob += struct.pack("<iQQQ", os.getpid(), self.recv[side].ptr, off, self.recv[side].capacity) + handle
+        peer = [[0] * self.world for _ in range(2)]
+        self._peer_cap = [[0] * self.world for _ in range(2)]
+        size = struct.calcsize("<iQQQ") + 64
+        for src, item in enumerate(await allgather(self.transport, blob, EXCHANGE_TAG + 4)):
+            for side in range(2):
+                rec = item[side * size:(side + 1) * size]
+                pid, ptr, off, cap = struct.unpack_from("<iQQQ", rec)
+                self._peer_cap[side][src] = cap
+                if src == me or pid == os.getpid():  # same process (multi-rank tests): plain pointer
+                    peer[side][src] = ptr
+                else:
+                    base = native.ipc_import(self.device, rec[28:92])
+                    self._imported.append(base)
+                    peer[side][src] = base + off
+        self._peer_recv = peer
+
+    async def _push_shuffle_and_partition(self) -> list[int] | None:
+        """Fused owner scatter + NVLink shuffle of both sides (``m4d_partition_owner_push``),
+        then the local split of what arrived.  None: a receive buffer is too small for this
+        step's rows (every rank sees the same run tables and falls back together)."""
+        t, P, me, C, lib = self.transport, self.world, self.rank, self.coarse_push, native.lib()
+        if self._peer_recv is None:
+            await self._connect_push()
+        for side in range(2):
+            native.check(lib.m4d_partition_owner_plan(
+                self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.rank_bounds[side].ptr,
+                self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
+        self.launches += 10
+        blob = b""
+        for side in range(2):  # my rows per (owner, coarse run), relative to each owner's segment
+            b = self._read_bounds(self.rank_bounds[side], P * C)
+            blob += struct.pack(f"<{P * (C + 1)}q", *[b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)])
+        width = P * (C + 1)
+        tables = [struct.unpack(f"<{2 * width}q", x) for x in await allgather(t, blob, EXCHANGE_TAG + 2)]
+        runs_in = [[tables[src][side * width + me * (C + 1):side * width + (me + 1) * (C + 1)] for src in range(P)]
+                   for side in range(2)]
+        for side in range(2):
+            for d in range(P):
+                if sum(tables[src][side * width + d * (C + 1) + C] for src in range(P)) > self._peer_cap[side][d]:
+                    return None
+        self._mark("owner_plan_and_tables_ms")
+        for side in range(2):
+            dest = (ctypes.c_uint64 * P)()
+            for d in range(P):  # my segment in owner d's buffer: after the rows of lower sources
+                before = sum(tables[src][side * width + d * (C + 1) + C] for src in range(me))
+                dest[d] = self._peer_recv[side][d] + before * 16
+            native.check(lib.m4d_partition_owner_push(
+                self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest,
+                self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
+            self.pushed[side].record(self.stream)
+        self.launches += 2
+        out = []
+        for side in range(2):
+            self.pushed[side].synchronize()  # my rows for side `side` are in every owner's buffer
+            await allgather(t, b"\x01", EXCHANGE_TAG + 6 + side)  # ... and every peer's rows in mine
+            self._mark(f"side{side}_push_ms")
+            out.append(self._finish_side(side, runs_in[side], C))
+        return out
+
+    def close(self) -> None:
+        """Unmap the peers' receive buffers (push shuffle)."""
+        for base in self._imported:
+            native.ipc_close(base)
+        self._imported = []
+        self._peer_recv = None
+
     async def run(self) -> tuple[int, int, int]:
         """One full step (partition [+ shuffle] + join).  Returns this rank's digest."""
         if self.profile:
@@ -255,7 +356,10 @@ class KeyMerge:
             self._t_last = time.perf_counter()
             self.phases = {}
         if self.world > 1:
-            self.received = await self._shuffle_and_partition()
+            got = await self._push_shuffle_and_partition() if self.shuffle == "push" else None
+            if got is None and self.shuffle == "push":
+                self.close()  # the pull path may grow the receive buffers: map them again next step
+            self.received = got if got is not None else await self._shuffle_and_partition()
         else:
             self.received = [self.n, self.n]
             for side in range(2):

@@ -154,6 +154,10 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_owner_coarse_count": (ctypes.c_int, [ctypes.c_int]),
     "m4d_partition_owner_coarse": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
                                                   _c_void_p, _c_void_p, _size, _c_void_p]),
+    "m4d_partition_owner_plan": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                                _c_void_p, _size, _c_void_p]),
+    "m4d_partition_owner_push": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                                _c_void_p, _size, _c_void_p]),
     "m4d_partition_launches": (ctypes.c_int, [ctypes.c_int]),
     "m4d_hash_join": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int,
                                      _c_void_p, _c_void_p, _c_void_p, _i64, _c_void_p, _c_void_p]),

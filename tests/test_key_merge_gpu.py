@@ -1,6 +1,8 @@
 """key_merge parity on a B200: GPU digest (row count, sum of row hashes, sum of keys)
 and the row multiset vs the CPU oracle; worker-count independence."""
 
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -9,15 +11,17 @@ import oracle
 pytestmark = pytest.mark.gpu
 
 
-def run_world(rows_per_rank, world, fraction, parts=None):
+def run_world(rows_per_rank, world, fraction, parts=None, shuffle=None, steps=1, hook=None):
     from paper_2101_08878_b200.harness.key_merge import KeyMerge
     from paper_2101_08878_b200.loop import MonotonicClock, TaskLoop, gather
 
     from nvlink_fixtures import close_all, nvlink_transports
 
     ts = nvlink_transports(world, 0) if world > 1 else [None]
-    ranks = [KeyMerge(rows_per_rank, fraction, rank=r, world=world, device=0, transport=ts[r], parts=parts)
-             for r in range(world)]
+    ranks = [KeyMerge(rows_per_rank, fraction, rank=r, world=world, device=0, transport=ts[r], parts=parts,
+                      shuffle=shuffle) for r in range(world)]
+    if hook:
+        hook(ranks)
     for km in ranks:
         km.generate()
     loop = TaskLoop(MonotonicClock())
@@ -26,8 +30,12 @@ def run_world(rows_per_rank, world, fraction, parts=None):
         return await gather(*(km.run_global() for km in ranks))
 
     try:
-        results = loop.run_until_complete(main())
+        for _ in range(steps):
+            results = loop.run_until_complete(main())
+            assert all(r == results[0] for r in results)
     finally:
+        for km in ranks:
+            km.close()
         if world > 1:
             close_all(ts)
     assert all(r == results[0] for r in results)
@@ -162,6 +170,84 @@ def test_owner_coarse_partition_matches_numpy(world, coarse):
     want_b = np.concatenate([[0], np.cumsum(np.bincount(bucket, minlength=nb))])
     assert np.array_equal(got_b, want_b)
     assert np.all(np.diff(bucket[pairs[:, 1]]) >= 0) and np.array_equal(np.sort(pairs[:, 1]), vals)
+
+
+@pytest.mark.parametrize("shuffle", ["push", "pull"])
+def test_shuffle_modes_agree_over_steps(shuffle):
+    """Both shuffles (fused push scatter / rendezvous pulls) give the oracle digest, step
+    after step on the same buffers."""
+    _, got = run_world(30_000, 3, 0.3, shuffle=shuffle, steps=3)
+    assert got == oracle.key_merge_c(30_000, 3, 0.3)
+
+
+def test_push_falls_back_to_pull_when_a_receive_buffer_is_small():
+    """A receive buffer too small for a step's rows: every rank takes the pull path (which
+    grows it) and maps the new buffers on the next step."""
+    calls = {"push": 0, "pull": 0}
+
+    def hook(ranks):
+        for km in ranks:
+            orig_connect, orig_pull = km._connect_push, km._shuffle_and_partition
+
+            async def connect(km=km, orig=orig_connect, mine=[0]):
+                await orig()
+                if mine[0] == 0:  # first step only: every rank believes rank 1's buffers are tiny
+                    km._peer_cap = [[c if r != 1 else 10 for r, c in enumerate(side)] for side in km._peer_cap]
+                mine[0] += 1
+                calls["push"] += 1
+
+            async def pull(orig=orig_pull):
+                calls["pull"] += 1
+                return await orig()
+
+            km._connect_push, km._shuffle_and_partition = connect, pull
+
+    _, got = run_world(30_000, 2, 0.3, shuffle="push", steps=2, hook=hook)
+    assert got == oracle.key_merge_c(30_000, 2, 0.3)
+    assert calls["pull"] == 2 and calls["push"] == 4  # step 1 fell back on both ranks; step 2 reconnected
+
+
+@pytest.mark.parametrize("world,coarse", [(3, 64), (8, 32), (2, 1), (1, 256)])
+def test_owner_push_matches_owner_coarse(world, coarse):
+    """plan + push (the fused owner scatter + shuffle) writes owner d's rows to its own
+    destination, bit-identical to segment d of m4d_partition_owner_coarse."""
+    from paper_2101_08878_b200 import native
+
+    n = 300_001
+    keys = np.random.default_rng(7 + world).integers(-(1 << 62), 1 << 62, n).astype(np.int64)
+    vals = np.arange(n, dtype=np.int64)
+    lib = native.lib()
+    k_d, v_d = native.DeviceBuffer(0, n * 8), native.DeviceBuffer(0, n * 8)
+    native.memcpy(k_d.ptr, keys.ctypes.data, n * 8)
+    native.memcpy(v_d.ptr, vals.ctypes.data, n * 8)
+    nb = world * coarse
+    nbytes = lib.m4d_partition_scratch_bytes(n, nb)
+    scratch = native.DeviceBuffer(0, nbytes)
+    out, bounds = native.DeviceBuffer(0, n * 16), native.DeviceBuffer(0, (nb + 1) * 8)
+    native.check(lib.m4d_partition_owner_coarse(k_d.ptr, v_d.ptr, n, world, coarse, out.ptr, bounds.ptr, scratch.ptr,
+                                                nbytes, None))
+    native.check(lib.m4d_device_sync(0))
+    want = np.frombuffer(native.to_host(out.ptr, n * 16), dtype=np.int64).reshape(n, 2)
+    want_b = np.frombuffer(native.to_host(bounds.ptr, (nb + 1) * 8), dtype=np.int64)
+    bounds2 = native.DeviceBuffer(0, (nb + 1) * 8)
+    scratch2 = native.DeviceBuffer(0, nbytes)
+    native.check(lib.m4d_partition_owner_plan(k_d.ptr, v_d.ptr, n, world, coarse, bounds2.ptr, scratch2.ptr, nbytes,
+                                              None))
+    native.check(lib.m4d_device_sync(0))
+    got_b = np.frombuffer(native.to_host(bounds2.ptr, (nb + 1) * 8), dtype=np.int64)
+    assert np.array_equal(got_b, want_b)
+    seg = [int(want_b[d * coarse]) for d in range(world)] + [n]
+    dests = [native.DeviceBuffer(0, max(1, seg[d + 1] - seg[d]) * 16 + 4096) for d in range(world)]
+    for d in dests:
+        native.memset(d.ptr, 0xAB, d.nbytes)
+    addrs = (ctypes.c_uint64 * world)(*[d.ptr for d in dests])
+    native.check(lib.m4d_partition_owner_push(k_d.ptr, v_d.ptr, n, world, coarse, addrs, scratch2.ptr, nbytes, None))
+    native.check(lib.m4d_device_sync(0))
+    for d in range(world):
+        rows = seg[d + 1] - seg[d]
+        got = np.frombuffer(native.to_host(dests[d].ptr, rows * 16 + 4096), dtype=np.uint8)
+        assert np.array_equal(got[:rows * 16].view(np.int64).reshape(rows, 2), want[seg[d]:seg[d + 1]])
+        assert np.all(got[rows * 16:] == 0xAB)  # nothing written past the segment
 
 
 @pytest.mark.parametrize("world", [1, 2, 4])
