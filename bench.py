@@ -518,6 +518,8 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
     # host frames (Dask control messages; the reference arm's frames): transport and comm path at 1 B
     host_lat = p2p.osu_latency(t, 1 - dist.rank, 1, 2000, False)
     host_pp = p2p.pingpong(t, 1 - dist.rank, 1, 2000, False)
+    # SM pull kernels this rank launched (device frames >= 64 KiB; smaller ones ride the copy engine)
+    launches = t.native_stats()["pull_kernel_launches"]
     t.close()
     cpu = None
     if dist.rank == 0 and not args.skip_cpu:
@@ -542,13 +544,17 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
                            "comm_path_latency_us": host_pp["mean_s"] * 1e6 if host_pp else None},
         "comm_path": {str(k): {"latency_us": v["mean_s"] * 1e6, "GBps": v["throughput_Bps"] / 1e9}
                       for k, v in pp.items() if v},
-        "gpu_launches": None,
+        "gpu_launches": launches,
+        "gpu_launches_note": "rank 0's rendezvous pull kernels over the whole sweep (no separate timed region)",
         "e2e": {"value": top["throughput_Bps"] / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0,
                 "note": f"send_payload/recv_payload ping-pong of {args.max_size}-byte device frames (2*size/RTT)"},
         "cpu_baseline": cpu,
-        "roofline": {"bound": "nvlink", "achieved": best["osu_bw_GBps"], "peak": 900.0, "unit": "GB/s",
-                     "frac": best["osu_bw_GBps"] / 900.0, "traffic": None, "peak_source": "nominal NVLink 5"},
+        "roofline": {"bound": "nvlink", "achieved": best["osu_bw_GBps"], "peak": 770.0, "unit": "GB/s",
+                     "frac": best["osu_bw_GBps"] / 770.0, "traffic": None,
+                     "peak_source": "measured peer copy per direction (B200_PROFILING.md)",
+                     "frac_of_nominal_900": best["osu_bw_GBps"] / 900.0,
+                     "by_size_GBps": {str(r["size"]): r["osu_bw_GBps"] for r in big}},
     }
 
 

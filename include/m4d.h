@@ -128,6 +128,7 @@ typedef struct m4d_transport_stats {
     uint64_t nvlink_bytes;      /* device payload bytes pulled peer-to-peer      */
     uint64_t rendezvous_pulls;
     uint64_t unexpected_messages;
+    uint64_t pull_kernel_launches; /* SM copy kernels issued for rendezvous pulls  */
 } m4d_transport_stats;
 
 /* transport_init: publishes this rank and maps the peers that are already up

@@ -17,7 +17,8 @@ int fail(int code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
 int alloc_info(const void* ptr, uint64_t* base, uint64_t* size, uint64_t* buffer_id);
 
 // Rendezvous pulls launched as one SM copy kernel (pull.cu).
-constexpr int kMaxPull = 8;
+constexpr int kMaxPull = 32;  // array capacity; messages per launch = pull_batch() (M4D_PULL_BATCH, default 8)
+int pull_batch();
 struct PullDesc {
     const uint8_t* src;
     uint8_t* dst;

@@ -8,10 +8,16 @@
 // per-launch ramp is shared when several messages are matched together.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "m4d_internal.h"
 
 namespace {
 
+// kIlp: each thread moves kIlp 16-byte words per round, all loads issued before
+// any store (the stores may alias the loads as far as the compiler knows, so
+// without this it keeps one load in flight per thread).
+template <int kIlp>
 __global__ void __launch_bounds__(512) pull_kernel(m4d::PullBatch batch) {
     const size_t tid = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -26,8 +32,15 @@ __global__ void __launch_bounds__(512) pull_kernel(m4d::PullBatch batch) {
         const size_t body = (len - head) / 16;
         const int4* s16 = reinterpret_cast<const int4*>(src + head);
         int4* d16 = reinterpret_cast<int4*>(dst + head);
-#pragma unroll 4
-        for (size_t i = tid; i < body; i += stride) d16[i] = __ldcs(s16 + i);
+        size_t i = tid;
+        for (; i + (kIlp - 1) * stride < body; i += kIlp * stride) {
+            int4 v[kIlp];
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u) v[u] = __ldcs(s16 + i + u * stride);
+#pragma unroll
+            for (int u = 0; u < kIlp; ++u) d16[i + u * stride] = v[u];
+        }
+        for (; i < body; i += stride) d16[i] = __ldcs(s16 + i);
         for (size_t i = tid; i < head; i += stride) dst[i] = src[i];
         for (size_t i = head + body * 16 + tid; i < len; i += stride) dst[i] = src[i];
     }
@@ -36,6 +49,24 @@ __global__ void __launch_bounds__(512) pull_kernel(m4d::PullBatch batch) {
 }  // namespace
 
 namespace m4d {
+
+int pull_batch() {
+    static const int b = [] {
+        const char* v = getenv("M4D_PULL_BATCH");
+        const int x = v ? atoi(v) : 8;
+        return x < 1 ? 1 : x > kMaxPull ? kMaxPull : x;
+    }();
+    return b;
+}
+
+static int pull_ilp() {
+    static const int k = [] {
+        const char* v = getenv("M4D_PULL_ILP");
+        const int x = v ? atoi(v) : 1;
+        return x >= 4 ? 4 : x >= 2 ? 2 : 1;
+    }();
+    return k;
+}
 
 int launch_pull_batch(const PullBatch& batch, cudaStream_t stream, int max_ctas) {
     size_t total = 0;
@@ -46,7 +77,11 @@ int launch_pull_batch(const PullBatch& batch, cudaStream_t stream, int max_ctas)
     unsigned grid = static_cast<unsigned>((total + 8191) / 8192);
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    pull_kernel<<<grid, 512, 0, stream>>>(batch);
+    switch (pull_ilp()) {
+        case 4: pull_kernel<4><<<grid, 512, 0, stream>>>(batch); break;
+        case 2: pull_kernel<2><<<grid, 512, 0, stream>>>(batch); break;
+        default: pull_kernel<1><<<grid, 512, 0, stream>>>(batch);
+    }
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? M4D_OK : cuda_fail(e, "pull kernel launch");
 }

@@ -415,9 +415,10 @@ void flush_pulls(m4d_transport* t) {
         } else if (e == cudaSuccess) {
             m4d::PullBatch batch;
             batch.n = 0;
-            for (j = i; j < v.size() && batch.n < m4d::kMaxPull && via_kernel(v[j]); ++j)
+            for (j = i; j < v.size() && batch.n < m4d::pull_batch() && via_kernel(v[j]); ++j)
                 batch.d[batch.n++] = m4d::PullDesc{v[j].src, v[j].recv->ptr, v[j].len};
             if (m4d::launch_pull_batch(batch, s, t->pull_ctas) != M4D_OK) e = cudaErrorLaunchFailure;
+            else t->stats.pull_kernel_launches++;
         }
         if (e == cudaSuccess) e = cudaEventRecord(ev, s);
         if (e != cudaSuccess) {
@@ -1006,7 +1007,7 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
         // Pulls matched here are launched in batches: a window of posted
         // receives becomes a few multi-message launches, not one launch per
         // post (the next progress() issues whatever is left).
-        if (t->pending_pulls.size() >= static_cast<size_t>(m4d::kMaxPull)) flush_pulls(t);
+        if (t->pending_pulls.size() >= static_cast<size_t>(m4d::pull_batch())) flush_pulls(t);
         flush_peer(t, peer);  // a truncation / empty-rendezvous FIN leaves now
     } else if (p.dead) {
         fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
