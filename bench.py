@@ -388,6 +388,10 @@ def km_cpu_sample(rows: int, target_rows: int, min_seconds: float = 10.0) -> dic
     return {"seconds": dt, "runs": done, "rows": rows, "full_ms": per * target_rows / rows * 1e3}
 
 
+def digest_rows(km) -> int:
+    return int(getattr(km, "rows_out", 0))
+
+
 def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
     from paper_2101_08878_b200 import native
     from paper_2101_08878_b200.harness.key_merge import KeyMerge
@@ -408,6 +412,7 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
     stream.synchronize()
     sampler.start()
     km.launches = 0
+    km.timing, km.kernel_ms = True, {"partition": 0.0, "join": 0.0}
     t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(args.steps):
@@ -421,6 +426,8 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
     if got != digest:
         raise RuntimeError("merge digest changed between steps")
     launches = km.launches
+    km.timing = False
+    kern = {k: v / args.steps for k, v in km.kernel_ms.items()}  # this rank's per-step event times
 
     # per-phase timing on this rank: one extra step with a synchronise at each phase boundary
     km.profile = True
@@ -442,6 +449,24 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
     roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": args.traffic,
                  "kernel": "whole merge step (partition + shuffle + join kernels)",
                  "algorithmic_bytes_per_step": alg, "t_roof_ms": max(t_hbm, t_nvl) * 1e3, "phases": phase})
+    # Per kernel group, CUDA events on the merge stream inside the timed steps (rank 0).
+    # join: reads both partitioned tables once, writes the output once.  partition (N=1):
+    # two passes per side, each reading and writing 16 B per row (the algorithm's own
+    # bytes; the strict step roofline above counts only the inputs once).
+    rows_in = km.received if dist.world > 1 else [km.n, km.n]
+    join_bytes = 16 * sum(rows_in) + 24 * digest_rows(km)
+    groups = {"join": {"ms": kern["join"], "bytes": join_bytes, "bound": "hbm", "peak": hbm_peak}}
+    if dist.world == 1:
+        groups["partition"] = {"ms": kern["partition"], "bytes": 2 * 2 * 32 * km.n + 2 * 8 * km.n, "bound": "hbm",
+                               "peak": hbm_peak, "note": "per side: full-id histogram (8 B/row) + 2 passes x 32 B/row"}
+    else:
+        groups["partition_and_shuffle"] = {
+            "ms": kern["partition"], "bytes": alg["nvlink"], "bound": "nvlink", "peak": NVLINK_PEER_GBS,
+            "note": "plan + push scatter of both sides, exchange, receiver split: NVLink bytes / time"}
+    for g in groups.values():
+        g["GBps"] = g["bytes"] / (g["ms"] * 1e-3) / 1e9 if g["ms"] else None
+        g["frac"] = g["GBps"] / g["peak"] if g["GBps"] else None
+    roof["kernel_groups"] = groups
 
     e2e = None
     if not args.skip_e2e:

@@ -284,6 +284,9 @@ m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t*
                               int buckets, int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
                               void* stream);
 size_t m4d_partition_runs_scratch_bytes(int sources, int buckets, int coarse);
+/* Target rows per local partition for the hash join's shared-memory tables (the
+ * harness sizes its partition count from it). */
+int m4d_join_partition_rows(void);
 /* Kernel launches (plus memsets) one m4d_partition call issues for that bucket count. */
 int m4d_partition_launches(int buckets);
 /* Inner join of partitioned build (left) and probe (right) pair arrays,

@@ -55,6 +55,18 @@ constexpr size_t kJoinSmem = kSlots * sizeof(uint32_t) + kChunk * (sizeof(int64_
 static_assert(kChunk < (1 << kIdxBits) && kIdxBits + 12 <= 32 && kJoinThreads * kJoinPer <= (1 << 12),
               "stage entry packing");
 static_assert(kJoinSmem <= 227 * 1024, "join shared memory");
+// Join variant "small" (M4D_JOIN=small): two 512-thread CTAs per SM, each with
+// half the table (8192 heads, 6500-row chunks), for ~6K-row partitions.  Twice
+// the resident warps make the join itself faster (1.74 -> 1.61 ms at 1e8
+// rows/side) but the 16384 partitions it needs slow pass 2 more (partition
+// 3.69 -> 3.95 ms): merge step 5.48 -> 5.60 ms, so "big" stays the default.
+constexpr int kSmallThreads = 512;
+constexpr int kSmallSlotBits = 13;
+constexpr int kSmallChunk = 6500;
+constexpr int kSmallStage = 128;
+constexpr size_t kSmallSmem = (1 << kSmallSlotBits) * sizeof(uint32_t) + kSmallChunk * (sizeof(int64_t) + sizeof(uint16_t)) +
+                              (kSmallThreads / 32) * kSmallStage * sizeof(uint32_t);
+static_assert(2 * (kSmallSmem + 1024) <= 228 * 1024, "two small join CTAs per SM");
 
 // mode LOCAL: log2b bits of the low word; RANK: owner of `buckets` ranks;
 // OWNER_COARSE: owner of buckets >> log2b ranks, then log2b low-word bits.
@@ -69,9 +81,10 @@ __device__ __forceinline__ uint32_t bucket_of(int64_t key, int mode, int buckets
 
 // Shared-table slot: a 32-bit multiplicative hash of the folded key (cheap;
 // independent of the partition bits, which come from splitmix64).
+template <int kBits = kSlotBits>
 __device__ __forceinline__ uint32_t slot_of(int64_t k) {
     const uint32_t x = static_cast<uint32_t>(k) ^ static_cast<uint32_t>(static_cast<uint64_t>(k) >> 32);
-    return (x * 0x9E3779B1u) >> (32 - kSlotBits);
+    return (x * 0x9E3779B1u) >> (32 - kBits);
 }
 
 __device__ __forceinline__ uint64_t row_hash(int64_t k, int64_t l, int64_t r) {
@@ -687,11 +700,13 @@ __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int bu
 // (re-walking only rows with several matches); (4) the warp emits the stage
 // with all 32 lanes: coalesced output stores, full-width row hashes.
 // Indices are 32-bit offsets from the partition start.
-__global__ void __launch_bounds__(kJoinThreads, 1)
+template <int kJoinThreads, int kSlotBits, int kChunk, int kStage, int kMinBlocks>
+__global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
     join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
                 const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
                 int64_t* __restrict__ ol, int64_t* __restrict__ orr, int64_t capacity,
                 unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ digest) {
+    constexpr int kSlots = 1 << kSlotBits;
     extern __shared__ __align__(16) unsigned char smem[];
     int64_t* bkey = reinterpret_cast<int64_t*>(smem);                                   // [kChunk]
     uint32_t* head = reinterpret_cast<uint32_t*>(smem + kChunk * sizeof(int64_t));      // [kSlots]
@@ -727,7 +742,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                 const int i = base + u * T + threadIdx.x;
                 if (i >= cn) break;  // rows ascend with u
                 bkey[i] = k[u];
-                const uint32_t old = atomicExch(&head[slot_of(k[u])], static_cast<uint32_t>(i));
+                const uint32_t old = atomicExch(&head[slot_of<kSlotBits>(k[u])], static_cast<uint32_t>(i));
                 link[i] = old == kEmpty ? kNil : static_cast<uint16_t>(old);
             }
         }
@@ -746,7 +761,7 @@ __global__ void __launch_bounds__(kJoinThreads, 1)
                 info[u] = 0;
                 if (base + u * T + static_cast<int>(threadIdx.x) >= pn) continue;
                 uint32_t c = 0, first = 0;
-                const uint32_t h0 = head[slot_of(r[u])];
+                const uint32_t h0 = head[slot_of<kSlotBits>(r[u])];
                 for (uint32_t i = h0 == kEmpty ? kNil : h0; i != kNil; i = link[i])
                     if (bkey[i] == r[u]) {
                         first = c ? first : i;
@@ -1112,6 +1127,15 @@ m4d_status m4d_partition_owner_push(const int64_t* keys, const int64_t* vals, in
                             scratch_bytes, static_cast<cudaStream_t>(stream), kScatter, &push, true);
 }
 
+// Join variant (M4D_JOIN = big | small, default big): see kSmallThreads.
+static bool join_small() {
+    static const bool b = [] {
+        const char* v = getenv("M4D_JOIN");
+        return v && strcmp(v, "small") == 0;
+    }();
+    return b;
+}
+
 // Row ranges per (coarse run, source) piece of the receiver split: about 8 CTAs
 // of 1024 threads per SM in total, at most kMaxRunGroups.
 constexpr int kMaxRunGroups = 64;
@@ -1163,6 +1187,8 @@ m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t*
     return M4D_OK;
 }
 
+int m4d_join_partition_rows(void) { return join_small() ? 6200 : 12400; }
+
 int m4d_partition_launches(int buckets) { return buckets > kSinglePassMax ? 9 : 6; }
 
 m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const int64_t* rpairs,
@@ -1170,14 +1196,23 @@ m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const in
                          int64_t* out_rvals, int64_t capacity, unsigned long long* result, void* stream) {
     if (parts < 0) return fail(M4D_ERR_USAGE, "negative partition count");
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    M4D_CUDA_TRY(cudaFuncSetAttribute(join_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kJoinSmem)));
     // result = {cursor, count, hash_sum, key_sum}
     M4D_CUDA_TRY(cudaMemsetAsync(result, 0, 4 * sizeof(unsigned long long), s));
-    if (parts)
-        join_kernel<<<parts, kJoinThreads, kJoinSmem, s>>>(reinterpret_cast<const longlong2*>(lpairs), lbounds,
-                                                           reinterpret_cast<const longlong2*>(rpairs), rbounds,
-                                                           out_keys, out_lvals, out_rvals, capacity, result,
-                                                           result + 1);
+    if (parts) {
+        const longlong2* lp = reinterpret_cast<const longlong2*>(lpairs);
+        const longlong2* rp = reinterpret_cast<const longlong2*>(rpairs);
+        if (join_small()) {
+            auto k = join_kernel<kSmallThreads, kSmallSlotBits, kSmallChunk, kSmallStage, 2>;
+            M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
+            k<<<parts, kSmallThreads, kSmallSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals, out_rvals, capacity,
+                                                       result, result + 1);
+        } else {
+            auto k = join_kernel<kJoinThreads, kSlotBits, kChunk, kStage, 1>;
+            M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kJoinSmem)));
+            k<<<parts, kJoinThreads, kJoinSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals, out_rvals, capacity,
+                                                     result, result + 1);
+        }
+    }
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }

@@ -60,10 +60,12 @@ def merge_band(total: int, fraction: float) -> int:
 
 
 def choose_parts(rows: int) -> int:
-    """Power-of-two partition count with ~1.5K rows per partition (8192-slot shared tables,
-    load <= 0.19, two join CTAs per SM), at most 65536."""
+    """Power-of-two partition count with about m4d_join_partition_rows() rows per
+    partition (~12K: one 1024-thread join CTA per SM with a 16384-head table), at most
+    65536."""
+    per = native.lib().m4d_join_partition_rows()
     parts = 1
-    while parts < 65536 and rows / parts > 12400:
+    while parts < 65536 and rows / parts > per:
         parts *= 2
     return parts
 
@@ -147,6 +149,11 @@ class KeyMerge:
         self.received = [0, 0]
         self.launches = 0
         self.profile = False  # diagnostics: synchronise and stamp each phase (never in timed runs)
+        # CUDA-event kernel timing inside timed runs (no synchronisation added): partition
+        # kernels (local or plan + push) and the join, summed over steps in kernel_ms
+        self.timing = False
+        self.kernel_ms = {"partition": 0.0, "join": 0.0}
+        self._ev = [native.Event() for _ in range(4)]
         self.phases: dict[str, float] = {}
 
     # -- data -------------------------------------------------------------------------------
@@ -355,6 +362,8 @@ class KeyMerge:
             self.stream.synchronize()
             self._t_last = time.perf_counter()
             self.phases = {}
+        if self.timing:
+            self._ev[0].record(self.stream)
         if self.world > 1:
             got = await self._push_shuffle_and_partition() if self.shuffle == "push" else None
             if got is None and self.shuffle == "push":
@@ -365,13 +374,20 @@ class KeyMerge:
             for side in range(2):
                 self._partition(self.inputs[side], self.n, 0, self.parts, self.parted[side], self.bounds[side])
         self._mark("local_partition_ms")
+        if self.timing:
+            self._ev[1].record(self.stream)
         while True:
             native.check(native.lib().m4d_hash_join(
                 self.parted[0].ptr, self.bounds[0].ptr, self.parted[1].ptr, self.bounds[1].ptr, self.parts,
                 self.out[0].ptr, self.out[1].ptr, self.out[2].ptr, self.out_capacity, self.result.ptr,
                 self.stream.handle))
             self.launches += 2
+            if self.timing:
+                self._ev[2].record(self.stream)
             raw = native.to_host(self.result.ptr, 32, self.stream)
+            if self.timing:  # the read-back synchronised the stream
+                self.kernel_ms["partition"] += self._ev[0].elapsed_ms(self._ev[1])
+                self.kernel_ms["join"] += self._ev[1].elapsed_ms(self._ev[2])
             self._mark("join_ms")
             produced, count, hsum, ksum = struct.unpack("<4Q", raw)
             if count <= self.out_capacity:

@@ -159,6 +159,7 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_partition_owner_push": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
                                                 _c_void_p, _size, _c_void_p]),
     "m4d_partition_launches": (ctypes.c_int, [ctypes.c_int]),
+    "m4d_join_partition_rows": (ctypes.c_int, []),
     "m4d_hash_join": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int,
                                      _c_void_p, _c_void_p, _c_void_p, _i64, _c_void_p, _c_void_p]),
     "m4d_fill_block_f64": (ctypes.c_int, [_c_void_p, _i64, _i64, _i64, _i64, _u64, _c_void_p]),
