@@ -75,6 +75,7 @@ m4d_status m4d_event_create(void** ev_out);
 m4d_status m4d_event_destroy(void* ev);
 m4d_status m4d_event_record(void* ev, void* stream);
 m4d_status m4d_event_sync(void* ev);
+m4d_status m4d_stream_wait_event(void* stream, void* ev);  /* later work on stream waits for ev */
 m4d_status m4d_event_elapsed_ms(void* start, void* stop, float* ms_out);
 m4d_status m4d_malloc(int device, size_t nbytes, void** ptr_out);
 m4d_status m4d_free(void* ptr);

@@ -141,6 +141,11 @@ m4d_status m4d_event_record(void* ev, void* stream) {
     return M4D_OK;
 }
 
+m4d_status m4d_stream_wait_event(void* stream, void* ev) {
+    M4D_CUDA_TRY(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(ev), 0));
+    return M4D_OK;
+}
+
 m4d_status m4d_event_sync(void* ev) {
     M4D_CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(ev)));
     return M4D_OK;

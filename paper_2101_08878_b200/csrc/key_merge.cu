@@ -875,9 +875,10 @@ static int tile_threads() {
     return t;
 }
 
-static int partition_ctas(int64_t n, int threads = tile_threads()) {
+static int partition_ctas(int64_t n, int threads = tile_threads(), int per_sm_cap = 4) {
     // One wave of the tile scatter (its L2 write frontier must fit, see top).
-    const int per_sm = threads >= 1024 ? 1 : threads >= 512 ? 2 : 4;
+    int per_sm = threads >= 1024 ? 1 : threads >= 512 ? 2 : 4;
+    if (per_sm > per_sm_cap) per_sm = per_sm_cap;
     const int64_t per = 65536 * 2 / per_sm;
     int64_t c = (n + per - 1) / per;
     if (c < 1) c = 1;
@@ -905,6 +906,26 @@ static int push_tile_threads() {
         const char* v = getenv("M4D_PUSH_TILE_THREADS");
         const int x = v ? atoi(v) : 1024;
         return x == 256 || x == 512 ? x : 1024;
+    }();
+    return t;
+}
+
+// Push-scatter CTAs per SM (M4D_PUSH_CTAS_PER_SM, default 4 = as many as fit):
+// fewer leave SM room for the receiver split running beside the push.
+static int push_ctas_per_sm() {
+    static const int c = [] {
+        const char* v = getenv("M4D_PUSH_CTAS_PER_SM");
+        const int x = v ? atoi(v) : 4;
+        return x < 1 ? 1 : x > 4 ? 4 : x;
+    }();
+    return c;
+}
+
+// Threads per receiver-split CTA (M4D_RUNS_THREADS = 512 | 1024, default 1024).
+static int runs_threads() {
+    static const int t = [] {
+        const char* v = getenv("M4D_RUNS_THREADS");
+        return v && atoi(v) == 512 ? 512 : 1024;
     }();
     return t;
 }
@@ -959,7 +980,8 @@ static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int
                                    const PushTargets* push = nullptr, bool push_layout = false) {
     if (scratch_bytes < m4d_partition_scratch_bytes(n, buckets)) return fail(M4D_ERR_USAGE, "partition scratch too small");
     // (the push scatter's plan and scatter calls both size the grid for its CTAs)
-    const int ctas = partition_ctas(n, push_layout ? push_tile_threads() : tile_threads());
+    const int ctas = push_layout ? partition_ctas(n, push_tile_threads(), push_ctas_per_sm())
+                                 : partition_ctas(n, tile_threads());
     const int64_t run = (n + ctas - 1) / ctas;
     if (buckets > kMaxBuckets) return fail(M4D_ERR_USAGE, "bucket count %d above the single-pass limit", buckets);
     if (push && buckets > kTileBuckets) return fail(M4D_ERR_USAGE, "push scatter limited to %d buckets", kTileBuckets);
@@ -1176,11 +1198,11 @@ m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t*
     M4D_CUDA_TRY(cudaMemcpyAsync(runs, runs_host, run_bytes, cudaMemcpyHostToDevice, s));
     const int ctas = coarse * sources * groups;
     const size_t sub_smem = static_cast<size_t>(buckets >> cbits) * sizeof(uint32_t);
-    runs_hist_kernel<<<ctas, 1024, sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
+    runs_hist_kernel<<<ctas, runs_threads(), sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
                                                   log2b, cbits, hist_grp);
     group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, sources * groups, buckets, hist_all);
     exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
-    runs_pass2_kernel<<<ctas, 1024, sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
+    runs_pass2_kernel<<<ctas, runs_threads(), sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
                                                    hist_grp, bounds, log2b, cbits,
                                                    reinterpret_cast<longlong2*>(out_pairs));
     M4D_CUDA_TRY(cudaGetLastError());

@@ -141,6 +141,11 @@ class KeyMerge:
             self.push_scratch = [native.DeviceBuffer(device, nb) for _ in range(2)]
             self.push_scratch_bytes = nb
             self.pushed = [native.Event(), native.Event()]
+            # M4D_MERGE_OVERLAP=1 (default): the receiver splits run on a second stream, so
+            # side 0's split (HBM-bound) overlaps side 1's push (NVLink-bound)
+            self.overlap = os.environ.get("M4D_MERGE_OVERLAP", "1") != "0"
+            self.split_stream = native.Stream(device) if self.overlap else self.stream
+            self.split_done = native.Event()
         self._peer_recv: list[list[int]] | None = None  # [side][rank] receive-buffer address (mapped)
         self._imported: list[int] = []
         self.out_capacity = int(fraction * self.n * 1.25) + 65536
@@ -180,6 +185,8 @@ class KeyMerge:
             import time
 
             self.stream.synchronize()
+            if getattr(self, "split_stream", None) is not None:
+                self.split_stream.synchronize()
             now = time.perf_counter()
             self.phases[name] = (now - self._t_last) * 1e3
             self._t_last = now
@@ -240,7 +247,7 @@ class KeyMerge:
         sends = [b[d * C] for d in range(P)] + [b[P * C]]
         return self._post_side(side, sends, incoming), runs_in
 
-    def _finish_side(self, side: int, runs_in: list, coarse: int | None = None) -> int:
+    def _finish_side(self, side: int, runs_in: list, coarse: int | None = None, stream=None) -> int:
         """Split the received source segments (each C coarse runs) into the local partitions."""
         import numpy as np
 
@@ -253,7 +260,7 @@ class KeyMerge:
         total = int(starts[-1])
         native.check(native.lib().m4d_partition_runs(self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts,
                                                      self.parted[side].ptr, self.bounds[side].ptr, self.scratch.ptr,
-                                                     self.scratch_bytes, self.stream.handle))
+                                                     self.scratch_bytes, (stream or self.stream).handle))
         self.launches += 4
         return total
 
@@ -344,7 +351,10 @@ class KeyMerge:
             self.pushed[side].synchronize()  # my rows for side `side` are in every owner's buffer
             await allgather(t, b"\x01", EXCHANGE_TAG + 6 + side)  # ... and every peer's rows in mine
             self._mark(f"side{side}_push_ms")
-            out.append(self._finish_side(side, runs_in[side], C))
+            out.append(self._finish_side(side, runs_in[side], C, self.split_stream))
+        if self.split_stream is not self.stream:  # the join waits for both splits
+            self.split_done.record(self.split_stream)
+            self.split_done.wait_on(self.stream)
         return out
 
     def close(self) -> None:

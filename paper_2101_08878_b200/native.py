@@ -117,6 +117,7 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_event_destroy": (ctypes.c_int, [_c_void_p]),
     "m4d_event_record": (ctypes.c_int, [_c_void_p, _c_void_p]),
     "m4d_event_sync": (ctypes.c_int, [_c_void_p]),
+    "m4d_stream_wait_event": (ctypes.c_int, [_c_void_p, _c_void_p]),
     "m4d_event_elapsed_ms": (ctypes.c_int, [_c_void_p, _c_void_p, ctypes.POINTER(ctypes.c_float)]),
     "m4d_malloc": (ctypes.c_int, [ctypes.c_int, _size, ctypes.POINTER(_c_void_p)]),
     "m4d_free": (ctypes.c_int, [_c_void_p]),
@@ -299,6 +300,10 @@ class Event:
 
     def synchronize(self) -> None:
         check(lib().m4d_event_sync(self.handle))
+
+    def wait_on(self, stream: Stream) -> None:
+        """Make later work on `stream` wait for this event (no host synchronisation)."""
+        check(lib().m4d_stream_wait_event(stream.handle, self.handle))
 
     def elapsed_ms(self, later: "Event") -> float:
         out = ctypes.c_float()
