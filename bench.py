@@ -373,19 +373,29 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
 # -- key_merge ------------------------------------------------------------------------------------
 
 
-def km_cpu_sample(rows: int, target_rows: int, min_seconds: float = 10.0) -> dict:
-    """Oracle (C restatement, 1 thread) joins of `rows` rows per side, repeated to >= min_seconds."""
+def km_cpu_sample(rows: int, target_rows: int, min_seconds: float = 10.0, fraction: float = 0.3) -> dict:
+    """Oracle CPU join (C, all host threads: radix partition + per-partition hash joins) of
+    `rows` resident rows per side (generated outside the timed region, as the GPU's inputs
+    are), repeated to >= min_seconds, scaled to `target_rows` rows per side."""
     import oracle
 
+    threads = len(os.sched_getaffinity(0))
+    band = oracle.merge_band(rows, fraction)
+    lk, lv = oracle.gen_side_c(0, rows, rows, oracle.SEED_LEFT, 0)
+    rk, rv = oracle.gen_side_c(0, rows, rows, oracle.SEED_RIGHT, band)
+    want = oracle.key_merge_c(rows, 1, fraction) if rows <= 2_000_000 else None
     done, t0 = 0, time.perf_counter()
     while True:
-        oracle.key_merge_c(rows, 1, 0.3)
+        got = oracle.join_mt_c(lk, lv, rk, rv, threads)
         done += 1
         dt = time.perf_counter() - t0
         if dt >= min_seconds:
             break
+    if want is not None and got != want:
+        raise RuntimeError("multithreaded CPU join disagrees with the oracle")
     per = dt / done
-    return {"seconds": dt, "runs": done, "rows": rows, "full_ms": per * target_rows / rows * 1e3}
+    return {"seconds": dt, "runs": done, "rows": rows, "threads": threads, "rows_out": got[0],
+            "full_ms": per * target_rows / rows * 1e3}
 
 
 def digest_rows(km) -> int:
@@ -501,10 +511,12 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
                   "full_rows_out": digest[0], "expected_fraction": args.fraction,
                   "observed_fraction": digest[0] / max(1, args.rows * dist.world)}
         if not args.skip_cpu:
-            c = km_cpu_sample(min(args.rows, 2_000_000), args.rows * dist.world, min(10.0, args.cpu_seconds))
-            cpu = {"value": c["full_ms"], "unit": "ms", "cores": 1, "kind": "port",
-                   "sample": f"oracle C hash join (1 thread), {c['rows']} rows/side x {c['runs']} runs in "
-                             f"{c['seconds']:.1f} s, extrapolated linearly to {args.rows * dist.world} rows/side"}
+            target = args.rows * dist.world
+            c = km_cpu_sample(min(target, 100_000_000), target, min(10.0, args.cpu_seconds), args.fraction)
+            cpu = {"value": c["full_ms"], "unit": "ms", "cores": c["threads"], "kind": "port",
+                   "sample": f"oracle C join ({c['threads']} threads, radix partition + per-partition hash joins) "
+                             f"of {c['rows']} resident rows/side x {c['runs']} runs in {c['seconds']:.1f} s"
+                             + ("" if c["rows"] == target else f", scaled linearly to {target} rows/side")}
     if dist.rank != 0:
         return None
     return {
@@ -791,9 +803,14 @@ def reference_transpose_sum(args) -> dict:
 
 def reference_key_merge(args) -> dict:
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    per = [km_cpu_sample(min(args.rows, 2_000_000), args.rows * world, max(2.0, args.cpu_seconds / max(1, args.steps)))
+    target = args.rows * world
+    rows = min(target, 100_000_000)
+    per = [km_cpu_sample(rows, target, max(2.0, args.cpu_seconds / max(1, args.steps)), args.fraction)
            for _ in range(args.steps)]
     value = statistics.mean(p["full_ms"] for p in per)
+    threads = per[0]["threads"]
+    sample = (f"oracle C join ({threads} threads, radix partition + per-partition hash joins) of {rows} resident "
+              f"rows/side per step" + ("" if rows == target else f", scaled linearly to {target} rows/side"))
     return {
         "impl": "reference",
         "metric": f"merge wall time ({args.rows} rows/side/GPU, int64 key, fraction {args.fraction})",
@@ -801,8 +818,7 @@ def reference_key_merge(args) -> dict:
         "ms_per_step": value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
         "config": {"workload": "key_merge", "rows_per_side_per_gpu": args.rows, "fraction": args.fraction},
-        "cpu_baseline": {"value": value, "unit": "ms", "cores": 1, "kind": "port",
-                         "sample": f"oracle C hash join, {per[0]['rows']} rows/side per step, extrapolated"},
+        "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 

@@ -77,6 +77,8 @@ def lib():
         h.orc_row_hash.argtypes = [i64, i64, i64]
         h.orc_hash_join.restype = ctypes.c_int
         h.orc_hash_join.argtypes = [p, p, i64, p, p, i64, p, p, p, i64, ctypes.POINTER(JoinResult)]
+        h.orc_join_mt.restype = ctypes.c_int
+        h.orc_join_mt.argtypes = [p, p, i64, p, p, i64, ctypes.c_int, ctypes.POINTER(JoinResult)]
         h.orc_key_merge.restype = ctypes.c_int
         h.orc_key_merge.argtypes = [i64, ctypes.c_int, ctypes.c_double, u64, u64, ctypes.POINTER(JoinResult)]
         _lib = h
@@ -224,6 +226,17 @@ def hash_join_c(lk, lv, rk, rv, want_rows: bool = False):
         if n > cap:
             raise RuntimeError("oracle output capacity exceeded")
         return res.as_tuple(), tuple(o[:n] for o in outs)
+    return res.as_tuple()
+
+
+def join_mt_c(lk, lv, rk, rv, threads: int) -> tuple[int, int, int]:
+    """Digest of the inner join of resident tables with `threads` POSIX threads (radix
+    partition + per-partition hash joins): the timed CPU baseline of key_merge."""
+    lk, lv, rk, rv = (np.ascontiguousarray(a, dtype=np.int64) for a in (lk, lv, rk, rv))
+    res = JoinResult()
+    rc = lib().orc_join_mt(_ptr(lk), _ptr(lv), len(lk), _ptr(rk), _ptr(rv), len(rk), threads, ctypes.byref(res))
+    if rc:
+        raise RuntimeError(f"orc_join_mt failed ({rc})")
     return res.as_tuple()
 
 

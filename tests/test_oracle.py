@@ -109,3 +109,17 @@ def test_hash_join_rows_match_pandas_multiset():
     want = sorted(zip(df["key"], df["lval"], df["rval"]))
     assert got == want and count == len(want)
     assert (count, hs, ks) == oracle.join_digest_np(df["key"].to_numpy(), df["lval"].to_numpy(), df["rval"].to_numpy())
+
+
+@pytest.mark.parametrize("rows,threads", [(0, 4), (1, 1), (20_000, 1), (20_000, 7), (300_000, 8)])
+def test_multithreaded_join_digest_equals_single_threaded(rows, threads):
+    """orc_join_mt (the timed CPU baseline: radix partition + per-partition joins) gives the
+    key_merge oracle's digest for every thread count, duplicates included."""
+    band = oracle.merge_band(rows, 0.3) if rows else 0
+    lk, lv = oracle.gen_side_c(0, rows, max(rows, 1), oracle.SEED_LEFT, 0)
+    rk, rv = oracle.gen_side_c(0, rows, max(rows, 1), oracle.SEED_RIGHT, band)
+    assert oracle.join_mt_c(lk, lv, rk, rv, threads) == oracle.key_merge_c(rows, 1, 0.3)
+    m = min(rows, 20_000)
+    dup = np.arange(m, dtype=np.int64) % 97  # heavy duplicates
+    assert (oracle.join_mt_c(dup, lv[:m], dup[::-1].copy(), rv[:m], threads)
+            == oracle.hash_join_c(dup, lv[:m], dup[::-1].copy(), rv[:m]))
