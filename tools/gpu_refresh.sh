@@ -13,3 +13,6 @@ run 4 29568 --workload storm --steps 3 --warmup 3 > gpurun_out/storm_n4.json 2> 
 python bench.py --impl reference > gpurun_out/ts_ref.json 2> gpurun_out/ts_ref.err; echo ts_ref=$?
 python bench.py --impl reference --workload key_merge > gpurun_out/km_ref.json 2> gpurun_out/km_ref.err; echo km_ref=$?
 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
+# key_merge M-S (strong: 1e8 rows per side in total) at N=2 and N=4
+run 2 29601 --workload key_merge --rows 50000000 --steps 5 --warmup 3 --skip-cpu > gpurun_out/km_ms_n2.json 2>/dev/null; echo ms2=$?
+run 4 29602 --workload key_merge --rows 25000000 --steps 5 --warmup 3 --skip-cpu > gpurun_out/km_ms_n4.json 2>/dev/null; echo ms4=$?
