@@ -705,7 +705,7 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
     join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
                 const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
                 int64_t* __restrict__ ol, int64_t* __restrict__ orr, int64_t capacity,
-                unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ digest) {
+                unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ digest, int parts) {
     constexpr int kSlots = 1 << kSlotBits;
     extern __shared__ __align__(16) unsigned char smem[];
     int64_t* bkey = reinterpret_cast<int64_t*>(smem);                                   // [kChunk]
@@ -717,13 +717,25 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
     constexpr int T = kJoinThreads;
     constexpr int kPer = kJoinPer;
     uint32_t* stage = stage_all + warp * kStage;
-    const longlong2* brow = build + loff[blockIdx.x];
-    const longlong2* prow = probe + roff[blockIdx.x];
-    if (loff[blockIdx.x + 1] - loff[blockIdx.x] > INT32_MAX || roff[blockIdx.x + 1] - roff[blockIdx.x] > INT32_MAX)
-        __trap();  // partitions are < 2^31 rows (32-bit offsets); fail loudly rather than mis-join
-    const int bn = static_cast<int>(loff[blockIdx.x + 1] - loff[blockIdx.x]);
-    const int pn = static_cast<int>(roff[blockIdx.x + 1] - roff[blockIdx.x]);
     unsigned long long cnt = 0, hsum = 0, ksum = 0;
+    // grid = parts: one partition per CTA; a smaller (persistent) grid walks partitions
+    // blockIdx.x, + gridDim.x, ... and prefetches the next one's rows into L2 meanwhile.
+    for (int part = blockIdx.x; part < parts; part += gridDim.x) {
+    if (part != static_cast<int>(blockIdx.x)) __syncthreads();  // the previous partition's table is done
+    if (threadIdx.x == 0 && part + static_cast<int>(gridDim.x) < parts) {
+        const int nx = part + gridDim.x;
+        const int64_t ln = loff[nx + 1] - loff[nx], rn = roff[nx + 1] - roff[nx];
+        const uint32_t lb = static_cast<uint32_t>((ln < (1 << 20) ? ln : (1 << 20)) * 16);
+        const uint32_t rb = static_cast<uint32_t>((rn < (1 << 20) ? rn : (1 << 20)) * 16);
+        if (lb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(build + loff[nx]), "r"(lb) : "memory");
+        if (rb) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(probe + roff[nx]), "r"(rb) : "memory");
+    }
+    const longlong2* brow = build + loff[part];
+    const longlong2* prow = probe + roff[part];
+    if (loff[part + 1] - loff[part] > INT32_MAX || roff[part + 1] - roff[part] > INT32_MAX)
+        __trap();  // partitions are < 2^31 rows (32-bit offsets); fail loudly rather than mis-join
+    const int bn = static_cast<int>(loff[part + 1] - loff[part]);
+    const int pn = static_cast<int>(roff[part + 1] - roff[part]);
     for (int c0 = 0; c0 < bn; c0 += kChunk) {
         const int cn = bn - c0 < kChunk ? bn - c0 : kChunk;
         const longlong2* crow = brow + c0;
@@ -825,6 +837,7 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
             }
         }
     }
+    }  // partitions
     for (int o = 16; o; o >>= 1) {
         cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         hsum += __shfl_xor_sync(0xffffffffu, hsum, o);
@@ -1158,6 +1171,16 @@ static bool join_small() {
     return b;
 }
 
+// Join grid: one CTA per partition, or (M4D_JOIN_PERSIST=1) one wave of
+// persistent CTAs that walk the partitions and prefetch the next one into L2.
+static int join_grid(int parts, int per_sm) {
+    static const bool persist = [] {
+        const char* v = getenv("M4D_JOIN_PERSIST");
+        return v && atoi(v) == 1;
+    }();
+    return persist && parts > 148 * per_sm ? 148 * per_sm : parts;
+}
+
 // Row ranges per (coarse run, source) piece of the receiver split: about 8 CTAs
 // of 1024 threads per SM in total, at most kMaxRunGroups.
 constexpr int kMaxRunGroups = 64;
@@ -1226,13 +1249,13 @@ m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const in
         if (join_small()) {
             auto k = join_kernel<kSmallThreads, kSmallSlotBits, kSmallChunk, kSmallStage, 2>;
             M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
-            k<<<parts, kSmallThreads, kSmallSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals, out_rvals, capacity,
-                                                       result, result + 1);
+            k<<<join_grid(parts, 2), kSmallThreads, kSmallSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals,
+                                                                     out_rvals, capacity, result, result + 1, parts);
         } else {
             auto k = join_kernel<kJoinThreads, kSlotBits, kChunk, kStage, 1>;
             M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kJoinSmem)));
-            k<<<parts, kJoinThreads, kJoinSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals, out_rvals, capacity,
-                                                     result, result + 1);
+            k<<<join_grid(parts, 1), kJoinThreads, kJoinSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals,
+                                                                   out_rvals, capacity, result, result + 1, parts);
         }
     }
     M4D_CUDA_TRY(cudaGetLastError());
