@@ -125,14 +125,26 @@ class Dist:
         self.world = int(os.environ.get("WORLD_SIZE", "1"))
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.device = self.local_rank
         self.torch = None
         self.gloo = None
         if self.world > 1:
             import torch
             import torch.distributed as dist
 
-            torch.cuda.set_device(self.local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
+            # More ranks than GPUs (a functional check of an N-rank run on a smaller box,
+            # never a measurement): ranks share GPUs round-robin, NCCL cannot, so the
+            # default group is gloo too.
+            ngpu = torch.cuda.device_count()
+            local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(self.world)))
+            shared = ngpu and local_world > ngpu
+            self.device = self.local_rank % ngpu if shared else self.local_rank
+            torch.cuda.set_device(self.device)
+            if shared:
+                print(f"bench: {local_world} ranks on {ngpu} GPUs (shared; functional check only)", file=sys.stderr)
+                dist.init_process_group("gloo")
+            else:
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
             self.gloo = dist.new_group(backend="gloo")
             self.torch = torch
             self.dist = dist
@@ -227,7 +239,7 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
     from paper_2101_08878_b200.harness.transpose_sum import TransposeSum
 
     n, b = args.n, args.block
-    device = dist.local_rank
+    device = dist.device
     native.set_device(device)
     exchange = None
     if dist.world > 1:
@@ -407,7 +419,7 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
     from paper_2101_08878_b200.harness.key_merge import KeyMerge
     from paper_2101_08878_b200.loop import MonotonicClock, TaskLoop
 
-    device = dist.local_rank
+    device = dist.device
     native.set_device(device)
     transport = open_transport(dist, device) if dist.world > 1 else None
     km = KeyMerge(args.rows, args.fraction, rank=dist.rank, world=dist.world, device=device, transport=transport)
@@ -540,7 +552,7 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
 
     if dist.world != 2:
         raise SystemExit("--workload p2p needs exactly 2 ranks (torchrun --nproc-per-node 2)")
-    device = dist.local_rank
+    device = dist.device
     t = open_transport(dist, device)
     rows, n = [], 1
     while n <= args.max_size:
@@ -616,8 +628,8 @@ def bench_storm(args, dist: Dist, peaks: dict) -> dict | None:
 
     if dist.world < 2:
         raise SystemExit("--workload storm needs >= 2 ranks (torchrun --nproc-per-node N)")
-    t = open_transport(dist, dist.local_rank)
-    sampler = ClockSampler(dist.local_rank)
+    t = open_transport(dist, dist.device)
+    sampler = ClockSampler(dist.device)
     sampler.start()
     r = storm.run_worker(storm.namespace_of("paper_2101_08878_b200"), t, dist.allgather_bytes,
                          conns=args.conns, total=args.frames, rounds=args.steps, warmup=args.warmup)
