@@ -126,6 +126,7 @@ class Dist:
         self.rank = int(os.environ.get("RANK", "0"))
         self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
         self.device = self.local_rank
+        self.shared = False
         self.torch = None
         self.gloo = None
         if self.world > 1:
@@ -139,6 +140,7 @@ class Dist:
             local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(self.world)))
             shared = ngpu and local_world > ngpu
             self.device = self.local_rank % ngpu if shared else self.local_rank
+            self.shared = bool(shared)
             torch.cuda.set_device(self.device)
             if shared:
                 print(f"bench: {local_world} ranks on {ngpu} GPUs (shared; functional check only)", file=sys.stderr)
@@ -891,6 +893,8 @@ def main(argv=None) -> int:
     finally:
         dist.close()
     if line is not None:
+        if dist.shared:
+            line["functional_check_only"] = "more ranks than GPUs: ranks shared GPUs; not a measurement"
         emit(line)
     return 0
 
