@@ -919,13 +919,15 @@ int log2_exact(int v) {
 
 using m4d::fail;
 
-// Threads per tile-scatter CTA (M4D_TILE_THREADS = 256 | 512 | 1024, default 256): sets the
-// resident CTAs per SM (2048 / threads, at most 4) and so the partition grid.
+// Threads per tile-scatter CTA (M4D_TILE_THREADS = 256 | 512 | 1024, default 512): sets the
+// resident CTAs per SM (2048 / threads, at most 4) and so the partition grid.  Measured
+// (1e8 rows/side, both sides' partitions): ballot ranking 1.02 / 1.12 / 1.35 ms per tile
+// scatter at 256 / 512 / 1024; atomic ranking 3.47 / 3.27 / 3.66 ms for all partitions.
 static int tile_threads() {
     static const int t = [] {
         const char* v = getenv("M4D_TILE_THREADS");
-        const int x = v ? atoi(v) : 256;  // measured: 1.02 / 1.12 / 1.35 ms at 256 / 512 / 1024 (1e8 rows)
-        return x == 512 || x == 1024 ? x : 256;
+        const int x = v ? atoi(v) : 512;
+        return x == 256 || x == 1024 ? x : 512;
     }();
     return t;
 }
