@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
     uint16_t* wbase = reinterpret_cast<uint16_t*>(sbucket + kTileRows);  // [warps][256]
     __shared__ uint32_t gcur[kTileBuckets];
     __shared__ uint32_t tstart[kTileBuckets + 1];
+    __shared__ uint32_t dbase[kTileBuckets];  // global row of a tile row r in bucket b: dbase[b] + r
     __shared__ uint32_t scan_tmp[kTileBuckets / 32];
     constexpr int kW = kT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -413,8 +414,11 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         else
             load_and_rank<false, 0>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, nbits, wb, row, bk, off);
         __syncthreads();
-        // 3. per-bucket tile totals, exclusive over buckets; warp bases within each bucket
-        uint32_t total = 0;
+        // 3. per-bucket tile totals, exclusive over buckets; warp bases within each bucket.
+        // Thread b also owns bucket b's cursor: it records where the tile's run goes
+        // (dbase) and advances gcur itself, so no barrier follows the copy-out (the
+        // next tile's first barrier already orders it before anything it reads).
+        uint32_t total = 0, tst = 0, gstart = 0;
         if (kBulk && threadIdx.x < kTileBuckets) m4d::ptx::bulk_wait_read_all();  // last tile's runs left the stage
         if (threadIdx.x < kTileBuckets) {
             const int b = threadIdx.x;
@@ -440,10 +444,14 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
                 if (lane >= o) incl += y;
             }
-            tstart[b] = before + incl - total;
+            tst = before + incl - total;
+            tstart[b] = tst;
             if (b == kTileBuckets - 1) tstart[kTileBuckets] = before + incl;
+            gstart = gcur[b];
+            dbase[b] = gstart - tst;  // (mod 2^32: dbase[b] + r with r >= tst is the row)
+            gcur[b] = gstart + total;
             for (int ww = 0; ww < kW; ++ww)
-                wbase[ww * kTileBuckets + b] = static_cast<uint16_t>(wbase[ww * kTileBuckets + b] + tstart[b]);
+                wbase[ww * kTileBuckets + b] = static_cast<uint16_t>(wbase[ww * kTileBuckets + b] + tst);
         }
         __syncthreads();
         // 4. stage rows in bucket order
@@ -462,10 +470,9 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         if (kBulk) {
             if (threadIdx.x < kTileBuckets) {
                 const int b = threadIdx.x;
-                const uint32_t cnt = tstart[b + 1] - tstart[b];
-                if (cnt) {
-                    longlong2* dst = (kPush ? bptr[b] : out) + gcur[b];
-                    m4d::ptx::bulk_s2g(dst, stage + tstart[b], cnt * static_cast<uint32_t>(sizeof(longlong2)));
+                if (total) {
+                    longlong2* dst = (kPush ? bptr[b] : out) + gstart;
+                    m4d::ptx::bulk_s2g(dst, stage + tst, total * static_cast<uint32_t>(sizeof(longlong2)));
                 }
                 m4d::ptx::bulk_commit();
             }
@@ -474,14 +481,11 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
             for (uint32_t r = threadIdx.x; r < valid; r += blockDim.x) {
                 const uint32_t b = sbucket[r];
                 if (kPush)
-                    bptr[b][gcur[b] + (r - tstart[b])] = stage[r];
+                    bptr[b][dbase[b] + r] = stage[r];
                 else
-                    out[gcur[b] + (r - tstart[b])] = stage[r];
+                    out[dbase[b] + r] = stage[r];
             }
         }
-        __syncthreads();
-        if (threadIdx.x < kTileBuckets) gcur[threadIdx.x] += tstart[threadIdx.x + 1] - tstart[threadIdx.x];
-        __syncthreads();
     }
     if (kBulk && threadIdx.x < kTileBuckets) m4d::ptx::bulk_wait_all();
 }
