@@ -751,7 +751,8 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
     join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
                 const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
                 int64_t* __restrict__ ol, int64_t* __restrict__ orr, int64_t capacity,
-                unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ digest, int parts) {
+                unsigned long long* __restrict__ cursor, unsigned long long* __restrict__ digest, int parts, int pf,
+                int ahead) {
     constexpr int kSlots = 1 << kSlotBits;
     extern __shared__ __align__(16) unsigned char smem[];
     int64_t* bkey = reinterpret_cast<int64_t*>(smem);                                   // [kChunk]
@@ -778,6 +779,22 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
     }
     const longlong2* brow = build + loff[part];
     const longlong2* prow = probe + roff[part];
+    // L2 bulk prefetches (M4D_JOIN_PF bits): 1 = this partition's probe rows
+    // (stream in while the table is built), 2 = its build rows, 4 = both sides
+    // of partition part + ahead (about one wave of CTAs later, any SM).
+    if (pf && threadIdx.x == 0) {
+        auto l2 = [](const longlong2* p, int64_t rows) {
+            const uint32_t b = static_cast<uint32_t>((rows < (1 << 20) ? rows : (1 << 20)) * 16);
+            if (b) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(b) : "memory");
+        };
+        if (pf & 1) l2(prow, roff[part + 1] - roff[part]);
+        if (pf & 2) l2(brow, loff[part + 1] - loff[part]);
+        if ((pf & 4) && part + ahead < parts) {
+            const int nx = part + ahead;
+            l2(build + loff[nx], loff[nx + 1] - loff[nx]);
+            l2(probe + roff[nx], roff[nx + 1] - roff[nx]);
+        }
+    }
     if (loff[part + 1] - loff[part] > INT32_MAX || roff[part + 1] - roff[part] > INT32_MAX)
         __trap();  // partitions are < 2^31 rows (32-bit offsets); fail loudly rather than mis-join
     const int bn = static_cast<int>(loff[part + 1] - loff[part]);
@@ -1233,6 +1250,24 @@ static bool join_small() {
 
 // Join grid: one CTA per partition, or (M4D_JOIN_PERSIST=1) one wave of
 // persistent CTAs that walk the partitions and prefetch the next one into L2.
+static int join_pf() {
+    static const int v = [] {
+        // default 3: 1.75 -> 1.58 ms per join at 1e8 rows/side (tools/km_join_pf_sweep.sh;
+        // the look-ahead bit 4 made it slower: 1.8-2.1 ms)
+        const char* e = getenv("M4D_JOIN_PF");
+        return e ? atoi(e) & 7 : 3;
+    }();
+    return v;
+}
+
+static int join_pf_ahead() {
+    static const int v = [] {
+        const char* e = getenv("M4D_JOIN_PF_AHEAD");
+        return e && atoi(e) > 0 ? atoi(e) : 148;
+    }();
+    return v;
+}
+
 static int join_grid(int parts, int per_sm) {
     static const bool persist = [] {
         const char* v = getenv("M4D_JOIN_PERSIST");
@@ -1310,12 +1345,14 @@ m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const in
             auto k = join_kernel<kSmallThreads, kSmallSlotBits, kSmallChunk, kSmallStage, 2>;
             M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
             k<<<join_grid(parts, 2), kSmallThreads, kSmallSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals,
-                                                                     out_rvals, capacity, result, result + 1, parts);
+                                                                     out_rvals, capacity, result, result + 1, parts, join_pf(),
+                                                                     join_pf_ahead());
         } else {
             auto k = join_kernel<kJoinThreads, kSlotBits, kChunk, kStage, 1>;
             M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kJoinSmem)));
             k<<<join_grid(parts, 1), kJoinThreads, kJoinSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals,
-                                                                   out_rvals, capacity, result, result + 1, parts);
+                                                                   out_rvals, capacity, result, result + 1, parts, join_pf(),
+                                                                     join_pf_ahead());
         }
     }
     M4D_CUDA_TRY(cudaGetLastError());

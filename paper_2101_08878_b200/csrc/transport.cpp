@@ -254,6 +254,7 @@ struct m4d_transport {
     size_t inflight_launches = 0;
     std::vector<PendingPull> pending_pulls;
     bool use_ce = false;                                        // M4D_PULL_ENGINE=ce: copy engine only
+    int pull_hold = 0;                                          // M4D_PULL_HOLD (see m4d_transport_progress)
     int pull_ctas = 296;                                        // pull-kernel grid cap (M4D_PULL_CTAS / setter)
     std::vector<cudaEvent_t> spare_events;
     std::vector<m4d_completion> done;
@@ -890,6 +891,7 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
         t->inflight.resize(t->pull_streams.size());
         if (const char* eng = getenv("M4D_PULL_ENGINE")) t->use_ce = strcmp(eng, "ce") == 0;
         if (const char* c = getenv("M4D_PULL_CTAS")) t->pull_ctas = atoi(c) > 0 ? atoi(c) : 296;
+        if (const char* c = getenv("M4D_PULL_HOLD")) t->pull_hold = atoi(c) > 0 ? atoi(c) : 0;
         if (e != cudaSuccess) {
             m4d_transport* raw = t.release();
             m4d_transport_close(raw);
@@ -1035,7 +1037,12 @@ int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
             drain_peer(t, q);
             flush_peer(t, q);
         }
-    flush_pulls(t);
+    // Pull hold (M4D_PULL_HOLD = h > 0): while h or more pull launches are still in
+    // flight, matched pulls wait (up to one full batch) so that a stream of
+    // rendezvous messages becomes fewer, larger multi-message launches.
+    if (t->pull_hold <= 0 || t->inflight_launches < static_cast<size_t>(t->pull_hold) ||
+        t->pending_pulls.size() >= static_cast<size_t>(m4d::pull_batch()))
+        flush_pulls(t);
     if (!t->reqs.empty()) check_liveness(t);
     int n = 0;
     const int avail = static_cast<int>(t->done.size());
