@@ -254,7 +254,6 @@ struct m4d_transport {
     size_t inflight_launches = 0;
     std::vector<PendingPull> pending_pulls;
     bool use_ce = false;                                        // M4D_PULL_ENGINE=ce: copy engine only
-    int pull_hold = 0;                                          // M4D_PULL_HOLD (see m4d_transport_progress)
     int pull_ctas = 296;                                        // pull-kernel grid cap (M4D_PULL_CTAS / setter)
     std::vector<cudaEvent_t> spare_events;
     std::vector<m4d_completion> done;
@@ -891,7 +890,6 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
         t->inflight.resize(t->pull_streams.size());
         if (const char* eng = getenv("M4D_PULL_ENGINE")) t->use_ce = strcmp(eng, "ce") == 0;
         if (const char* c = getenv("M4D_PULL_CTAS")) t->pull_ctas = atoi(c) > 0 ? atoi(c) : 296;
-        if (const char* c = getenv("M4D_PULL_HOLD")) t->pull_hold = atoi(c) > 0 ? atoi(c) : 0;
         if (e != cudaSuccess) {
             m4d_transport* raw = t.release();
             m4d_transport_close(raw);
@@ -1006,10 +1004,6 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
         u->second.pop_front();
         if (u->second.empty()) p.unexpected.erase(u);
         deliver_unexpected(t, peer, raw, msg);
-        // Pulls matched here are launched in batches: a window of posted
-        // receives becomes a few multi-message launches, not one launch per
-        // post (the next progress() issues whatever is left).
-        if (t->pending_pulls.size() >= static_cast<size_t>(m4d::pull_batch())) flush_pulls(t);
         flush_peer(t, peer);  // a truncation / empty-rendezvous FIN leaves now
     } else if (p.dead) {
         fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
@@ -1018,6 +1012,15 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
         raw->in_posted = true;
         p.posted[key].push_back(raw);
     }
+    // Pulls matched here (this receive, or earlier posted receives whose RTS
+    // drain_peer just took) are launched in batches: a window of posted
+    // receives becomes a few multi-message launches, not one launch per post.
+    // With no pull in flight they go at once, so the link starts while the
+    // caller is still posting instead of at its next progress() (measured
+    // osu_bw, 4 MiB messages, window 64: a fixed ~120 us per window before).
+    if (!t->pending_pulls.empty() &&
+        (t->pending_pulls.size() >= static_cast<size_t>(m4d::pull_batch()) || t->inflight_launches == 0))
+        flush_pulls(t);
     for (size_t i = before; i < t->done.size(); ++i)
         if (t->done[i].req_id == req_id) {
             *now = t->done[i];
@@ -1037,12 +1040,7 @@ int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
             drain_peer(t, q);
             flush_peer(t, q);
         }
-    // Pull hold (M4D_PULL_HOLD = h > 0): while h or more pull launches are still in
-    // flight, matched pulls wait (up to one full batch) so that a stream of
-    // rendezvous messages becomes fewer, larger multi-message launches.
-    if (t->pull_hold <= 0 || t->inflight_launches < static_cast<size_t>(t->pull_hold) ||
-        t->pending_pulls.size() >= static_cast<size_t>(m4d::pull_batch()))
-        flush_pulls(t);
+    flush_pulls(t);
     if (!t->reqs.empty()) check_liveness(t);
     int n = 0;
     const int avail = static_cast<int>(t->done.size());
