@@ -51,7 +51,40 @@ static PFN_pointerGetAttribute pointer_attribute_fn() {
     return fn;
 }
 
+typedef CUresult (*PFN_pointerGetAttributes)(unsigned, CUpointer_attribute*, void**, CUdeviceptr);
+static PFN_pointerGetAttributes pointer_attributes_fn() {
+    static PFN_pointerGetAttributes fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuPointerGetAttributes", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_pointerGetAttributes>(p);
+    });
+    return fn;
+}
+
 int alloc_info(const void* ptr, uint64_t* base, uint64_t* size, uint64_t* buffer_id) {
+    // One driver call for range start, range size and buffer id (every device
+    // send of the rendezvous path asks); anything it cannot answer takes the
+    // two-call path below, which also produces the errors.
+    if (PFN_pointerGetAttributes all = pointer_attributes_fn()) {
+        CUdeviceptr b = 0;
+        size_t sz = 0;
+        unsigned long long id = 0;
+        CUpointer_attribute which[3] = {CU_POINTER_ATTRIBUTE_RANGE_START_ADDR, CU_POINTER_ATTRIBUTE_RANGE_SIZE,
+                                        CU_POINTER_ATTRIBUTE_BUFFER_ID};
+        void* out[3] = {&b, &sz, &id};
+        if (all(3, which, out, reinterpret_cast<CUdeviceptr>(ptr)) == CUDA_SUCCESS && b && sz && id &&
+            reinterpret_cast<uint64_t>(ptr) >= static_cast<uint64_t>(b) &&
+            reinterpret_cast<uint64_t>(ptr) < static_cast<uint64_t>(b) + sz) {
+            *base = static_cast<uint64_t>(b);
+            *size = sz;
+            *buffer_id = id;
+            return M4D_OK;
+        }
+    }
     PFN_getAddressRange range = address_range_fn();
     PFN_pointerGetAttribute attr = pointer_attribute_fn();
     if (!range || !attr) return fail(M4D_ERR_CUDA, "driver entry points unavailable");
