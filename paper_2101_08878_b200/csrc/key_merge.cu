@@ -1327,7 +1327,15 @@ m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t*
     return M4D_OK;
 }
 
-int m4d_join_partition_rows(void) { return join_small() ? 6200 : 12400; }
+int m4d_join_partition_rows(void) {
+    // M4D_JOIN_PART_ROWS overrides the target rows per partition (the small join
+    // then builds a 12K-row partition in two chunks, re-reading probe rows from L2).
+    static const int rows = [] {
+        const char* v = getenv("M4D_JOIN_PART_ROWS");
+        return v && atoi(v) > 0 ? atoi(v) : 0;
+    }();
+    return rows ? rows : join_small() ? 6200 : 12400;
+}
 
 int m4d_partition_launches(int buckets) { return buckets > kSinglePassMax ? 9 : 6; }
 
