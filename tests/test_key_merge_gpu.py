@@ -260,3 +260,36 @@ def test_spec_application_oracle(world, fraction):
     assert got == oracle.key_merge_c(rows, world, fraction)
     if fraction == 0.0:
         assert got[0] == 0
+
+
+_VARIANT_SCRIPT = """
+import sys
+sys.path[:0] = [{root!r}, {tests!r}]
+from test_key_merge_gpu import run_world
+_, got = run_world({rows}, {world}, 0.3)
+print(list(got))
+"""
+
+
+@pytest.mark.parametrize("env", [
+    {"M4D_JOIN_PF": "0"},
+    {"M4D_JOIN_PF": "7", "M4D_JOIN_PF_AHEAD": "3"},
+    {"M4D_JOIN": "small"},
+    {"M4D_JOIN": "small", "M4D_JOIN_PART_ROWS": "12400"},  # two build chunks per partition
+    {"M4D_JOIN_PERSIST": "1", "M4D_JOIN_PART_ROWS": "500"},  # more partitions than one wave
+])
+def test_tuning_knobs_keep_the_digest(env):
+    """Every join knob (read once per process, so each runs in its own interpreter) gives
+    the oracle's digest: the knobs change the schedule, never the result."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    rows = 400_000
+    code = _VARIANT_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), rows=rows, world=1)
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, cwd=root, capture_output=True,
+                         text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    got = tuple(int(x) for x in out.stdout.strip().splitlines()[-1].strip("[]").split(","))
+    assert got == tuple(oracle.key_merge_c(rows, 1, 0.3))
