@@ -199,7 +199,24 @@ def recorded_traffic(key: str):
         return None
 
 
+def host_info() -> dict:
+    """The host the CPU baseline ran on (core counts, CPU model, RAM)."""
+    info = {"cpu_count": os.cpu_count(), "affinity": len(os.sched_getaffinity(0))}
+    try:
+        with open("/proc/cpuinfo") as fh:
+            info["cpu_model"] = next((ln.split(":", 1)[1].strip() for ln in fh if ln.startswith("model name")), None)
+        with open("/proc/meminfo") as fh:
+            kb = next((int(ln.split()[1]) for ln in fh if ln.startswith("MemTotal")), 0)
+        info["mem_total_gb"] = round(kb / 2**20, 1)
+    except (OSError, ValueError):
+        pass
+    return info
+
+
 def emit(line: dict) -> None:
+    cpu = line.get("cpu_baseline")
+    if isinstance(cpu, dict) and "host" not in cpu:
+        cpu["host"] = host_info()
     print(json.dumps(line), flush=True)
 
 
