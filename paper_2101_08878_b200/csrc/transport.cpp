@@ -219,7 +219,23 @@ struct PendingPull {
     uint64_t len;
 };
 
-constexpr uint64_t kSmallPull = 64 * 1024;  // below this a copy-engine memcpy is cheaper than a launch
+// Largest lone pull that takes the copy engine (M4D_LONE_CE_MAX, bytes; 0 = never).
+static uint64_t lone_ce_max() {
+    static const uint64_t v = [] {
+        const char* e = getenv("M4D_LONE_CE_MAX");
+        return e ? static_cast<uint64_t>(atoll(e)) : uint64_t(1) << 20;
+    }();
+    return v;
+}
+
+// Below this a copy-engine memcpy is cheaper than a launch (M4D_SMALL_PULL overrides, bytes).
+static uint64_t small_pull() {
+    static const uint64_t v = [] {
+        const char* e = getenv("M4D_SMALL_PULL");
+        return e ? static_cast<uint64_t>(atoll(e)) : uint64_t(64 * 1024);
+    }();
+    return v;
+}
 
 inline uint64_t ckey(uint32_t channel, uint32_t tag) { return (static_cast<uint64_t>(channel) << 32) | tag; }
 
@@ -409,7 +425,15 @@ void flush_pulls(m4d_transport* t) {
         cudaError_t e = take_event(&ev);
         size_t j = i + 1;
         // The SM kernel needs a device destination; host buffers use the copy engine.
-        auto via_kernel = [&](const PendingPull& pp) { return !t->use_ce && pp.len >= kSmallPull && pp.recv->device; };
+        // A lone pull (nothing else pending or in flight: a ping-pong) of up to
+        // 1 MiB rides the copy engine, whose latency is lower than a launch's
+        // (osu_latency 64 KiB / 256 KiB / 1 MiB: 20.5 / 21.5 / 22.7 us via the
+        // kernel, 14.8 / 14.8 / 16.4 us via the copy engine); pulls that arrive
+        // together keep the batched kernel, which carries more per window.
+        const bool lone = v.size() == 1 && t->inflight_launches == 0;
+        auto via_kernel = [&](const PendingPull& pp) {
+            return !t->use_ce && pp.len >= small_pull() && pp.recv->device && !(lone && pp.len <= lone_ce_max());
+        };
         if (e == cudaSuccess && !via_kernel(v[i])) {
             e = cudaMemcpyAsync(v[i].recv->ptr, v[i].src, v[i].len, cudaMemcpyDefault, s);
         } else if (e == cudaSuccess) {
