@@ -19,6 +19,7 @@ int alloc_info(const void* ptr, uint64_t* base, uint64_t* size, uint64_t* buffer
 // Rendezvous pulls launched as one SM copy kernel (pull.cu).
 constexpr int kMaxPull = 32;  // array capacity; messages per launch = pull_batch() (M4D_PULL_BATCH, default 8)
 int pull_batch();
+uint64_t pull_batch_bytes();  // a launch also closes at this many bytes (M4D_PULL_BATCH_BYTES)
 struct PullDesc {
     const uint8_t* src;
     uint8_t* dst;

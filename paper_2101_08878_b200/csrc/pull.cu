@@ -59,6 +59,18 @@ int pull_batch() {
     return b;
 }
 
+// A launch also closes once it holds this many bytes (M4D_PULL_BATCH_BYTES,
+// default 16 MiB): 4 x 4 MiB per launch beat 8 x 4 MiB (osu_bw 705 vs 684 GB/s,
+// profiles/r1_p2p_batch_sweep.txt) while 1 MiB messages keep 8 per launch
+// (a count cap of 4 cut them from 317 to 240 GB/s).
+uint64_t pull_batch_bytes() {
+    static const uint64_t b = [] {
+        const char* v = getenv("M4D_PULL_BATCH_BYTES");
+        return v && atoll(v) > 0 ? static_cast<uint64_t>(atoll(v)) : uint64_t(16) << 20;
+    }();
+    return b;
+}
+
 static int pull_ilp() {
     static const int k = [] {
         const char* v = getenv("M4D_PULL_ILP");

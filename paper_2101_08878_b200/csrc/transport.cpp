@@ -439,8 +439,13 @@ void flush_pulls(m4d_transport* t) {
         } else if (e == cudaSuccess) {
             m4d::PullBatch batch;
             batch.n = 0;
-            for (j = i; j < v.size() && batch.n < m4d::pull_batch() && via_kernel(v[j]); ++j)
+            uint64_t bytes = 0;
+            for (j = i; j < v.size() && batch.n < m4d::pull_batch() && via_kernel(v[j]) &&
+                        (batch.n == 0 || bytes + v[j].len <= m4d::pull_batch_bytes());
+                 ++j) {
                 batch.d[batch.n++] = m4d::PullDesc{v[j].src, v[j].recv->ptr, v[j].len};
+                bytes += v[j].len;
+            }
             if (m4d::launch_pull_batch(batch, s, t->pull_ctas) != M4D_OK) e = cudaErrorLaunchFailure;
             else t->stats.pull_kernel_launches++;
         }
@@ -1042,9 +1047,13 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
     // With no pull in flight they go at once, so the link starts while the
     // caller is still posting instead of at its next progress() (measured
     // osu_bw, 4 MiB messages, window 64: a fixed ~120 us per window before).
-    if (!t->pending_pulls.empty() &&
-        (t->pending_pulls.size() >= static_cast<size_t>(m4d::pull_batch()) || t->inflight_launches == 0))
-        flush_pulls(t);
+    if (!t->pending_pulls.empty()) {
+        uint64_t bytes = 0;
+        for (const PendingPull& pp : t->pending_pulls) bytes += pp.len;
+        if (t->pending_pulls.size() >= static_cast<size_t>(m4d::pull_batch()) || bytes >= m4d::pull_batch_bytes() ||
+            t->inflight_launches == 0)
+            flush_pulls(t);
+    }
     for (size_t i = before; i < t->done.size(); ++i)
         if (t->done[i].req_id == req_id) {
             *now = t->done[i];

@@ -1,4 +1,4 @@
-"""osu_bw (window 64, distinct buffers) at 4 / 8 / 16 MiB under the current M4D_PULL_HOLD_MB (2 ranks, torchrun)."""
+"""osu_bw (window 64, distinct buffers) at 4 / 8 / 16 MiB under the current M4D_PULL_BATCH (2 ranks, torchrun)."""
 import os
 import sys
 
@@ -17,4 +17,4 @@ for n in (4 << 20, 8 << 20, 16 << 20):
 launches = t.native_stats()["pull_kernel_launches"]
 t.close()
 if rank == 0:
-    print(f"hold={os.environ.get('M4D_PULL_HOLD_MB', '0')} launches(rank0)={launches} | " + " | ".join(out), flush=True)
+    print(f"batch={os.environ.get('M4D_PULL_BATCH', '8')} launches(rank0)={launches} | " + " | ".join(out), flush=True)
