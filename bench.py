@@ -182,12 +182,15 @@ class Dist:
 
 
 def open_transport(dist: "Dist", device: int):
-    """This rank's nvlink transport (session derived from the torchrun rendezvous)."""
+    """This rank's nvlink transport (session derived from the torchrun rendezvous), opened
+    once per process and shared by every workload of the run (closed by main)."""
     from paper_2101_08878_b200.transport import TransportConfig, transport_init
 
-    t = transport_init(dist.world, dist.rank, TransportConfig(kind="nvlink", device=device, connect_timeout=60))
-    t.wait_ready()
-    return t
+    if getattr(dist, "transport", None) is None:
+        t = transport_init(dist.world, dist.rank, TransportConfig(kind="nvlink", device=device, connect_timeout=60))
+        t.wait_ready()
+        dist.transport = t
+    return dist.transport
 
 
 def recorded_traffic(key: str):
@@ -328,28 +331,42 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
     roof["t_roof_ms"] = max(t_hbm, t_nvl) * 1e3
 
     # -- e2e: x from pinned host memory through the public harness API --
+    # Two different arrays (seed, seed + 1) alternate between steps, each uploaded with
+    # TransposeSum.load_x (H2D + the cross-rank input-ready fence) and checked against its
+    # own resident checksum, so a kernel that read a peer's pool before the upload landed
+    # would fail the run.
     e2e = None
     if not args.skip_e2e:
         pool = len(ts.owned) * ts.block_bytes
-        host = native.PinnedHostBuffer(pool)
-        native.memcpy(host.ptr, ts.x.ptr, pool, stream)  # snapshot x to host once (untimed)
-        stream.synchronize()
-        e2e_steps = max(1, min(args.steps, 3))
+        hosts, want = [], []
+        for seed in (ts.seed, ts.seed + 1):
+            ts.seed = seed
+            ts.generate()
+            h = native.PinnedHostBuffer(pool)
+            native.memcpy(h.ptr, ts.x.ptr, pool, stream)  # snapshot (untimed)
+            stream.synchronize()
+            hosts.append(h)
+            want.append(ts.step().checksum)  # resident checksum of this array (untimed)
+        if want[0] != checksum:
+            raise RuntimeError("regenerated x does not reproduce the timed checksum")
+        e2e_steps = max(2, min(args.steps, 4))
         dist.barrier()
         t0 = time.perf_counter()
         e0.record(stream)
-        for _ in range(e2e_steps):
-            native.memcpy(ts.x.ptr, host.ptr, pool, stream)
+        for k in range(e2e_steps):
+            ts.load_x(hosts[k % 2].ptr)
             r = ts.step()
+            if r.checksum != want[k % 2]:
+                raise RuntimeError(f"e2e step {k}: checksum {r.checksum!r} != {want[k % 2]!r} (input fence?)")
         e1.record(stream)
         e1.synchronize()
         e2e_ms = max(e0.elapsed_ms(e1), (time.perf_counter() - t0) * 1e3) / e2e_steps
         e2e_ms = dist.max(e2e_ms)
-        if r.checksum != checksum:
-            raise RuntimeError("e2e checksum differs from the resident-input checksum")
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(dist.sum(pool)),
-               "d2h_bytes_per_step": int(dist.sum(len(ts.owned) * 8)), "steps": e2e_steps}
-        host.free()
+               "d2h_bytes_per_step": int(dist.sum(len(ts.owned) * 8)), "steps": e2e_steps,
+               "inputs": "two arrays alternated between steps (seed, seed + 1), each checked"}
+        for h in hosts:
+            h.free()
 
     # -- parity (outside timing): sampled block sums vs the oracle --
     parity = None
@@ -371,6 +388,8 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
                              f"extrapolated to the full {n}^2 array"}
     launches_per_step = native.lib().m4d_ts_launches_per_run(ts._plan)
     ts.close()
+    ts.x.free()  # 25.6 GB of pools at N=1: give the HBM back before the next workload
+    ts.y.free()
     if dist.rank != 0:
         return None
     launches = args.steps * launches_per_step
@@ -404,29 +423,32 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
 # -- key_merge ------------------------------------------------------------------------------------
 
 
-def km_cpu_sample(rows: int, target_rows: int, min_seconds: float = 10.0, fraction: float = 0.3) -> dict:
+def km_cpu_sample(rows: int, min_seconds: float = 10.0, fraction: float = 0.3) -> dict:
     """Oracle CPU join (C, all host threads: radix partition + per-partition hash joins) of
-    `rows` resident rows per side (generated outside the timed region, as the GPU's inputs
-    are), repeated to >= min_seconds, scaled to `target_rows` rows per side."""
+    the FULL global inputs (`rows` per side, generated outside the timed region, as the
+    GPU's inputs are): the digest pins the GPU result at full size; the join is repeated
+    to >= min_seconds for the timing (min_seconds 0: one run)."""
     import oracle
 
     threads = len(os.sched_getaffinity(0))
     band = oracle.merge_band(rows, fraction)
     lk, lv = oracle.gen_side_c(0, rows, rows, oracle.SEED_LEFT, 0)
     rk, rv = oracle.gen_side_c(0, rows, rows, oracle.SEED_RIGHT, band)
-    want = oracle.key_merge_c(rows, 1, fraction) if rows <= 2_000_000 else None
     done, t0 = 0, time.perf_counter()
+    digest = None
     while True:
         got = oracle.join_mt_c(lk, lv, rk, rv, threads)
+        if digest is not None and got != digest:
+            raise RuntimeError("multithreaded CPU join is not deterministic")
+        digest = got
         done += 1
         dt = time.perf_counter() - t0
         if dt >= min_seconds:
             break
-    if want is not None and got != want:
-        raise RuntimeError("multithreaded CPU join disagrees with the oracle")
-    per = dt / done
-    return {"seconds": dt, "runs": done, "rows": rows, "threads": threads, "rows_out": got[0],
-            "full_ms": per * target_rows / rows * 1e3}
+    if rows <= 2_000_000 and digest != oracle.key_merge_c(rows, 1, fraction):
+        raise RuntimeError("multithreaded CPU join disagrees with the scalar oracle")
+    return {"seconds": dt, "runs": done, "rows": rows, "threads": threads, "digest": tuple(digest),
+            "ms": dt / done * 1e3}
 
 
 def digest_rows(km) -> int:
@@ -529,25 +551,22 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
         e2e = {"value": e2e_ms, "unit": "ms", "h2d_bytes_per_step": int(dist.sum(4 * nbytes)),
                "d2h_bytes_per_step": int(dist.sum(32 + 8 * (2 * dist.world + 2)))}
 
+    km.close()
+    dist.barrier()  # every rank unmapped its peers' receive buffers before any rank frees its own
     cpu, parity = None, None
     if dist.rank == 0:
-        import oracle
-
-        sample_rows = min(args.rows, 2_000_000)
-        small = KeyMerge(sample_rows, args.fraction, device=device)
-        small.generate()
-        got_small = TaskLoop(MonotonicClock()).run_until_complete(small.run())
-        want_small = oracle.key_merge_c(sample_rows, 1, args.fraction)
-        parity = {"sample_rows_per_side": sample_rows, "digest_equal": got_small == want_small,
-                  "full_rows_out": digest[0], "expected_fraction": args.fraction,
-                  "observed_fraction": digest[0] / max(1, args.rows * dist.world)}
+        # parity at FULL size: the oracle's digest of the same global inputs
+        target = args.rows * dist.world
+        c = km_cpu_sample(target, 0.0 if args.skip_cpu else min(10.0, args.cpu_seconds), args.fraction)
+        parity = {"rows_per_side": target, "digest_equal": tuple(digest) == c["digest"],
+                  "oracle_digest": list(c["digest"]), "rows_out": digest[0], "expected_fraction": args.fraction,
+                  "observed_fraction": digest[0] / max(1, target), "row_conservation": dist.world == 1 or km.conserved}
+        if not parity["digest_equal"]:
+            raise RuntimeError(f"key_merge digest {digest} differs from the oracle's {c['digest']}")
         if not args.skip_cpu:
-            target = args.rows * dist.world
-            c = km_cpu_sample(min(target, 100_000_000), target, min(10.0, args.cpu_seconds), args.fraction)
-            cpu = {"value": c["full_ms"], "unit": "ms", "cores": c["threads"], "kind": "port",
+            cpu = {"value": c["ms"], "unit": "ms", "cores": c["threads"], "kind": "port",
                    "sample": f"oracle C join ({c['threads']} threads, radix partition + per-partition hash joins) "
-                             f"of {c['rows']} resident rows/side x {c['runs']} runs in {c['seconds']:.1f} s"
-                             + ("" if c["rows"] == target else f", scaled linearly to {target} rows/side")}
+                             f"of the full {target} resident rows/side x {c['runs']} runs in {c['seconds']:.1f} s"}
     if dist.rank != 0:
         return None
     return {
@@ -588,7 +607,6 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
     host_pp = p2p.pingpong(t, 1 - dist.rank, 1, 2000, False)
     # SM pull kernels this rank launched (device frames >= 64 KiB; smaller ones ride the copy engine)
     launches = t.native_stats()["pull_kernel_launches"]
-    t.close()
     cpu = None
     if dist.rank == 0 and not args.skip_cpu:
         sample = SimpleNamespace(**{**vars(args), "max_size": 4 << 20})
@@ -653,7 +671,6 @@ def bench_storm(args, dist: Dist, peaks: dict) -> dict | None:
     r = storm.run_worker(storm.namespace_of("paper_2101_08878_b200"), t, dist.allgather_bytes,
                          conns=args.conns, total=args.frames, rounds=args.steps, warmup=args.warmup)
     clocks = sampler.stop()
-    t.close()
     if dist.rank != 0:
         return None
     line = storm_line(r, args, dist.world)
@@ -835,13 +852,12 @@ def reference_transpose_sum(args) -> dict:
 def reference_key_merge(args) -> dict:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     target = args.rows * world
-    rows = min(target, 100_000_000)
-    per = [km_cpu_sample(rows, target, max(2.0, args.cpu_seconds / max(1, args.steps)), args.fraction)
+    per = [km_cpu_sample(target, max(2.0, args.cpu_seconds / max(1, args.steps)), args.fraction)
            for _ in range(args.steps)]
-    value = statistics.mean(p["full_ms"] for p in per)
+    value = statistics.mean(p["ms"] for p in per)
     threads = per[0]["threads"]
-    sample = (f"oracle C join ({threads} threads, radix partition + per-partition hash joins) of {rows} resident "
-              f"rows/side per step" + ("" if rows == target else f", scaled linearly to {target} rows/side"))
+    sample = (f"oracle C join ({threads} threads, radix partition + per-partition hash joins) of the full "
+              f"{target} resident rows/side per step")
     return {
         "impl": "reference",
         "metric": f"merge wall time ({args.rows} rows/side/GPU, int64 key, fraction {args.fraction})",
@@ -851,6 +867,7 @@ def reference_key_merge(args) -> dict:
         "config": {"workload": "key_merge", "rows_per_side_per_gpu": args.rows, "fraction": args.fraction},
         "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "digest": list(per[0]["digest"]),
     }
 
 
@@ -879,6 +896,7 @@ def main(argv=None) -> int:
     ap.add_argument("--cpu-seconds", type=float, default=30.0, help="CPU-baseline time budget (whole run)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--no-merge", action="store_true", help="default run without the key_merge sub-record")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture (reported as roofline.traffic)")
     args = ap.parse_args(argv)
@@ -892,7 +910,12 @@ def main(argv=None) -> int:
         if int(os.environ.get("RANK", "0")) != 0:
             return 0
         if args.workload == "transpose_sum":
-            emit(reference_transpose_sum(args))
+            line = reference_transpose_sum(args)
+            if not args.no_merge:
+                km = reference_key_merge(args)
+                line["key_merge"] = {k: km[k] for k in ("metric", "value", "unit", "ms_per_step", "config",
+                                                        "cpu_baseline", "e2e", "digest")}
+            emit(line)
         elif args.workload == "key_merge":
             emit(reference_key_merge(args))
         elif args.workload == "storm":
@@ -907,7 +930,19 @@ def main(argv=None) -> int:
               "storm": bench_storm}[args.workload]
     try:
         line = runner(args, dist, peaks)
+        # The default run carries the other half of BASELINE.json's metric as a sub-record:
+        # the merge (config 4) at the same N, with its own timed region, roofline, e2e,
+        # CPU baseline and full-size parity.
+        if args.workload == "transpose_sum" and not args.no_merge:
+            km = bench_key_merge(args, dist, peaks)
+            if line is not None and km is not None:
+                line["key_merge"] = {k: km[k] for k in ("metric", "value", "unit", "ms_per_step", "higher_is_better",
+                                                        "scaling", "dtype", "config", "gpu_launches", "roofline",
+                                                        "e2e", "cpu_baseline", "parity", "clocks", "wall_ms_per_step")}
     finally:
+        if getattr(dist, "transport", None) is not None:
+            dist.barrier()
+            dist.transport.close()
         dist.close()
     if line is not None:
         if dist.shared:

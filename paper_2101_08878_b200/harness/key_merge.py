@@ -412,11 +412,20 @@ class KeyMerge:
         mine = await self.run()
         if self.world == 1:
             return mine
-        parts = await allgather(self.transport, struct.pack("<3Q", *mine), tag=EXCHANGE_TAG + 1)
+        parts = await allgather(self.transport, struct.pack("<5Q", *mine, *self.received), tag=EXCHANGE_TAG + 1)
         total = [0, 0, 0]
+        received = [0, 0]
         for blob in parts:
-            for k, v in enumerate(struct.unpack("<3Q", blob)):
-                total[k] = (total[k] + v) & _MASK64
+            vals = struct.unpack("<5Q", blob)
+            for k in range(3):
+                total[k] = (total[k] + vals[k]) & _MASK64
+            received[0] += vals[3]
+            received[1] += vals[4]
+        # row conservation: every generated row reached exactly one owner
+        if received != [self.total, self.total]:
+            raise CommShimError(f"row conservation violated: owners received {received} rows per side, "
+                                f"{self.total} generated")
+        self.conserved = True
         return tuple(total)
 
     def output_rows(self, limit: int | None = None):

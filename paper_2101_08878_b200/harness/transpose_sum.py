@@ -196,6 +196,21 @@ class TransposeSum:
         self.launch()
         return self.combine(self.read_block_sums())
 
+    def load_x(self, host_ptr: int, stream: native.Stream | None = None) -> None:
+        """Upload this rank's x pool (block-major, the layout of ``self.x``) from host
+        memory for the next step, then fence: peers read partner tiles straight out of
+        this pool over NVLink, so no rank may launch before every rank's upload has
+        landed.  (The reverse hazard -- overwriting a pool a peer's previous kernel is
+        still reading -- is excluded by step(): its block-sum exchange completes only
+        after every rank's kernel finished.)"""
+        s = stream or self.stream
+        native.memcpy(self.x.ptr, host_ptr, len(self.owned) * self.block_bytes, s)
+        if self.world > 1:
+            s.synchronize()
+            self.exchange(b"\x01")  # input-ready barrier
+        elif s is not self.stream:
+            s.synchronize()
+
     def read_y_block(self, g: int) -> bytes:
         native.set_device(self.device)
         return native.to_host(self.y_ptr(g), self.block_bytes, self.stream)

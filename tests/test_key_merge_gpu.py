@@ -107,6 +107,19 @@ def test_large_config_properties():
     assert ranks[0].received == [rows, rows]
 
 
+def test_full_scale_digest_against_the_oracle():
+    """5e7 rows/side on one GPU: the digest equals the multithreaded C oracle's at full
+    size (the bench checks 1e8 the same way)."""
+    import os
+
+    rows = 50_000_000
+    _, got = run_world(rows, 1, 0.3)
+    band = oracle.merge_band(rows, 0.3)
+    lk, lv = oracle.gen_side_c(0, rows, rows, oracle.SEED_LEFT, 0)
+    rk, rv = oracle.gen_side_c(0, rows, rows, oracle.SEED_RIGHT, band)
+    assert got == oracle.join_mt_c(lk, lv, rk, rv, len(os.sched_getaffinity(0)))
+
+
 @pytest.mark.parametrize("buckets", [32768, 65536])
 def test_partition_bounds_under_extreme_skew(buckets):
     """One key fills whole CTAs (>= 65536 equal rows each): the 16-bit shared histogram
