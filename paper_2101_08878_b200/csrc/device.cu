@@ -119,6 +119,15 @@ size_t m4d_last_error(char* buf, size_t n) {
 
 int m4d_version(void) { return (1 << 16) | 0; }
 
+m4d_status m4d_mem_get_info(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
+    M4D_CUDA_TRY(cudaSetDevice(device));
+    size_t f = 0, t = 0;
+    M4D_CUDA_TRY(cudaMemGetInfo(&f, &t));
+    *free_bytes = f;
+    *total_bytes = t;
+    return M4D_OK;
+}
+
 int m4d_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) {
@@ -202,6 +211,7 @@ m4d_status m4d_malloc(int device, size_t nbytes, void** ptr_out) {
 }
 
 m4d_status m4d_free(void* ptr) {
+    if (m4d::release_exported(ptr)) return M4D_OK;  // freed once the importers unmapped it
     M4D_CUDA_TRY(cudaFree(ptr));
     return M4D_OK;
 }

@@ -31,6 +31,10 @@ struct PullBatch {
 };
 int launch_pull_batch(const PullBatch& batch, cudaStream_t stream, int max_ctas);
 
+// m4d_free hook: true when a transport took over the free of an allocation it exported
+// (deferred until every peer that mapped it closed the mapping; transport.cpp).
+bool release_exported(void* ptr);
+
 inline int cuda_fail(cudaError_t err, const char* what) {
     return fail(M4D_ERR_CUDA, "%s: %s (%s)", what, cudaGetErrorName(err), cudaGetErrorString(err));
 }

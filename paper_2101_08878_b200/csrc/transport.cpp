@@ -38,6 +38,7 @@
 #include <deque>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -79,7 +80,7 @@ struct SegHeader {
     uint64_t ring_stride;
 };
 
-enum Kind : uint16_t { kPad = 0, kMsg = 1, kCont = 2, kRts = 3, kFin = 4, kBye = 5 };
+enum Kind : uint16_t { kPad = 0, kMsg = 1, kCont = 2, kRts = 3, kFin = 4, kBye = 5, kUnmap = 6, kUnmapAck = 7 };
 
 struct RecHdr {
     uint32_t bytes;  // whole record, 8-byte multiple
@@ -121,6 +122,20 @@ struct FinRec {
     uint64_t send_id;
     uint64_t bytes;
 };
+
+// Allocation lifetime across processes: a sender about to free an allocation it
+// exported asks every peer that saw it to close the mapping (kUnmap: exporter
+// pid, buffer id, exporter base); the peer closes it once no pull reads it and
+// answers kUnmapAck(base); the allocation is cudaFree'd when the last answer
+// arrives (cuda_runtime_api.h: an exporter must not free before importers close).
+struct UnmapRec {
+    RecHdr h;
+    int32_t pid;
+    uint32_t reserved;
+    uint64_t buffer_id;
+    uint64_t base;  // exporter-process address, echoed in the ack
+};
+static_assert(sizeof(UnmapRec) == sizeof(FinRec), "control records share the fin queue");
 
 inline uint64_t align8(uint64_t n) { return (n + 7) & ~7ull; }
 
@@ -196,11 +211,19 @@ struct Inbound {
     uint64_t total = 0, got = 0;
 };
 
+struct MapKey {
+    int pid = 0;
+    uint64_t buffer_id = 0;
+    bool mapped = false;  // the source is a CUDA-IPC mapping (not a same-process pointer)
+    bool operator<(const MapKey& o) const { return pid != o.pid ? pid < o.pid : buffer_id < o.buffer_id; }
+};
+
 struct Copy {
     Req* recv;
     int peer;
     uint64_t send_id;
     uint64_t bytes;
+    MapKey src;
 };
 
 // One pull launch (or copy-engine copy) and the messages its event completes.
@@ -217,6 +240,16 @@ struct PendingPull {
     uint64_t send_id;
     const uint8_t* src;
     uint64_t len;
+    MapKey key;
+};
+
+// A peer allocation mapped through CUDA IPC.
+struct PeerMap {
+    void* base = nullptr;
+    int inflight = 0;          // pulls reading it right now
+    bool unmap_requested = false;
+    int unmap_peer = -1;       // who asked (gets the ack)
+    uint64_t exporter_base = 0;
 };
 
 // Largest lone pull that takes the copy engine (M4D_LONE_CE_MAX, bytes; 0 = never).
@@ -248,7 +281,7 @@ struct Peer {
     bool dead = false;
     bool said_bye = false;
     std::deque<Req*> outq;     // sends not yet fully in the ring, post order
-    std::deque<FinRec> fins;   // control records waiting for ring space
+    std::deque<FinRec> fins;   // control records (fin, unmap, unmap ack) waiting for ring space
     std::unordered_map<uint64_t, std::deque<Req*>> posted;
     std::unordered_map<uint64_t, std::deque<std::shared_ptr<Unexpected>>> unexpected;
     Inbound inbound;
@@ -273,7 +306,7 @@ struct m4d_transport {
     int pull_ctas = 296;                                        // pull-kernel grid cap (M4D_PULL_CTAS / setter)
     std::vector<cudaEvent_t> spare_events;
     std::vector<m4d_completion> done;
-    std::map<std::pair<int, uint64_t>, void*> ipc_maps;         // (pid, buffer id) -> mapped base
+    std::map<MapKey, PeerMap> ipc_maps;                         // (pid, buffer id) -> mapping
     std::unordered_map<uint64_t, std::pair<uint64_t, std::array<uint8_t, 64>>> exports;  // buffer id -> (base, handle)
     cudaStream_t stream = nullptr;                             // (kept: first of the pull streams)
     std::vector<cudaStream_t> pull_streams;                     // copies round-robin over these
@@ -341,12 +374,94 @@ void queue_fin(m4d_transport* t, int peer, uint64_t send_id, int status, uint64_
     t->peers[peer].fins.push_back(f);
 }
 
-void* map_peer_allocation(m4d_transport* t, const RtsRec& rts, int* status) {
+void queue_unmap(m4d_transport* t, int peer, int kind, int32_t pid, uint64_t buffer_id, uint64_t base) {
+    UnmapRec u{};
+    u.h.bytes = sizeof(UnmapRec);
+    u.h.kind = static_cast<uint16_t>(kind);
+    u.pid = pid;
+    u.buffer_id = buffer_id;
+    u.base = base;
+    FinRec f;
+    memcpy(&f, &u, sizeof f);
+    t->peers[peer].fins.push_back(f);
+}
+
+// -- process-wide registry of exported allocations (sender side) --------------------------
+
+struct ExportHold {
+    m4d_transport* t;
+    int peer;
+};
+struct ExportEntry {
+    uint64_t buffer_id = 0;
+    std::vector<ExportHold> holds;  // (transport, peer) pairs that were sent an RTS for it
+    int acks_pending = 0;           // > 0: the owner freed it; cudaFree when the last ack arrives
+};
+std::mutex g_exp_mu;
+std::unordered_map<uint64_t, ExportEntry> g_exports;  // allocation base -> entry
+
+void note_export(m4d_transport* t, int peer, uint64_t base, uint64_t buffer_id) {
+    std::lock_guard<std::mutex> lk(g_exp_mu);
+    ExportEntry& e = g_exports[base];
+    if (e.buffer_id != buffer_id) e = ExportEntry{buffer_id, {}, 0};  // a new allocation at a reused address
+    for (const ExportHold& h : e.holds)
+        if (h.t == t && h.peer == peer) return;
+    e.holds.push_back(ExportHold{t, peer});
+}
+
+// One awaited answer for `base` will never come (ack arrived, peer gone, transport closed).
+void settle_export(uint64_t base) {
+    std::lock_guard<std::mutex> lk(g_exp_mu);
+    auto it = g_exports.find(base);
+    if (it == g_exports.end() || it->second.acks_pending <= 0) return;
+    if (--it->second.acks_pending == 0) {
+        cudaFree(reinterpret_cast<void*>(base));
+        g_exports.erase(it);
+    }
+}
+
+// Drops `t`'s holds (peer == -1: every peer); holds whose answer was awaited settle.
+void drop_holds(m4d_transport* t, int peer) {
+    std::vector<uint64_t> settle;
+    {
+        std::lock_guard<std::mutex> lk(g_exp_mu);
+        for (auto it = g_exports.begin(); it != g_exports.end();) {
+            ExportEntry& e = it->second;
+            for (size_t i = 0; i < e.holds.size();) {
+                if (e.holds[i].t == t && (peer < 0 || e.holds[i].peer == peer)) {
+                    if (e.acks_pending > 0) settle.push_back(it->first);
+                    e.holds.erase(e.holds.begin() + static_cast<long>(i));
+                } else {
+                    ++i;
+                }
+            }
+            if (e.holds.empty() && e.acks_pending == 0) it = g_exports.erase(it);
+            else ++it;
+        }
+    }
+    for (uint64_t b : settle) settle_export(b);
+}
+
+// Receiver: close a mapping nobody reads any more and answer the exporter.
+void close_mapping(m4d_transport* t, std::map<MapKey, PeerMap>::iterator it) {
+    cudaIpcCloseMemHandle(it->second.base);
+    if (it->second.unmap_requested && it->second.unmap_peer >= 0 && !t->peers[it->second.unmap_peer].dead)
+        queue_unmap(t, it->second.unmap_peer, kUnmapAck, 0, it->first.buffer_id, it->second.exporter_base);
+    t->ipc_maps.erase(it);
+}
+
+void* map_peer_allocation(m4d_transport* t, const RtsRec& rts, MapKey* key, int* status) {
     *status = M4D_OK;
+    key->pid = rts.pid;
+    key->buffer_id = rts.buffer_id;
+    key->mapped = false;
     if (rts.pid == static_cast<int32_t>(getpid())) return reinterpret_cast<void*>(rts.src_ptr);
-    const std::pair<int, uint64_t> key(rts.pid, rts.buffer_id);
-    auto it = t->ipc_maps.find(key);
-    if (it != t->ipc_maps.end()) return static_cast<uint8_t*>(it->second) + rts.offset;
+    key->mapped = true;
+    auto it = t->ipc_maps.find(*key);
+    if (it != t->ipc_maps.end()) {
+        it->second.inflight++;
+        return static_cast<uint8_t*>(it->second.base) + rts.offset;
+    }
     cudaIpcMemHandle_t h;
     memcpy(&h, rts.handle, 64);
     void* base = nullptr;
@@ -362,8 +477,18 @@ void* map_peer_allocation(m4d_transport* t, const RtsRec& rts, int* status) {
         *status = m4d::cuda_fail(e, "cudaIpcOpenMemHandle (rendezvous source)");
         return nullptr;
     }
-    t->ipc_maps[key] = base;
+    PeerMap& m = t->ipc_maps[*key];
+    m.base = base;
+    m.inflight = 1;
     return static_cast<uint8_t*>(base) + rts.offset;
+}
+
+// A pull from a mapped source finished: close the mapping if its exporter asked.
+void pull_done(m4d_transport* t, const MapKey& key) {
+    if (!key.mapped) return;
+    auto it = t->ipc_maps.find(key);
+    if (it == t->ipc_maps.end()) return;
+    if (--it->second.inflight <= 0 && it->second.unmap_requested) close_mapping(t, it);
 }
 
 // Matched rendezvous: pull the peer's bytes device-to-device (or D2H for a
@@ -382,13 +507,14 @@ void start_pull(m4d_transport* t, int peer, Req* r, const RtsRec& rts) {
         return;
     }
     int st;
-    void* src = map_peer_allocation(t, rts, &st);
+    MapKey key;
+    void* src = map_peer_allocation(t, rts, &key, &st);
     if (st != M4D_OK) {
         queue_fin(t, peer, rts.send_id, M4D_ERR_TRANSFER, 0);
         complete(t, r, M4D_ERR_CUDA, 0);
         return;
     }
-    t->pending_pulls.push_back(PendingPull{r, peer, rts.send_id, static_cast<const uint8_t*>(src), rts.len});
+    t->pending_pulls.push_back(PendingPull{r, peer, rts.send_id, static_cast<const uint8_t*>(src), rts.len, key});
     t->stats.rendezvous_pulls++;
     t->stats.nvlink_bytes += rts.len;
 }
@@ -412,6 +538,7 @@ void flush_pulls(m4d_transport* t) {
         m4d::cuda_fail(e, "rendezvous pull");
         for (size_t i = from; i < to; ++i) {
             PendingPull& pp = t->pending_pulls[i];
+            pull_done(t, pp.key);
             queue_fin(t, pp.peer, pp.send_id, M4D_ERR_TRANSFER, 0);
             complete(t, pp.recv, M4D_ERR_CUDA, 0);
         }
@@ -456,7 +583,8 @@ void flush_pulls(m4d_transport* t) {
         } else {
             Launch l{ev, {}};
             l.msgs.reserve(j - i);
-            for (size_t k = i; k < j; ++k) l.msgs.push_back(Copy{v[k].recv, v[k].peer, v[k].send_id, v[k].len});
+            for (size_t k = i; k < j; ++k)
+                l.msgs.push_back(Copy{v[k].recv, v[k].peer, v[k].send_id, v[k].len, v[k].key});
             t->inflight[si].push_back(std::move(l));
             ++t->inflight_launches;
         }
@@ -515,6 +643,7 @@ void fail_peer(m4d_transport* t, int peer, int status, const char* why) {
         }
     }
     for (Req* r : victims) complete(t, r, M4D_ERR_TRANSFER, r->kind == kSend ? r->sent : 0);
+    drop_holds(t, peer);  // its answers to unmap requests will never come
 }
 
 // -- producer side ---------------------------------------------------------------------
@@ -694,6 +823,18 @@ void on_fin(m4d_transport* t, const FinRec* f) {
     complete(t, r, f->status, f->bytes);
 }
 
+void on_unmap(m4d_transport* t, int peer, const UnmapRec* u) {
+    auto it = t->ipc_maps.find(MapKey{u->pid, u->buffer_id, true});
+    if (it == t->ipc_maps.end()) {  // never mapped here (same process, or a purged send): answer now
+        queue_unmap(t, peer, kUnmapAck, 0, u->buffer_id, u->base);
+        return;
+    }
+    it->second.unmap_requested = true;
+    it->second.unmap_peer = peer;
+    it->second.exporter_base = u->base;
+    if (it->second.inflight <= 0) close_mapping(t, it);
+}
+
 int drain_peer(m4d_transport* t, int peer) {
     Peer& p = t->peers[peer];
     Ring& ring = p.in;
@@ -708,6 +849,8 @@ int drain_peer(m4d_transport* t, int peer) {
             case kRts: on_rts(t, peer, reinterpret_cast<const RtsRec*>(h)); break;
             case kFin: on_fin(t, reinterpret_cast<const FinRec*>(h)); break;
             case kBye: p.said_bye = true; break;
+            case kUnmap: on_unmap(t, peer, reinterpret_cast<const UnmapRec*>(h)); break;
+            case kUnmapAck: settle_export(reinterpret_cast<const UnmapRec*>(h)->base); break;
             default: break;  // kPad
         }
         ring.cursor += h->bytes;
@@ -727,6 +870,7 @@ int poll_copies(m4d_transport* t) {
             if (e == cudaErrorNotReady) break;
             if (e != cudaSuccess) m4d::cuda_fail(e, "rendezvous copy");
             for (const Copy& c : l.msgs) {
+                pull_done(t, c.src);
                 if (e == cudaSuccess) {
                     queue_fin(t, c.peer, c.send_id, M4D_OK, c.bytes);
                     complete(t, c.recv, M4D_OK, c.bytes);
@@ -816,6 +960,43 @@ void map_missing_peers(m4d_transport* t) {
 }
 
 }  // namespace
+
+namespace m4d {
+
+// m4d_free of an allocation a transport exported: every peer that was sent an RTS
+// for it is asked to close its mapping, and the cudaFree waits for their answers
+// (settle_export).  Returns true when the free was taken over (deferred).
+bool release_exported(void* ptr) {
+    const uint64_t base = reinterpret_cast<uint64_t>(ptr);
+    std::vector<ExportHold> holds;
+    uint64_t id = 0;
+    {
+        std::lock_guard<std::mutex> lk(g_exp_mu);
+        auto it = g_exports.find(base);
+        if (it == g_exports.end()) return false;
+        if (it->second.acks_pending > 0) return true;  // already being released
+        if (it->second.holds.empty()) {
+            g_exports.erase(it);
+            return false;
+        }
+        holds = it->second.holds;
+        id = it->second.buffer_id;
+        it->second.holds.clear();
+        it->second.acks_pending = static_cast<int>(holds.size());
+    }
+    for (const ExportHold& h : holds) {
+        h.t->exports.erase(id);
+        if (h.t->peers[h.peer].dead) {
+            settle_export(base);
+            continue;
+        }
+        queue_unmap(h.t, h.peer, kUnmap, static_cast<int32_t>(getpid()), id, base);
+        flush_peer(h.t, h.peer);
+    }
+    return true;
+}
+
+}  // namespace m4d
 
 extern "C" {
 
@@ -989,6 +1170,7 @@ m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer,
             ex = t->exports.insert_or_assign(rts.buffer_id, std::make_pair(base, h)).first;
         }
         memcpy(rts.handle, ex->second.second.data(), 64);
+        note_export(t, peer, base, rts.buffer_id);
     }
     t->reqs[req_id] = std::move(r);
     raw->in_outq = true;
@@ -1219,7 +1401,8 @@ m4d_status m4d_transport_close(m4d_transport* t) {
         for (cudaEvent_t e : t->spare_events) cudaEventDestroy(e);
         for (cudaStream_t st : t->pull_streams) cudaStreamDestroy(st);
     }
-    for (auto& kv : t->ipc_maps) cudaIpcCloseMemHandle(kv.second);
+    for (auto& kv : t->ipc_maps) cudaIpcCloseMemHandle(kv.second.base);
+    drop_holds(t, -1);
     for (Peer& p : t->peers)
         if (p.seg) munmap(p.seg, p.seg_len);
     if (t->me) {

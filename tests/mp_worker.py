@@ -10,6 +10,7 @@ MODE     ts        transpose_sum, 2048^2 fp64 / 256 blocks, peers' x pools mappe
                    mapped through CUDA IPC), digest checked against the oracle
          km_pull   key_merge with the rendezvous pull shuffle (device frames of the transport)
          frames    device frames of many sizes both ways through the transport, bit-exact
+         churn     150 freshly allocated device frames sent and freed: no exporter memory leak
 DEVMODE  same      every rank on cuda:0 (one B200: still separate processes, so IPC)
          own       rank r on cuda:r (NVLink between B200s)
 
@@ -128,6 +129,40 @@ def run_frames(t, rank, world, device):
     return {"sizes": len(sizes), "staged": t.metrics.staging_copies, "pulls": stats["rendezvous_pulls"]}
 
 
+def run_churn(t, rank, world, device):
+    """Rank 0 sends 150 freshly allocated 8 MiB device frames (freed after each send),
+    rank 1 receives them; rank 0's free device memory must come back (the receiver closes
+    each CUDA-IPC mapping before the exporter's cudaFree, transport.cpp release_exported)."""
+    from paper_2101_08878_b200.transport import MemoryDomain
+    from paper_2101_08878_b200.transport.base import DeviceView
+    from paper_2101_08878_b200.transport.nvlink import CudaRegion
+
+    n, frames = 8 << 20, 150
+    recv = native.DeviceBuffer(device, n)
+    allgather_sync(t, b"\x00", 980)
+    before = native.mem_get_info(device)[0]
+    for i in range(frames):
+        if rank == 0:
+            region = CudaRegion(n, device)
+            native.check(native.lib().m4d_memset(region.ptr, i % 251, n, None))
+            req = t.post_send(0, 1, 600, region.window(), MemoryDomain.DEVICE)
+        else:
+            req = t.post_recv(0, 0, 600, DeviceView(recv.ptr, n, device), MemoryDomain.DEVICE)
+        while req.pending:
+            t.progress()
+        assert not req.failed, req.error
+        if rank == 0:
+            del region, req
+        else:
+            assert native.to_host(recv.ptr + n - 1, 1)[0] == i % 251
+    allgather_sync(t, b"\x00", 981)  # drives both sides' progress: unmaps and their answers
+    for _ in range(100):
+        t.progress()
+    allgather_sync(t, b"\x00", 982)
+    after = native.mem_get_info(device)[0]
+    return {"frames": frames, "leak_mib": (before - after) / 2**20}
+
+
 def main() -> int:
     mode, rank, world, session, devmode = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
     device = rank if devmode == "own" else 0
@@ -139,6 +174,8 @@ def main() -> int:
         out = run_km(t, rank, world, device, mode[3:])
     elif mode == "frames":
         out = run_frames(t, rank, world, device)
+    elif mode == "churn":
+        out = run_churn(t, rank, world, device)
     else:
         raise SystemExit(f"unknown mode {mode}")
     allgather_sync(t, b"\x00", 990)  # nobody closes while a peer still reads its memory

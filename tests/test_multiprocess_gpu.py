@@ -82,3 +82,11 @@ def test_key_merge_four_processes_own_gpus():
 def test_device_frames_across_processes(devmode):
     res = launch("frames", 2, devmode)
     assert all(r["staged"] == 0 and r["pulls"] > 0 for r in res)
+
+
+@pytest.mark.parametrize("devmode", ["same", "own"])
+def test_freed_device_frames_are_unmapped_before_free(devmode):
+    """150 fresh 8 MiB frames (1.2 GB) sent and freed: the sender's device memory stays
+    flat because every importer closes its mapping before the deferred cudaFree."""
+    res = launch("churn", 2, devmode)
+    assert res[0]["leak_mib"] < 64, res
