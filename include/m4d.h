@@ -60,6 +60,8 @@ size_t m4d_last_error(char* buf, size_t n);
 int m4d_version(void);
 /* Number of visible CUDA devices (0 on a host without a driver; never fails). */
 int m4d_device_count(void);
+/* Device that owns device (or managed) memory `ptr`; *device = -1 for host memory. */
+m4d_status m4d_pointer_device(const void* ptr, int* device);
 /* cudaMemGetInfo of `device` (bytes free / total). */
 m4d_status m4d_mem_get_info(int device, uint64_t* free_bytes, uint64_t* total_bytes);
 

@@ -119,6 +119,13 @@ size_t m4d_last_error(char* buf, size_t n) {
 
 int m4d_version(void) { return (1 << 16) | 0; }
 
+m4d_status m4d_pointer_device(const void* ptr, int* device) {
+    cudaPointerAttributes a;
+    M4D_CUDA_TRY(cudaPointerGetAttributes(&a, ptr));
+    *device = (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) ? a.device : -1;
+    return M4D_OK;
+}
+
 m4d_status m4d_mem_get_info(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
     M4D_CUDA_TRY(cudaSetDevice(device));
     size_t f = 0, t = 0;

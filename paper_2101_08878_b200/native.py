@@ -108,6 +108,7 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_last_error": (_size, [ctypes.c_char_p, _size]),
     "m4d_version": (ctypes.c_int, []),
     "m4d_device_count": (ctypes.c_int, []),
+    "m4d_pointer_device": (ctypes.c_int, [_c_void_p, ctypes.POINTER(ctypes.c_int)]),
     "m4d_mem_get_info": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "m4d_set_device": (ctypes.c_int, [ctypes.c_int]),
     "m4d_stream_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_c_void_p)]),
@@ -384,6 +385,13 @@ def memcpy(dst: int, src: int, nbytes: int, stream: Stream | None = None) -> Non
 
 def memset(dst: int, value: int, nbytes: int, stream: Stream | None = None) -> None:
     check(lib().m4d_memset(dst, value, nbytes, stream.handle if stream else None))
+
+
+def pointer_device(ptr: int) -> int:
+    """CUDA device owning `ptr` (-1: host memory)."""
+    dev = ctypes.c_int(-1)
+    check(lib().m4d_pointer_device(ptr, ctypes.byref(dev)))
+    return dev.value
 
 
 def mem_get_info(device: int) -> tuple[int, int]:

@@ -11,6 +11,7 @@ MODE     ts        transpose_sum, 2048^2 fp64 / 256 blocks, peers' x pools mappe
          km_pull   key_merge with the rendezvous pull shuffle (device frames of the transport)
          frames    device frames of many sizes both ways through the transport, bit-exact
          churn     150 freshly allocated device frames sent and freed: no exporter memory leak
+         torch     torch tensors through Endpoint.write/read as zero-copy device array frames
 DEVMODE  same      every rank on cuda:0 (one B200: still separate processes, so IPC)
          own       rank r on cuda:r (NVLink between B200s)
 
@@ -163,6 +164,62 @@ def run_churn(t, rank, world, device):
     return {"frames": frames, "leak_mib": (before - after) / 2**20}
 
 
+def run_torch(t, rank, world, device):
+    """Torch tensors (caching-allocator memory, several sharing one allocator segment)
+    written by rank 0 through Endpoint.write as array_frames (zero-copy device frames,
+    serializer tag 3) and read by rank 1 as CUDA arrays on its own device."""
+    import torch
+
+    from paper_2101_08878_b200.channels import build_comm_table
+    from paper_2101_08878_b200.endpoints import Node, connect, listen
+    from paper_2101_08878_b200.loop import MonotonicClock, TaskLoop, sleep
+    from paper_2101_08878_b200.messaging import Message, array_frames, frames_to_array
+
+    torch.cuda.set_device(device)
+    specs = [(torch.float32, (1,)), (torch.int64, (1000,)), (torch.float32, (250_000,)), (torch.float64, (3, 1_000_000)),
+             (torch.int16, (7, 5))]
+    node = Node(t, build_comm_table(t))
+    loop = TaskLoop(MonotonicClock())
+    got = []
+
+    def expect(i, dtype, shape):
+        n = 1
+        for d in shape:
+            n *= d
+        return (torch.arange(n, device=f"cuda:{device}", dtype=torch.int64) * (i + 3) % 997).to(dtype).reshape(shape)
+
+    async def main():
+        if rank == 0:
+            ep = await connect(node, "mpi://1")
+            tensors = [expect(i, dt, sh) for i, (dt, sh) in enumerate(specs)]  # caching-allocator blocks
+            for x in tensors:
+                await ep.write(Message(array_frames(x)))
+            await ep.read()  # the reader's "done"
+            await ep.close()
+        else:
+            done = []
+
+            async def handler(ep):
+                for i, (dt, sh) in enumerate(specs):
+                    msg = await ep.read()
+                    arr = frames_to_array(msg.frames)
+                    y = arr.to_torch()
+                    assert y.device.index == device and y.dtype == dt and tuple(y.shape) == sh, (y.device, y.dtype, y.shape)
+                    assert y.data_ptr() == arr.region.ptr  # zero copy: the tensor is the received region
+                    assert torch.equal(y, expect(i, dt, sh)), i
+                    got.append(tuple(sh))
+                from paper_2101_08878_b200.messaging import make_frame
+                await ep.write(Message([make_frame("done", 1)]))
+                done.append(True)
+
+            await listen(node, "mpi://1", handler).start()
+            while not done:
+                await sleep(0)
+
+    loop.run_until_complete(main())
+    return {"tensors": len(specs) if rank == 0 else len(got), "staged": t.metrics.staging_copies}
+
+
 def main() -> int:
     mode, rank, world, session, devmode = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), sys.argv[4], sys.argv[5]
     device = rank if devmode == "own" else 0
@@ -176,6 +233,8 @@ def main() -> int:
         out = run_frames(t, rank, world, device)
     elif mode == "churn":
         out = run_churn(t, rank, world, device)
+    elif mode == "torch":
+        out = run_torch(t, rank, world, device)
     else:
         raise SystemExit(f"unknown mode {mode}")
     allgather_sync(t, b"\x00", 990)  # nobody closes while a peer still reads its memory

@@ -41,7 +41,7 @@ def launch(mode, world, devmode, timeout=300):
         outs.append((p.returncode, out))
     for rc, out in outs:
         assert rc == 0, out[-4000:]
-    return [json.loads(out.strip().splitlines()[-1]) for _, out in outs]
+    return [json.loads(next(ln for ln in reversed(out.splitlines()) if ln.startswith('{"rank"'))) for _, out in outs]
 
 
 @pytest.mark.parametrize("devmode", ["same", "own"])
@@ -90,3 +90,11 @@ def test_freed_device_frames_are_unmapped_before_free(devmode):
     flat because every importer closes its mapping before the deferred cudaFree."""
     res = launch("churn", 2, devmode)
     assert res[0]["leak_mib"] < 64, res
+
+
+@pytest.mark.parametrize("devmode", ["same", "own"])
+def test_torch_tensors_cross_processes_as_device_array_frames(devmode):
+    """Dask-style Comm.write of torch tensors (caching-allocator memory, legacy CUDA IPC),
+    decoded on the far side as zero-copy CUDA arrays (serializer tag 3)."""
+    res = launch("torch", 2, devmode)
+    assert res[1]["tensors"] == 5 and all(r["staged"] == 0 for r in res)
