@@ -8,9 +8,10 @@ re-exported, ``errors``), the same module layout (``loop``, ``errors``,
   device-to-device between B200s (CUDA IPC over NVLink), never through host
   memory, driven by the C-ABI library ``libm4d.so``;
 * ``harness`` — the paper's two operators (``transpose_sum``, ``key_merge``)
-  as hand-written sm_100a kernels;
+  as hand-written sm_100a kernels, plus the mini cluster (scheduler / client /
+  worker roles, heartbeats with suspect marking: ``harness.cluster``);
 * ``cli`` — the ``commshim-bench`` / ``commshim-launch`` entry points the
-  reference declares (``pkg/pyproject.toml:14-16``).
+  reference declares (``pkg/pyproject.toml:14-16``), wired in ``pyproject.toml``.
 
 ``import commshim`` resolves to this package through the alias package at the
 repository root.
