@@ -164,6 +164,7 @@ class KeyMerge:
     # -- data -------------------------------------------------------------------------------
 
     def generate(self) -> None:
+        native.set_device(self.device)  # (several ranks may share a process: tests, profiling)
         lib = native.lib()
         row0 = self.rank * self.n
         for side, (cols, seed, band) in enumerate(zip(self.inputs, self.seeds, (0, self.band))):
@@ -176,6 +177,7 @@ class KeyMerge:
 
     def _partition(self, src, n: int, mode: int, buckets: int, dst: _Pairs, bounds) -> None:
         keys, vals = (src.keys.ptr, src.vals.ptr) if isinstance(src, _Columns) else (src.ptr, None)
+        native.set_device(self.device)  # ranks of one process may sit on different GPUs
         native.check(native.lib().m4d_partition(keys, vals, n, mode, buckets, dst.ptr, bounds.ptr, self.scratch.ptr,
                                                 self.scratch_bytes, self.stream.handle))
         self.launches += native.lib().m4d_partition_launches(buckets)
@@ -200,6 +202,7 @@ class KeyMerge:
         local partition), i.e. routed to their owner and already through the owner's first
         local pass.  Returns the P * C + 1 bucket bounds (synchronises)."""
         P, C = self.world, self.coarse
+        native.set_device(self.device)  # ranks of one process may sit on different GPUs
         native.check(native.lib().m4d_partition_owner_coarse(
             self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.sendbuf[side].ptr,
             self.rank_bounds[side].ptr, self.scratch.ptr, self.scratch_bytes, self.stream.handle))
@@ -258,6 +261,7 @@ class KeyMerge:
             for c in range(C):
                 runs[c, src] = (starts[src] + r[c], starts[src] + r[c + 1])
         total = int(starts[-1])
+        native.set_device(self.device)  # ranks of one process may sit on different GPUs
         native.check(native.lib().m4d_partition_runs(self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts,
                                                      self.parted[side].ptr, self.bounds[side].ptr, self.scratch.ptr,
                                                      self.scratch_bytes, (stream or self.stream).handle))
@@ -319,6 +323,7 @@ class KeyMerge:
         if self._peer_recv is None:
             await self._connect_push()
         for side in range(2):
+            native.set_device(self.device)  # ranks of one process may sit on different GPUs
             native.check(lib.m4d_partition_owner_plan(
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.rank_bounds[side].ptr,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
@@ -341,6 +346,7 @@ class KeyMerge:
             for d in range(P):  # my segment in owner d's buffer: after the rows of lower sources
                 before = sum(tables[src][side * width + d * (C + 1) + C] for src in range(me))
                 dest[d] = self._peer_recv[side][d] + before * 16
+            native.set_device(self.device)  # ranks of one process may sit on different GPUs
             native.check(lib.m4d_partition_owner_push(
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
@@ -366,6 +372,7 @@ class KeyMerge:
 
     async def run(self) -> tuple[int, int, int]:
         """One full step (partition [+ shuffle] + join).  Returns this rank's digest."""
+        native.set_device(self.device)
         if self.profile:
             import time
 
@@ -387,6 +394,7 @@ class KeyMerge:
         if self.timing:
             self._ev[1].record(self.stream)
         while True:
+            native.set_device(self.device)  # ranks of one process may sit on different GPUs
             native.check(native.lib().m4d_hash_join(
                 self.parted[0].ptr, self.bounds[0].ptr, self.parted[1].ptr, self.bounds[1].ptr, self.parts,
                 self.out[0].ptr, self.out[1].ptr, self.out[2].ptr, self.out_capacity, self.result.ptr,

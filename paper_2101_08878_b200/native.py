@@ -298,6 +298,8 @@ class Event:
         self.handle = h.value
 
     def record(self, stream: Stream | None) -> None:
+        if stream is not None:
+            set_device(stream.device)  # a stream belongs to its device (ranks may share a process)
         check(lib().m4d_event_record(self.handle, stream.handle if stream else None))
 
     def synchronize(self) -> None:
@@ -380,6 +382,8 @@ class PinnedHostBuffer:
 
 
 def memcpy(dst: int, src: int, nbytes: int, stream: Stream | None = None) -> None:
+    if stream is not None:
+        set_device(stream.device)
     check(lib().m4d_memcpy(dst, src, nbytes, stream.handle if stream else None))
 
 
