@@ -146,6 +146,12 @@ class KeyMerge:
             self.overlap = os.environ.get("M4D_MERGE_OVERLAP", "1") != "0"
             self.split_stream = native.Stream(device) if self.overlap else self.stream
             self.split_done = native.Event()
+        # world == 1: side 1 partitions on its own stream (M4D_MERGE_SIDES=serial: one stream)
+        self.side_stream = self.side_scratch = None
+        if world == 1 and os.environ.get("M4D_MERGE_SIDES", "concurrent") != "serial":
+            self.side_stream = native.Stream(device)
+            self.side_scratch = native.DeviceBuffer(device, scratch)
+            self.side_ready, self.side_done = native.Event(), native.Event()
         self._peer_recv: list[list[int]] | None = None  # [side][rank] receive-buffer address (mapped)
         self._imported: list[int] = []
         self.out_capacity = int(fraction * self.n * 1.25) + 65536
@@ -175,11 +181,13 @@ class KeyMerge:
 
     # -- pipeline ---------------------------------------------------------------------------
 
-    def _partition(self, src, n: int, mode: int, buckets: int, dst: _Pairs, bounds) -> None:
+    def _partition(self, src, n: int, mode: int, buckets: int, dst: _Pairs, bounds, stream=None,
+                   scratch=None) -> None:
         keys, vals = (src.keys.ptr, src.vals.ptr) if isinstance(src, _Columns) else (src.ptr, None)
         native.set_device(self.device)  # ranks of one process may sit on different GPUs
-        native.check(native.lib().m4d_partition(keys, vals, n, mode, buckets, dst.ptr, bounds.ptr, self.scratch.ptr,
-                                                self.scratch_bytes, self.stream.handle))
+        native.check(native.lib().m4d_partition(keys, vals, n, mode, buckets, dst.ptr, bounds.ptr,
+                                                (scratch or self.scratch).ptr, self.scratch_bytes,
+                                                (stream or self.stream).handle))
         self.launches += native.lib().m4d_partition_launches(buckets)
 
     def _mark(self, name: str) -> None:
@@ -387,9 +395,19 @@ class KeyMerge:
                 self.close()  # the pull path may grow the receive buffers: map them again next step
             self.received = got if got is not None else await self._shuffle_and_partition()
         else:
+            # The two sides partition concurrently on two streams: each pass is
+            # latency-bound with one or two CTAs per SM, so CTAs of the other side's
+            # kernels fill the rest of the SM.
             self.received = [self.n, self.n]
-            for side in range(2):
-                self._partition(self.inputs[side], self.n, 0, self.parts, self.parted[side], self.bounds[side])
+            if self.side_stream is not None:
+                self.side_ready.record(self.stream)
+                self.side_ready.wait_on(self.side_stream)
+            self._partition(self.inputs[0], self.n, 0, self.parts, self.parted[0], self.bounds[0])
+            self._partition(self.inputs[1], self.n, 0, self.parts, self.parted[1], self.bounds[1],
+                            self.side_stream, self.side_scratch)
+            if self.side_stream is not None:
+                self.side_done.record(self.side_stream)
+                self.side_done.wait_on(self.stream)
         self._mark("local_partition_ms")
         if self.timing:
             self._ev[1].record(self.stream)
