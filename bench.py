@@ -497,6 +497,11 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
     loop.run_until_complete(km.run_global())
     km.profile = False
     phase = {k: round(v, 3) for k, v in km.phases.items()}
+    # and an event trace of one more step without any added synchronisation (overlap visible)
+    km.tracing = True
+    loop.run_until_complete(km.run_global())
+    km.tracing = False
+    trace = dict(km.trace)
 
     alg = km.algorithmic_bytes()
     hbm_peak = float(peaks["hbm_gbs"])
@@ -511,7 +516,8 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
                 "peak_source": peaks["_source"]}
     roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": args.traffic,
                  "kernel": "whole merge step (partition + shuffle + join kernels)",
-                 "algorithmic_bytes_per_step": alg, "t_roof_ms": max(t_hbm, t_nvl) * 1e3, "phases": phase})
+                 "algorithmic_bytes_per_step": alg, "t_roof_ms": max(t_hbm, t_nvl) * 1e3, "phases": phase,
+                 "trace_ms": trace})
     # Per kernel group, CUDA events on the merge stream inside the timed steps (rank 0).
     # join: reads both partitioned tables once, writes the output once.  partition (N=1):
     # two passes per side, each reading and writing 16 B per row (the algorithm's own

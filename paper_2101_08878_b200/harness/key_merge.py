@@ -160,6 +160,9 @@ class KeyMerge:
         self.received = [0, 0]
         self.launches = 0
         self.profile = False  # diagnostics: synchronise and stamp each phase (never in timed runs)
+        self.tracing = False  # diagnostics: CUDA-event trace points without synchronisation
+        self._trace_points: list = []
+        self.trace: dict[str, float] = {}
         # CUDA-event kernel timing inside timed runs (no synchronisation added): partition
         # kernels (local or plan + push) and the join, summed over steps in kernel_ms
         self.timing = False
@@ -189,6 +192,15 @@ class KeyMerge:
                                                 (scratch or self.scratch).ptr, self.scratch_bytes,
                                                 (stream or self.stream).handle))
         self.launches += native.lib().m4d_partition_launches(buckets)
+
+    def _tp(self, name: str, stream=None) -> None:
+        """Trace point (diagnostics, ``self.tracing``): a CUDA event on `stream`; after the
+        step, ``self.trace`` maps each name to its time in ms since the step began.
+        Unlike ``profile`` this adds no synchronisation, so overlap stays visible."""
+        if self.tracing:
+            ev = native.Event()
+            ev.record(stream or self.stream)
+            self._trace_points.append((name, ev))
 
     def _mark(self, name: str) -> None:
         if self.profile:
@@ -336,6 +348,7 @@ class KeyMerge:
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.rank_bounds[side].ptr,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
         self.launches += 10
+        self._tp("plans_done")
         blob = b""
         for side in range(2):  # my rows per (owner, coarse run), relative to each owner's segment
             b = self._read_bounds(self.rank_bounds[side], P * C)
@@ -354,18 +367,22 @@ class KeyMerge:
             for d in range(P):  # my segment in owner d's buffer: after the rows of lower sources
                 before = sum(tables[src][side * width + d * (C + 1) + C] for src in range(me))
                 dest[d] = self._peer_recv[side][d] + before * 16
+            self._tp(f"push{side}_start")
             native.set_device(self.device)  # ranks of one process may sit on different GPUs
             native.check(lib.m4d_partition_owner_push(
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
             self.pushed[side].record(self.stream)
+            self._tp(f"push{side}_end")
         self.launches += 2
         out = []
         for side in range(2):
             self.pushed[side].synchronize()  # my rows for side `side` are in every owner's buffer
             await allgather(t, b"\x01", EXCHANGE_TAG + 6 + side)  # ... and every peer's rows in mine
             self._mark(f"side{side}_push_ms")
+            self._tp(f"split{side}_start", self.split_stream)
             out.append(self._finish_side(side, runs_in[side], C, self.split_stream))
+            self._tp(f"split{side}_end", self.split_stream)
         if self.split_stream is not self.stream:  # the join waits for both splits
             self.split_done.record(self.split_stream)
             self.split_done.wait_on(self.stream)
@@ -389,6 +406,8 @@ class KeyMerge:
             self.phases = {}
         if self.timing:
             self._ev[0].record(self.stream)
+        self._trace_points = []
+        self._tp("step_start")
         if self.world > 1:
             got = await self._push_shuffle_and_partition() if self.shuffle == "push" else None
             if got is None and self.shuffle == "push":
@@ -411,6 +430,7 @@ class KeyMerge:
         self._mark("local_partition_ms")
         if self.timing:
             self._ev[1].record(self.stream)
+        self._tp("join_start")
         while True:
             native.set_device(self.device)  # ranks of one process may sit on different GPUs
             native.check(native.lib().m4d_hash_join(
@@ -420,7 +440,11 @@ class KeyMerge:
             self.launches += 2
             if self.timing:
                 self._ev[2].record(self.stream)
+            self._tp("join_end")
             raw = native.to_host(self.result.ptr, 32, self.stream)
+            if self.tracing:  # the read-back synchronised the stream
+                t0 = self._trace_points[0][1]
+                self.trace = {name: round(t0.elapsed_ms(ev), 3) for name, ev in self._trace_points}
             if self.timing:  # the read-back synchronised the stream
                 self.kernel_ms["partition"] += self._ev[0].elapsed_ms(self._ev[1])
                 self.kernel_ms["join"] += self._ev[1].elapsed_ms(self._ev[2])
