@@ -256,7 +256,7 @@ struct PeerMap {
 static uint64_t lone_ce_max() {
     static const uint64_t v = [] {
         const char* e = getenv("M4D_LONE_CE_MAX");
-        return e ? static_cast<uint64_t>(atoll(e)) : uint64_t(1) << 20;
+        return e && atoll(e) >= 0 ? static_cast<uint64_t>(atoll(e)) : uint64_t(1) << 20;  // negative: default
     }();
     return v;
 }
@@ -265,7 +265,7 @@ static uint64_t lone_ce_max() {
 static uint64_t small_pull() {
     static const uint64_t v = [] {
         const char* e = getenv("M4D_SMALL_PULL");
-        return e ? static_cast<uint64_t>(atoll(e)) : uint64_t(64 * 1024);
+        return e && atoll(e) >= 0 ? static_cast<uint64_t>(atoll(e)) : uint64_t(64 * 1024);  // negative: default
     }();
     return v;
 }

@@ -311,3 +311,34 @@ def test_peer_death_fails_pending_receives_and_sends():
     finally:
         if child.poll() is None:
             child.kill()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("env,kernel", [
+    ({}, "some"),                                                     # defaults: window on the kernel, lone on the copy engine
+    ({"M4D_SMALL_PULL": str(1 << 40)}, "none"),                       # everything below 1 TiB on the copy engine
+    ({"M4D_PULL_ENGINE": "ce"}, "none"),                              # copy engine only
+    ({"M4D_LONE_CE_MAX": "0", "M4D_SMALL_PULL": "0"}, "all"),         # every device pull on the kernel
+    ({"M4D_PULL_BATCH_BYTES": "1"}, "some"),                          # one message per launch
+    ({"M4D_SMALL_PULL": "-5", "M4D_LONE_CE_MAX": "-1"}, "some"),      # negative knobs fall back to the defaults
+])
+def test_pull_routing_knobs_keep_the_bytes(env, kernel):
+    """Each pull route (SM kernel, copy engine, lone copy-engine pull, byte-capped batches)
+    moves a mixed window of 64 KiB-32 MiB device frames bit-exactly; the launch counter shows
+    which route ran."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "tests", "pull_routing_worker.py")],
+                         env={**os.environ, **env}, capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-3000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["ok"] and res["pulls"] == 12
+    if kernel == "none":
+        assert res["kernel_launches"] == 0
+    elif kernel == "all":
+        assert res["kernel_launches"] >= 6  # every lone pull launched the kernel
+    else:
+        assert 0 < res["kernel_launches"] < 12
