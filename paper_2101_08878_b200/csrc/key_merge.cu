@@ -999,6 +999,20 @@ static int push_ctas_per_sm() {
     return c;
 }
 
+// SMs the push scatter's grid may occupy (M4D_PUSH_SMS, default 96): the rest
+// stay free for the receiver split of the side pushed before (split stream),
+// which otherwise waits for push CTAs to retire (they hold the register file).
+// Sweep (tools/r2_push_sms.sh, N=2 / N=4 step ms): 148 -> 7.06 / 8.68,
+// 112 -> 6.84 / 8.19, 96 -> 6.84 / 8.04, 80 -> 6.90 / 8.40, 64 -> 6.89 / 8.51.
+static int push_sms() {
+    static const int c = [] {
+        const char* v = getenv("M4D_PUSH_SMS");
+        const int x = v ? atoi(v) : 96;
+        return x < 1 ? 1 : x > 148 ? 148 : x;
+    }();
+    return c;
+}
+
 // Threads per receiver-split CTA (M4D_RUNS_THREADS = 512 | 1024, default 1024).
 static int runs_threads() {
     static const int t = [] {
@@ -1070,8 +1084,13 @@ static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int
                                    const PushTargets* push = nullptr, bool push_layout = false) {
     if (scratch_bytes < m4d_partition_scratch_bytes(n, buckets)) return fail(M4D_ERR_USAGE, "partition scratch too small");
     // (the push scatter's plan and scatter calls both size the grid for its CTAs)
-    const int ctas = push_layout ? partition_ctas(n, push_tile_threads(), push_ctas_per_sm())
-                                 : partition_ctas(n, tile_threads());
+    int ctas = push_layout ? partition_ctas(n, push_tile_threads(), push_ctas_per_sm())
+                           : partition_ctas(n, tile_threads());
+    if (push_layout) {
+        const int per_sm = push_tile_threads() >= 1024 ? 1 : push_tile_threads() >= 512 ? 2 : 4;
+        const int cap = push_sms() * (per_sm < push_ctas_per_sm() ? per_sm : push_ctas_per_sm());
+        if (ctas > cap) ctas = cap;
+    }
     const int64_t run = (n + ctas - 1) / ctas;
     if (buckets > kMaxBuckets) return fail(M4D_ERR_USAGE, "bucket count %d above the single-pass limit", buckets);
     if (push && buckets > kTileBuckets) return fail(M4D_ERR_USAGE, "push scatter limited to %d buckets", kTileBuckets);

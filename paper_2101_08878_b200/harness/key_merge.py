@@ -123,6 +123,9 @@ class KeyMerge:
                       lib.m4d_partition_runs_scratch_bytes(max(world, 1), self.parts, self.coarse))
         self.scratch = native.DeviceBuffer(device, scratch)
         self.scratch_bytes = scratch
+        # side 1's receiver split may run beside side 0's: its own (small) scratch
+        runs_bytes = lib.m4d_partition_runs_scratch_bytes(max(world, 1), self.parts, self.coarse) if world > 1 else 0
+        self.split_scratch1 = (native.DeviceBuffer(device, max(1, runs_bytes)), runs_bytes) if world > 1 else None
         self.shuffle = (shuffle or _SHUFFLE) if world > 1 else "local"
         if self.shuffle not in ("push", "pull", "local"):
             raise UsageError(f"unknown shuffle {self.shuffle!r} (push | pull)")
@@ -144,8 +147,11 @@ class KeyMerge:
             # M4D_MERGE_OVERLAP=1 (default): the receiver splits run on a second stream, so
             # side 0's split (HBM-bound) overlaps side 1's push (NVLink-bound)
             self.overlap = os.environ.get("M4D_MERGE_OVERLAP", "1") != "0"
-            self.split_stream = native.Stream(device) if self.overlap else self.stream
-            self.split_done = native.Event()
+            # one split stream per side: side 1's split may start while side 0's finishes
+            self.split_streams = ([native.Stream(device), native.Stream(device)] if self.overlap
+                                  else [self.stream, self.stream])
+            self.split_stream = self.split_streams[0]
+            self.split_done = [native.Event(), native.Event()]
         # world == 1: side 1 partitions on its own stream (M4D_MERGE_SIDES=serial: one stream)
         self.side_stream = self.side_scratch = None
         if world == 1 and os.environ.get("M4D_MERGE_SIDES", "concurrent") != "serial":
@@ -207,8 +213,8 @@ class KeyMerge:
             import time
 
             self.stream.synchronize()
-            if getattr(self, "split_stream", None) is not None:
-                self.split_stream.synchronize()
+            for st in getattr(self, "split_streams", []):
+                st.synchronize()
             now = time.perf_counter()
             self.phases[name] = (now - self._t_last) * 1e3
             self._t_last = now
@@ -282,9 +288,10 @@ class KeyMerge:
                 runs[c, src] = (starts[src] + r[c], starts[src] + r[c + 1])
         total = int(starts[-1])
         native.set_device(self.device)  # ranks of one process may sit on different GPUs
+        scratch, nbytes = (self.scratch, self.scratch_bytes) if side == 0 else self.split_scratch1
         native.check(native.lib().m4d_partition_runs(self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts,
-                                                     self.parted[side].ptr, self.bounds[side].ptr, self.scratch.ptr,
-                                                     self.scratch_bytes, (stream or self.stream).handle))
+                                                     self.parted[side].ptr, self.bounds[side].ptr, scratch.ptr,
+                                                     nbytes, (stream or self.stream).handle))
         self.launches += 4
         return total
 
@@ -380,12 +387,13 @@ class KeyMerge:
             self.pushed[side].synchronize()  # my rows for side `side` are in every owner's buffer
             await allgather(t, b"\x01", EXCHANGE_TAG + 6 + side)  # ... and every peer's rows in mine
             self._mark(f"side{side}_push_ms")
-            self._tp(f"split{side}_start", self.split_stream)
-            out.append(self._finish_side(side, runs_in[side], C, self.split_stream))
-            self._tp(f"split{side}_end", self.split_stream)
-        if self.split_stream is not self.stream:  # the join waits for both splits
-            self.split_done.record(self.split_stream)
-            self.split_done.wait_on(self.stream)
+            self._tp(f"split{side}_start", self.split_streams[side])
+            out.append(self._finish_side(side, runs_in[side], C, self.split_streams[side]))
+            self._tp(f"split{side}_end", self.split_streams[side])
+        for side in range(2):  # the join waits for both splits
+            if self.split_streams[side] is not self.stream:
+                self.split_done[side].record(self.split_streams[side])
+                self.split_done[side].wait_on(self.stream)
         return out
 
     def close(self) -> None:
