@@ -144,6 +144,7 @@ class KeyMerge:
             self.push_scratch = [native.DeviceBuffer(device, nb) for _ in range(2)]
             self.push_scratch_bytes = nb
             self.pushed = [native.Event(), native.Event()]
+            self.plan_stream = native.Stream(device)
             # M4D_MERGE_OVERLAP=1 (default): the receiver splits run on a second stream, so
             # side 0's split (HBM-bound) overlaps side 1's push (NVLink-bound)
             self.overlap = os.environ.get("M4D_MERGE_OVERLAP", "1") != "0"
@@ -219,8 +220,8 @@ class KeyMerge:
             self.phases[name] = (now - self._t_last) * 1e3
             self._t_last = now
 
-    def _read_bounds(self, buf, count: int) -> list[int]:
-        raw = native.to_host(buf.ptr, (count + 1) * 8, self.stream)
+    def _read_bounds(self, buf, count: int, stream=None) -> list[int]:
+        raw = native.to_host(buf.ptr, (count + 1) * 8, stream or self.stream)
         return list(struct.unpack(f"<{count + 1}q", raw))
 
     def _owner_split(self, side: int) -> list[int]:
@@ -349,16 +350,18 @@ class KeyMerge:
         t, P, me, C, lib = self.transport, self.world, self.rank, self.coarse_push, native.lib()
         if self._peer_recv is None:
             await self._connect_push()
+        plan_streams = [self.stream, self.plan_stream]  # the two sides' plans run side by side
         for side in range(2):
             native.set_device(self.device)  # ranks of one process may sit on different GPUs
             native.check(lib.m4d_partition_owner_plan(
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.rank_bounds[side].ptr,
-                self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
+                self.push_scratch[side].ptr, self.push_scratch_bytes, plan_streams[side].handle))
         self.launches += 10
-        self._tp("plans_done")
         blob = b""
         for side in range(2):  # my rows per (owner, coarse run), relative to each owner's segment
-            b = self._read_bounds(self.rank_bounds[side], P * C)
+            b = self._read_bounds(self.rank_bounds[side], P * C, plan_streams[side])
+            if side == 1:
+                self._tp("plans_done")
             blob += struct.pack(f"<{P * (C + 1)}q", *[b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)])
         width = P * (C + 1)
         tables = [struct.unpack(f"<{2 * width}q", x) for x in await allgather(t, blob, EXCHANGE_TAG + 2)]
