@@ -88,6 +88,20 @@ class _Pairs:
         self.ptr = self.buf.ptr
 
 
+class _RawBytes:
+    """``__cuda_array_interface__`` of a raw device byte range (a torch view, no copy)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None, "stream": None}
+
+
+def _torch_bytes(ptr: int, nbytes: int, device: int):
+    import torch
+
+    return torch.as_tensor(_RawBytes(ptr, nbytes), device=torch.device("cuda", device))
+
+
 class KeyMerge:
     """One rank's share of a distributed inner merge on an int64 key."""
 
@@ -127,8 +141,16 @@ class KeyMerge:
         runs_bytes = lib.m4d_partition_runs_scratch_bytes(max(world, 1), self.parts, self.coarse) if world > 1 else 0
         self.split_scratch1 = (native.DeviceBuffer(device, max(1, runs_bytes)), runs_bytes) if world > 1 else None
         self.shuffle = (shuffle or _SHUFFLE) if world > 1 else "local"
-        if self.shuffle not in ("push", "pull", "local"):
-            raise UsageError(f"unknown shuffle {self.shuffle!r} (push | pull)")
+        if self.shuffle not in ("push", "pull", "nccl", "local"):
+            raise UsageError(f"unknown shuffle {self.shuffle!r} (push | pull | nccl)")
+        if self.shuffle == "nccl":
+            # owner pass per side on its own stream, NCCL all-to-all (torch.distributed, the
+            # default NCCL group) enqueued on that stream, receiver split on a split stream
+            self.nccl_streams = [self.stream, native.Stream(device)]
+            self.nccl_scratch1 = native.DeviceBuffer(device, scratch)
+            self.a2a_done = [native.Event(), native.Event()]
+            self.split_streams = [native.Stream(device), native.Stream(device)]
+            self.split_done = [native.Event(), native.Event()]
         if self.shuffle == "push":  # per-side plan scratch (both plans live until their push)
             # Coarse runs per owner of the push scatter (M4D_PUSH_BUCKETS = owners x runs,
             # default 256).  Fewer make each tile's run per bucket longer, so NVLink
@@ -399,6 +421,56 @@ class KeyMerge:
                 self.split_done[side].wait_on(self.stream)
         return out
 
+    async def _nccl_shuffle_and_partition(self) -> list[int]:
+        """Owner pass of each side into a local send buffer, then one NCCL all-to-all per
+        side (NVLink, ``torch.distributed.all_to_all_single`` on the raw buffers) enqueued
+        on that side's stream -- side 1's owner pass runs while side 0's bytes move --
+        and the receiver split of each side once its all-to-all is done.  The rows land
+        source-major, as in the pull shuffle."""
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        t, P, me, C, lib = self.transport, self.world, self.rank, self.coarse, native.lib()
+        out = []
+        runs = []
+        for side in range(2):
+            st = self.nccl_streams[side]
+            scratch = self.scratch if side == 0 else self.nccl_scratch1
+            native.set_device(self.device)  # ranks of one process may sit on different GPUs
+            native.check(lib.m4d_partition_owner_coarse(
+                self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.sendbuf[side].ptr,
+                self.rank_bounds[side].ptr, scratch.ptr, self.scratch_bytes, st.handle))
+            self.launches += lib.m4d_partition_launches(P * C)
+            b = self._read_bounds(self.rank_bounds[side], P * C, st)  # the send buffer is complete
+            self._tp(f"owner{side}_done", st)
+            rel = [b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)]
+            table = [struct.unpack(f"<{P * (C + 1)}q", blob) for blob in
+                     await allgather(t, struct.pack(f"<{P * (C + 1)}q", *rel), EXCHANGE_TAG + 2 + side)]
+            runs_in = [table[src][me * (C + 1):(me + 1) * (C + 1)] for src in range(P)]
+            incoming = [r[C] for r in runs_in]
+            total = sum(incoming)
+            if total > self.recv[side].capacity:
+                self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096)
+            if total > self.parted[side].capacity:
+                self.parted[side] = _Pairs(self.device, int(total * 1.1) + 4096)
+            send_t = _torch_bytes(self.sendbuf[side].ptr, max(1, b[P * C] * 16), self.device)
+            recv_t = _torch_bytes(self.recv[side].ptr, max(1, total * 16), self.device)
+            with torch.cuda.stream(torch.cuda.ExternalStream(st.handle, device=torch.device("cuda", self.device))):
+                dist.all_to_all_single(recv_t, send_t, [r * 16 for r in incoming],
+                                       [(b[(d + 1) * C] - b[d * C]) * 16 for d in range(P)])
+            self.a2a_done[side].record(st)
+            self._tp(f"a2a{side}_end", st)
+            runs.append(runs_in)
+        for side in range(2):
+            self.a2a_done[side].wait_on(self.split_streams[side])
+            self._tp(f"split{side}_start", self.split_streams[side])
+            out.append(self._finish_side(side, runs[side], C, self.split_streams[side]))
+            self._tp(f"split{side}_end", self.split_streams[side])
+            self.split_done[side].record(self.split_streams[side])
+            self.split_done[side].wait_on(self.stream)
+        return out
+
     def close(self) -> None:
         """Unmap the peers' receive buffers (push shuffle)."""
         for base in self._imported:
@@ -420,9 +492,12 @@ class KeyMerge:
         self._trace_points = []
         self._tp("step_start")
         if self.world > 1:
-            got = await self._push_shuffle_and_partition() if self.shuffle == "push" else None
-            if got is None and self.shuffle == "push":
-                self.close()  # the pull path may grow the receive buffers: map them again next step
+            if self.shuffle == "nccl":
+                got = await self._nccl_shuffle_and_partition()
+            else:
+                got = await self._push_shuffle_and_partition() if self.shuffle == "push" else None
+                if got is None and self.shuffle == "push":
+                    self.close()  # the pull path may grow the receive buffers: map them again next step
             self.received = got if got is not None else await self._shuffle_and_partition()
         else:
             # The two sides partition concurrently on two streams: each pass is
