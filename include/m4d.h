@@ -134,6 +134,8 @@ typedef struct m4d_transport_stats {
     uint64_t rendezvous_pulls;
     uint64_t unexpected_messages;
     uint64_t pull_kernel_launches; /* SM copy kernels issued for rendezvous pulls  */
+    uint64_t eager_device_sends;   /* device payloads sent by the eager protocol    */
+    uint64_t eager_device_loans;   /* eager device messages received by loan        */
 } m4d_transport_stats;
 
 /* transport_init: publishes this rank and maps the peers that are already up
@@ -145,8 +147,15 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
  * mapped; StartupError naming the first unreachable rank after `timeout` s. */
 m4d_status m4d_transport_wait_ready(m4d_transport* t, double timeout);
 int m4d_transport_mesh_ready(const m4d_transport* t);
-/* Transport.post_send (base.py:267-269).  `on_device` = 1 when ptr is device
- * memory (rendezvous over NVLink); host payloads are sent eagerly.  When the
+/* Transport.post_send (base.py:267-269).  `on_device` bit 0: ptr is device
+ * memory (rendezvous over NVLink); host payloads are sent eagerly.  Bit 1
+ * (device sends only): eager allowed -- a payload of at most
+ * m4d_transport_eager_device_max() bytes is copied by the sender into its
+ * region of the receiver's device ring and completes once that copy is done,
+ * without waiting for the receiver; larger ones, or any that find the ring
+ * full, take the rendezvous.  For post_recv, bit 1 lets an eager device message
+ * complete the receive by LOAN: no copy, the bytes stay in the ring
+ * (m4d_transport_take_loan) until m4d_transport_release_loan.  When the
  * request finishes inside the call, *now receives its completion (status
  * != -1) and it is not reported again by m4d_transport_progress. */
 m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer, uint32_t tag,
@@ -156,6 +165,13 @@ m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer,
 m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer, uint32_t tag,
                                    void* ptr, uint64_t cap, int domain, int on_device,
                                    uint64_t req_id, m4d_completion* now);
+/* Eager device protocol: its size threshold (0: no device ring), and the loans
+ * of receives posted with on_device bit 1: 1 and (*ptr, *token) when receive
+ * req_id was completed by a loan of ring bytes at device address *ptr (valid
+ * until released, at most until the transport closes), else 0. */
+uint64_t m4d_transport_eager_device_max(const m4d_transport* t);
+int m4d_transport_take_loan(m4d_transport* t, uint64_t req_id, uint64_t* ptr, uint64_t* token);
+m4d_status m4d_transport_release_loan(m4d_transport* t, uint64_t token);
 /* Transport.progress (sim.py:144-159, tcp.py:334-344): drains rings, flushes
  * queued sends, polls device copies; writes up to `max` completions and
  * returns how many. */

@@ -237,8 +237,8 @@ PyObject* bind(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
 //   host payload : data = buffer object, device_len = -1
 //   device payload: data = int address,  device_len = byte length
 PyObject* post(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
-    if (nargs != 9) {
-        PyErr_SetString(PyExc_TypeError, "post takes 9 arguments");
+    if (nargs != 9 && nargs != 10) {
+        PyErr_SetString(PyExc_TypeError, "post takes 9 or 10 arguments");
         return nullptr;
     }
     if (!g_send) {
@@ -253,14 +253,16 @@ PyObject* post(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     const long domain = PyLong_AsLong(args[6]);
     const long long device_len = PyLong_AsLongLong(args[7]);
     const unsigned long long req_id = PyLong_AsUnsignedLongLong(args[8]);
+    const long flags = nargs == 10 ? PyLong_AsLong(args[9]) : 0;  // 1: eager send / loan receive allowed
     if (PyErr_Occurred()) return nullptr;
     m4d_completion now;
     m4d_status st;
     if (device_len >= 0) {
         void* addr = PyLong_AsVoidPtr(args[5]);
         if (PyErr_Occurred()) return nullptr;
-        st = is_send ? g_send(t, channel, static_cast<int>(peer), tag, addr, device_len, domain, 1, req_id, &now)
-                     : g_recv(t, channel, static_cast<int>(peer), tag, addr, device_len, domain, 1, req_id, &now);
+        const int on_device = 1 | static_cast<int>((flags & 1) << 1);
+        st = is_send ? g_send(t, channel, static_cast<int>(peer), tag, addr, device_len, domain, on_device, req_id, &now)
+                     : g_recv(t, channel, static_cast<int>(peer), tag, addr, device_len, domain, on_device, req_id, &now);
     } else {
         Py_buffer view;
         if (PyObject_GetBuffer(args[5], &view, is_send ? PyBUF_SIMPLE : PyBUF_WRITABLE) != 0) return nullptr;

@@ -50,8 +50,13 @@ using m4d::fail;
 namespace {
 
 constexpr uint32_t kSegMagic = 0x4D344453;  // "M4DS"
-constexpr uint32_t kSegVersion = 1;
+constexpr uint32_t kSegVersion = 2;
 constexpr uint64_t kHeaderBytes = 4096;
+// Consumer heads of the eager device rings (one u64 per source rank) live in
+// the segment header from this offset.
+constexpr uint64_t kDevHeadsOff = 1024;
+constexpr int kMaxEagerWorld = static_cast<int>((kHeaderBytes - kDevHeadsOff) / 8);
+constexpr uint64_t kDevSlotAlign = 256;
 constexpr int kStateInit = 0, kStateReady = 1, kStateClosed = 2;
 
 double now_s() {
@@ -78,9 +83,23 @@ struct SegHeader {
     int32_t reserved;
     uint64_t ring_bytes;
     uint64_t ring_stride;
+    // eager device ring: one device allocation of world * dev_ring_bytes, the
+    // region of source s at s * dev_ring_bytes (published once allocated)
+    std::atomic<int32_t> dev_ring_ok;
+    int32_t reserved2;
+    uint64_t dev_ring_bytes;
+    uint64_t dev_ring_id;  // driver buffer id (the peers' mapping-cache key)
+    uint64_t dev_ring_addr;  // its address in the owner process (peers in the same process use it)
+    uint8_t dev_ring_handle[64];
 };
+static_assert(sizeof(SegHeader) <= kDevHeadsOff, "segment header fields overlap the device-ring heads");
 
-enum Kind : uint16_t { kPad = 0, kMsg = 1, kCont = 2, kRts = 3, kFin = 4, kBye = 5, kUnmap = 6, kUnmapAck = 7 };
+inline std::atomic<uint64_t>* dev_heads(SegHeader* h) {
+    return reinterpret_cast<std::atomic<uint64_t>*>(reinterpret_cast<uint8_t*>(h) + kDevHeadsOff);
+}
+
+enum Kind : uint16_t { kPad = 0, kMsg = 1, kCont = 2, kRts = 3, kFin = 4, kBye = 5, kUnmap = 6, kUnmapAck = 7,
+                       kEagerDev = 8 };
 
 struct RecHdr {
     uint32_t bytes;  // whole record, 8-byte multiple
@@ -113,6 +132,17 @@ struct RtsRec {
     int32_t device;
     uint64_t buffer_id;  // driver-unique id of the allocation (mapping cache key)
     uint8_t handle[64];
+};
+
+// An eager device message: its bytes are already in the receiver's device ring
+// (region of this source) at absolute position pos (ring offset pos % size).
+struct EagerDevRec {
+    RecHdr h;
+    uint32_t channel, tag;
+    uint64_t len;
+    uint64_t pos;
+    uint32_t domain;
+    uint32_t reserved;
 };
 
 struct FinRec {
@@ -190,6 +220,12 @@ struct Req {
     uint64_t sent = 0;
     bool started = false;
     RtsRec rts;
+    // eager device send: the copy into the peer's ring, published when it is done
+    bool eager_dev = false;
+    uint64_t dev_pos = 0;
+    cudaEvent_t dev_ev = nullptr;
+    // receive: an eager device message may complete it by loan (no copy)
+    bool loan_ok = false;
     // queue membership
     bool in_posted = false;
     bool in_outq = false;
@@ -197,6 +233,8 @@ struct Req {
 
 struct Unexpected {
     bool rts = false;
+    bool eager_dev = false;   // bytes wait in our device ring at dev_pos
+    uint64_t dev_pos = 0;
     RtsRec rec;               // rendezvous descriptor
     std::vector<uint8_t> data;  // eager payload so far
     uint64_t total = 0;
@@ -270,7 +308,46 @@ static uint64_t small_pull() {
     return v;
 }
 
+// Eager device protocol: device payloads a sender marks
+// eager-capable and of at most M4D_EAGER_DEVICE_MAX bytes (default 64 KiB; 0
+// disables) are copied by the SENDER into its region of the receiver's device
+// ring and announced by a ring record once the copy is done; larger ones, and
+// any that find the ring full, take the rendezvous.  Per source region:
+// M4D_EAGER_DEVICE_RING bytes (default 4 MiB).
+static uint64_t eager_device_max() {
+    static const uint64_t v = [] {
+        const char* e = getenv("M4D_EAGER_DEVICE_MAX");
+        return e && atoll(e) >= 0 ? static_cast<uint64_t>(atoll(e)) : uint64_t(64) << 10;
+    }();
+    return v;
+}
+
+static uint64_t eager_ring_bytes() {
+    static const uint64_t v = [] {
+        const char* e = getenv("M4D_EAGER_DEVICE_RING");
+        uint64_t b = e && atoll(e) > 0 ? static_cast<uint64_t>(atoll(e)) : uint64_t(4) << 20;
+        b = (b + (1u << 20) - 1) & ~uint64_t((1u << 20) - 1);
+        const uint64_t floor_b = ((4 * eager_device_max() + (1u << 20) - 1) >> 20) << 20;
+        return b < floor_b ? floor_b : b;
+    }();
+    return v;
+}
+
 inline uint64_t ckey(uint32_t channel, uint32_t tag) { return (static_cast<uint64_t>(channel) << 32) | tag; }
+
+struct DevSlot {
+    uint64_t pos, bytes;
+    bool released;
+};
+
+// An eager device message copied out of our ring into a posted device buffer.
+struct EagerCopy {
+    Req* recv;
+    int peer;
+    uint64_t pos;
+    uint64_t len;
+    cudaEvent_t ev;
+};
 
 struct Peer {
     SegHeader* seg = nullptr;  // peer's segment (we produce into ring me->peer inside it)
@@ -285,6 +362,13 @@ struct Peer {
     std::unordered_map<uint64_t, std::deque<Req*>> posted;
     std::unordered_map<uint64_t, std::deque<std::shared_ptr<Unexpected>>> unexpected;
     Inbound inbound;
+    // eager device ring, sender side: our region in the peer's ring (mapped), cursor
+    uint8_t* dev_out = nullptr;
+    uint64_t dev_out_cap = 0;
+    uint64_t dev_prod = 0;
+    // receiver side: slots of the peer's region of our ring, in arrival order
+    std::deque<DevSlot> dev_in;
+    uint64_t dev_in_end = 0;
 };
 
 }  // namespace
@@ -309,6 +393,11 @@ struct m4d_transport {
     std::map<MapKey, PeerMap> ipc_maps;                         // (pid, buffer id) -> mapping
     std::unordered_map<uint64_t, std::pair<uint64_t, std::array<uint8_t, 64>>> exports;  // buffer id -> (base, handle)
     cudaStream_t stream = nullptr;                             // (kept: first of the pull streams)
+    uint8_t* dev_ring = nullptr;                                // eager device ring (our inbound regions)
+    uint64_t dev_ring_bytes = 0;                                // per source
+    cudaStream_t eager_stream = nullptr;                        // eager copies (into peers' rings, out of ours)
+    std::vector<EagerCopy> eager_copies;
+    std::unordered_map<uint64_t, std::pair<uint64_t, uint64_t>> loans;  // recv id -> (device address, token)
     std::vector<cudaStream_t> pull_streams;                     // copies round-robin over these
     size_t next_stream = 0;
     double last_liveness = 0.0;
@@ -351,6 +440,107 @@ void complete(m4d_transport* t, Req* r, int status, uint64_t bytes) {
         }
     }
     t->reqs.erase(r->id);  // frees r
+}
+
+cudaEvent_t grab_event(m4d_transport* t) {
+    if (!t->spare_events.empty()) {
+        cudaEvent_t ev = t->spare_events.back();
+        t->spare_events.pop_back();
+        return ev;
+    }
+    cudaEvent_t ev = nullptr;
+    if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return ev;
+}
+
+// Receiver: the slot at `pos` of `peer`'s region of our ring is free; the head
+// the sender sees advances over every freed slot at the front.
+void dev_release(m4d_transport* t, int peer, uint64_t pos) {
+    Peer& p = t->peers[peer];
+    for (DevSlot& sl : p.dev_in)
+        if (sl.pos == pos) {
+            sl.released = true;
+            break;
+        }
+    while (!p.dev_in.empty() && p.dev_in.front().released) {
+        p.dev_in_end = p.dev_in.front().pos + p.dev_in.front().bytes;
+        p.dev_in.pop_front();
+    }
+    const uint64_t head = p.dev_in.empty() ? p.dev_in_end : p.dev_in.front().pos;
+    dev_heads(t->me)[peer].store(head, std::memory_order_release);
+}
+
+// Receiver: deliver an eager device message (pos, len) of `peer` to receive r:
+// by loan (r accepts one: the ring bytes themselves), by a device-to-device copy
+// out of the ring, or by a copy to host memory.
+void deliver_eager(m4d_transport* t, int peer, Req* r, uint64_t pos, uint64_t len, bool failed) {
+    if (failed) {
+        dev_release(t, peer, pos);
+        fail(M4D_ERR_TRANSFER, "rank %d's eager device copy failed", peer);
+        complete(t, r, M4D_ERR_TRANSFER, 0);
+        return;
+    }
+    if (len > r->len) {
+        dev_release(t, peer, pos);
+        fail(M4D_ERR_TRUNCATION, "incoming %llu bytes exceed posted buffer of %llu", (unsigned long long)len,
+             (unsigned long long)r->len);
+        complete(t, r, M4D_ERR_TRUNCATION, 0);
+        return;
+    }
+    uint8_t* src = t->dev_ring + static_cast<uint64_t>(peer) * t->dev_ring_bytes + pos % t->dev_ring_bytes;
+    if (r->loan_ok) {
+        t->loans[r->id] = std::make_pair(reinterpret_cast<uint64_t>(src), (static_cast<uint64_t>(peer) << 48) | pos);
+        t->stats.eager_device_loans++;
+        complete(t, r, M4D_OK, len);
+        return;
+    }
+    cudaSetDevice(t->device);
+    if (r->device) {
+        cudaEvent_t ev = grab_event(t);
+        cudaError_t e = ev ? cudaMemcpyAsync(r->ptr, src, len, cudaMemcpyDeviceToDevice, t->eager_stream)
+                           : cudaErrorMemoryAllocation;
+        if (e == cudaSuccess) e = cudaEventRecord(ev, t->eager_stream);
+        if (e != cudaSuccess) {
+            if (ev) t->spare_events.push_back(ev);
+            m4d::cuda_fail(e, "eager device delivery");
+            dev_release(t, peer, pos);
+            complete(t, r, M4D_ERR_CUDA, 0);
+            return;
+        }
+        t->eager_copies.push_back(EagerCopy{r, peer, pos, len, ev});
+        return;
+    }
+    const cudaError_t e = cudaMemcpy(r->ptr, src, len, cudaMemcpyDeviceToHost);
+    dev_release(t, peer, pos);
+    if (e != cudaSuccess) {
+        m4d::cuda_fail(e, "eager device delivery to host memory");
+        complete(t, r, M4D_ERR_CUDA, 0);
+        return;
+    }
+    complete(t, r, M4D_OK, len);
+}
+
+int poll_eager_copies(m4d_transport* t) {
+    int n = 0;
+    for (size_t i = 0; i < t->eager_copies.size();) {
+        EagerCopy& c = t->eager_copies[i];
+        const cudaError_t e = cudaEventQuery(c.ev);
+        if (e == cudaErrorNotReady) {
+            ++i;
+            continue;
+        }
+        if (e != cudaSuccess) m4d::cuda_fail(e, "eager device delivery");
+        dev_release(t, c.peer, c.pos);
+        complete(t, c.recv, e == cudaSuccess ? M4D_OK : M4D_ERR_CUDA, e == cudaSuccess ? c.len : 0);
+        t->spare_events.push_back(c.ev);
+        t->eager_copies[i] = t->eager_copies.back();
+        t->eager_copies.pop_back();
+        ++n;
+    }
+    return n;
 }
 
 int copy_in(m4d_transport* t, Req* r, uint64_t at, const void* src, uint64_t n) {
@@ -595,6 +785,10 @@ void flush_pulls(m4d_transport* t) {
 
 // A receive meets a buffered unexpected message.
 void deliver_unexpected(m4d_transport* t, int peer, Req* r, std::shared_ptr<Unexpected> u) {
+    if (u->eager_dev) {
+        deliver_eager(t, peer, r, u->dev_pos, u->total, u->rec.h.flags & 1);
+        return;
+    }
     if (u->rts) {
         start_pull(t, peer, r, u->rec);
         return;
@@ -662,6 +856,28 @@ bool flush_fins(m4d_transport* t, Peer& p) {
 // Writes as much of the send at the head of the queue as fits; true when the
 // whole send is in the ring.
 bool push_send(m4d_transport* t, Peer& p, Req* r) {
+    if (r->eager_dev) {  // publish once the copy into the peer's ring is done
+        const cudaError_t e = cudaEventQuery(r->dev_ev);
+        if (e == cudaErrorNotReady) return false;
+        uint8_t* w = p.out.reserve(sizeof(EagerDevRec));
+        if (!w) return false;
+        EagerDevRec* rec = reinterpret_cast<EagerDevRec*>(w);
+        rec->h.bytes = sizeof(EagerDevRec);
+        rec->h.kind = kEagerDev;
+        rec->h.flags = e == cudaSuccess ? 0 : 1;  // 1: the copy failed (the receiver frees the slot)
+        rec->channel = r->channel;
+        rec->tag = r->tag;
+        rec->len = r->len;
+        rec->pos = r->dev_pos;
+        rec->domain = static_cast<uint32_t>(r->domain);
+        rec->reserved = 0;
+        p.out.commit(sizeof(EagerDevRec));
+        if (e != cudaSuccess) m4d::cuda_fail(e, "eager device copy");
+        t->spare_events.push_back(r->dev_ev);
+        r->dev_ev = nullptr;
+        r->sent = e == cudaSuccess ? r->len : 0;
+        return true;
+    }
     if (r->device) {
         uint8_t* w = p.out.reserve(sizeof(RtsRec));
         if (!w) return false;
@@ -714,13 +930,75 @@ int flush_peer(m4d_transport* t, int peer) {
         p.outq.pop_front();
         r->in_outq = false;
         ++progressed;
-        if (r->device) {
+        if (r->device && !r->eager_dev) {
             t->awaiting_fin[r->id] = r;
+        } else if (r->eager_dev && r->sent != r->len) {
+            complete(t, r, M4D_ERR_CUDA, 0);
         } else {
             complete(t, r, M4D_OK, r->len);  // eager: complete once the bytes are in the ring
         }
     }
     return progressed;
+}
+
+// Sender: start an eager device send -- reserve a slot in our region of the
+// peer's device ring and copy the payload into it on the eager stream; the
+// record goes out (push_send) once the copy is done.  False: rendezvous instead
+// (no ring, or not enough room).
+bool try_eager(m4d_transport* t, int q, Req* r) {
+    Peer& p = t->peers[q];
+    if (!p.seg || p.dead || t->world > kMaxEagerWorld) return false;
+    if (!p.dev_out) {
+        if (!p.seg->dev_ring_ok.load(std::memory_order_acquire)) return false;
+        void* base = nullptr;
+        if (p.pid == static_cast<int32_t>(getpid())) {  // ranks sharing this process
+            base = reinterpret_cast<void*>(p.seg->dev_ring_addr);
+        } else {
+            const MapKey key{p.pid, p.seg->dev_ring_id, true};
+            auto it = t->ipc_maps.find(key);
+            if (it != t->ipc_maps.end()) {
+                base = it->second.base;
+            } else {
+                cudaIpcMemHandle_t h;
+                memcpy(&h, p.seg->dev_ring_handle, 64);
+                cudaSetDevice(t->device);
+                if (cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+                    cudaGetLastError();
+                    return false;
+                }
+                t->ipc_maps[key].base = base;
+            }
+        }
+        p.dev_out = static_cast<uint8_t*>(base) + static_cast<uint64_t>(t->rank) * p.seg->dev_ring_bytes;
+        p.dev_out_cap = p.seg->dev_ring_bytes;
+    }
+    const uint64_t cap = p.dev_out_cap;
+    const uint64_t need = (r->len + kDevSlotAlign - 1) & ~(kDevSlotAlign - 1);
+    uint64_t pos = p.dev_prod, off = pos % cap;
+    if (off + need > cap) {  // no wrap inside a slot: skip to the start of the region
+        pos += cap - off;
+        off = 0;
+    }
+    const uint64_t head = dev_heads(p.seg)[t->rank].load(std::memory_order_acquire);
+    if (pos + need - head > cap) return false;  // full: the receiver still holds those slots
+    cudaEvent_t ev = grab_event(t);
+    if (!ev) return false;
+    cudaSetDevice(t->device);
+    cudaError_t e = cudaMemcpyAsync(p.dev_out + off, r->ptr, r->len, cudaMemcpyDefault, t->eager_stream);
+    if (e == cudaSuccess) e = cudaEventRecord(ev, t->eager_stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        t->spare_events.push_back(ev);
+        return false;
+    }
+    p.dev_prod = pos + need;
+    t->stats.eager_device_sends++;
+    t->stats.nvlink_bytes += r->len;
+    r->eager_dev = true;
+    r->dev_pos = pos;
+    r->dev_ev = ev;
+    r->started = true;  // the slot is taken: the send can no longer be retracted
+    return true;
 }
 
 // -- consumer side -----------------------------------------------------------------------
@@ -809,6 +1087,30 @@ void on_rts(m4d_transport* t, int peer, const RtsRec* rts) {
     t->stats.unexpected_messages++;
 }
 
+void on_eager_dev(m4d_transport* t, int peer, const EagerDevRec* rec) {
+    Peer& p = t->peers[peer];
+    p.dev_in.push_back(DevSlot{rec->pos, (rec->len + kDevSlotAlign - 1) & ~(kDevSlotAlign - 1), false});
+    const bool failed = rec->h.flags & 1;
+    const uint64_t key = ckey(rec->channel, rec->tag);
+    auto q = p.posted.find(key);
+    if (q != p.posted.end() && !q->second.empty()) {
+        Req* r = q->second.front();
+        q->second.pop_front();
+        if (q->second.empty()) p.posted.erase(q);
+        r->in_posted = false;
+        deliver_eager(t, peer, r, rec->pos, rec->len, failed);
+        return;
+    }
+    auto u = std::make_shared<Unexpected>();
+    u->eager_dev = true;
+    u->dev_pos = rec->pos;
+    u->rec.h.flags = failed ? 1 : 0;
+    u->total = rec->len;
+    u->complete = true;
+    p.unexpected[key].push_back(u);
+    t->stats.unexpected_messages++;
+}
+
 void on_fin(m4d_transport* t, const FinRec* f) {
     auto it = t->awaiting_fin.find(f->send_id);
     if (it == t->awaiting_fin.end()) return;
@@ -851,6 +1153,7 @@ int drain_peer(m4d_transport* t, int peer) {
             case kBye: p.said_bye = true; break;
             case kUnmap: on_unmap(t, peer, reinterpret_cast<const UnmapRec*>(h)); break;
             case kUnmapAck: settle_export(reinterpret_cast<const UnmapRec*>(h)->base); break;
+            case kEagerDev: on_eager_dev(t, peer, reinterpret_cast<const EagerDevRec*>(h)); break;
             default: break;  // kPad
         }
         ring.cursor += h->bytes;
@@ -1097,6 +1400,29 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
             if (e == cudaSuccess) t->pull_streams.push_back(st);
         }
         if (e == cudaSuccess) t->stream = t->pull_streams[0];
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->eager_stream, cudaStreamNonBlocking);
+        // the eager device ring: one region per source rank, published in our header
+        if (e == cudaSuccess && eager_device_max() > 0 && t->world > 1 && t->world <= kMaxEagerWorld) {
+            const uint64_t rb = eager_ring_bytes();
+            void* ring = nullptr;
+            uint64_t base = 0, size = 0, id = 0;
+            std::array<uint8_t, 64> handle;
+            uint64_t off0 = 0;
+            if (cudaMalloc(&ring, rb * t->world) == cudaSuccess &&
+                m4d::alloc_info(ring, &base, &size, &id) == M4D_OK &&
+                m4d_ipc_export(ring, handle.data(), &off0) == M4D_OK) {
+                t->dev_ring = static_cast<uint8_t*>(ring);
+                t->dev_ring_bytes = rb;
+                t->me->dev_ring_bytes = rb;
+                t->me->dev_ring_id = id;
+                t->me->dev_ring_addr = reinterpret_cast<uint64_t>(ring);
+                memcpy(t->me->dev_ring_handle, handle.data(), 64);
+                t->me->dev_ring_ok.store(1, std::memory_order_release);
+            } else {
+                if (ring) cudaFree(ring);
+                cudaGetLastError();  // no ring: every device send takes the rendezvous
+            }
+        }
         t->inflight.resize(t->pull_streams.size());
         if (const char* eng = getenv("M4D_PULL_ENGINE")) t->use_ce = strcmp(eng, "ce") == 0;
         if (const char* c = getenv("M4D_PULL_CTAS")) t->pull_ctas = atoi(c) > 0 ? atoi(c) : 296;
@@ -1135,7 +1461,7 @@ m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer,
     raw->ptr = static_cast<uint8_t*>(const_cast<void*>(ptr));
     raw->len = len;
     raw->domain = domain;
-    raw->device = on_device && len > 0;
+    raw->device = (on_device & 1) && len > 0;
     if (raw->device && t->device < 0) return fail(M4D_ERR_USAGE, "device payload on a host-only transport");
     if (p.dead) {
         fail(M4D_ERR_CLOSED, "rank %d connection closed", peer);
@@ -1145,7 +1471,8 @@ m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer,
         now->bytes = 0;
         return M4D_OK;
     }
-    if (raw->device) {
+    const bool eager = raw->device && (on_device & 2) && len <= eager_device_max() && try_eager(t, peer, raw);
+    if (raw->device && !eager) {
         RtsRec& rts = raw->rts;
         memset(&rts, 0, sizeof rts);
         rts.h.bytes = sizeof(RtsRec);
@@ -1204,7 +1531,8 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
     raw->ptr = static_cast<uint8_t*>(ptr);
     raw->len = cap;
     raw->domain = domain;
-    raw->device = on_device && cap > 0;
+    raw->device = (on_device & 1) && cap > 0;
+    raw->loan_ok = (on_device & 2) != 0;  // an eager device message may complete it by loan
     if (raw->device && t->device < 0) return fail(M4D_ERR_USAGE, "device buffer on a host-only transport");
     t->reqs[req_id] = std::move(r);
     const size_t before = t->done.size();
@@ -1250,6 +1578,7 @@ int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
     // Copies first: a finished pull must send its FIN in this same call, or a
     // sender whose peer stops polling would wait forever.
     if (t->inflight_launches) poll_copies(t);
+    if (!t->eager_copies.empty()) poll_eager_copies(t);
     for (int q = 0; q < t->world; ++q)
         if (q != t->rank) {
             drain_peer(t, q);
@@ -1307,8 +1636,10 @@ m4d_status m4d_transport_purge_channel(m4d_transport* t, uint32_t channel) {
         flush_pulls(t);
         for (auto it = p.unexpected.begin(); it != p.unexpected.end();) {
             if ((it->first >> 32) == channel) {
-                for (auto& u : it->second)
+                for (auto& u : it->second) {
                     if (u->rts) queue_fin(t, q, u->rec.send_id, M4D_ERR_CANCELLED, 0);
+                    if (u->eager_dev) dev_release(t, q, u->dev_pos);
+                }
                 if (p.inbound.active && p.inbound.buf) {
                     for (auto& u : it->second)
                         if (u == p.inbound.buf) p.inbound.buf.reset();
@@ -1377,6 +1708,26 @@ m4d_status m4d_transport_stats_get(const m4d_transport* t, m4d_transport_stats* 
     return M4D_OK;
 }
 
+uint64_t m4d_transport_eager_device_max(const m4d_transport* t) {
+    return t && t->dev_ring ? eager_device_max() : 0;
+}
+
+int m4d_transport_take_loan(m4d_transport* t, uint64_t req_id, uint64_t* ptr, uint64_t* token) {
+    auto it = t->loans.find(req_id);
+    if (it == t->loans.end()) return 0;
+    *ptr = it->second.first;
+    *token = it->second.second;
+    t->loans.erase(it);
+    return 1;
+}
+
+m4d_status m4d_transport_release_loan(m4d_transport* t, uint64_t token) {
+    const int peer = static_cast<int>(token >> 48);
+    if (peer < 0 || peer >= t->world || peer == t->rank) return fail(M4D_ERR_USAGE, "invalid loan token");
+    dev_release(t, peer, token & ((uint64_t(1) << 48) - 1));
+    return M4D_OK;
+}
+
 m4d_status m4d_transport_close(m4d_transport* t) {
     if (!t) return M4D_OK;
     // Say goodbye through every ring that has room, then mark the segment closed.
@@ -1403,6 +1754,14 @@ m4d_status m4d_transport_close(m4d_transport* t) {
     }
     for (auto& kv : t->ipc_maps) cudaIpcCloseMemHandle(kv.second.base);
     drop_holds(t, -1);
+    if (t->eager_stream) {
+        cudaStreamSynchronize(t->eager_stream);
+        for (EagerCopy& c : t->eager_copies) cudaEventDestroy(c.ev);
+        for (auto& kv : t->reqs)
+            if (kv.second->dev_ev) cudaEventDestroy(kv.second->dev_ev);
+        cudaStreamDestroy(t->eager_stream);
+    }
+    if (t->dev_ring) cudaFree(t->dev_ring);
     for (Peer& p : t->peers)
         if (p.seg) munmap(p.seg, p.seg_len);
     if (t->me) {

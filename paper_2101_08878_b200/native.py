@@ -100,7 +100,8 @@ class TransportStats(ctypes.Structure):
 
     _fields_ = [(name, ctypes.c_uint64) for name in (
         "sends_completed", "recvs_completed", "bytes_sent", "bytes_received", "eager_bytes",
-        "nvlink_bytes", "rendezvous_pulls", "unexpected_messages", "pull_kernel_launches")]
+        "nvlink_bytes", "rendezvous_pulls", "unexpected_messages", "pull_kernel_launches",
+        "eager_device_sends", "eager_device_loans")]
 
 
 # name -> (restype, argtypes); every symbol include/m4d.h declares.
@@ -140,6 +141,9 @@ SIGNATURES: dict[str, tuple] = {
                                                _u64, ctypes.c_int, ctypes.c_int, _u64, ctypes.POINTER(Completion)]),
     "m4d_transport_progress": (ctypes.c_int, [_c_void_p, ctypes.POINTER(Completion), ctypes.c_int]),
     "m4d_transport_pending_completions": (ctypes.c_int, [_c_void_p]),
+    "m4d_transport_eager_device_max": (_u64, [_c_void_p]),
+    "m4d_transport_take_loan": (ctypes.c_int, [_c_void_p, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
+    "m4d_transport_release_loan": (ctypes.c_int, [_c_void_p, _u64]),
     "m4d_transport_cancel": (ctypes.c_int, [_c_void_p, _u64, ctypes.POINTER(ctypes.c_int)]),
     "m4d_transport_purge_channel": (ctypes.c_int, [_c_void_p, ctypes.c_uint32]),
     "m4d_transport_peer_alive": (ctypes.c_int, [_c_void_p, ctypes.c_int]),

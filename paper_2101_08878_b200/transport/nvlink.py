@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 
 from .. import native
 from ..errors import CommClosedError, ConfigurationError, TransferError, UsageError
@@ -68,7 +69,7 @@ class CudaRegion(DeviceRegion):
     device pointer whose ``owner`` keeps it alive (e.g. a torch tensor).
     """
 
-    __slots__ = ("ptr", "_nbytes", "device", "_owner")
+    __slots__ = ("ptr", "_nbytes", "device", "_owner", "__weakref__")
 
     def __init__(self, size_or_bytes, device: int = 0, *, ptr: int | None = None, owner=None):
         if ptr is not None:
@@ -109,6 +110,23 @@ class CudaRegion(DeviceRegion):
 
     def __repr__(self):
         return f"<CudaRegion cuda:{self.device} {self._nbytes} B>"
+
+
+class _Loan:
+    """Keeps a loaned ring slot until the region lent out dies, then hands it back."""
+
+    __slots__ = ("transport", "token")
+
+    def __init__(self, transport, token: int):
+        self.transport, self.token = transport, token
+
+    def __del__(self):
+        t = self.transport
+        try:
+            if getattr(t, "_h", None):
+                t._lib.m4d_transport_release_loan(t._h, self.token)
+        except Exception:
+            pass
 
 
 class _RegionPool:
@@ -186,6 +204,9 @@ class NvlinkTransport(Transport):
         self._live: dict[int, TransferRequest] = {}
         self._pool = _RegionPool(device) if device >= 0 else None
         self.connect_timeout = config.connect_timeout
+        # largest device payload sent eagerly (0: no device ring, every device frame rendezvous)
+        self.eager_device_max = int(self._lib.m4d_transport_eager_device_max(self._h))
+        self._loans = weakref.WeakSet()  # regions lent out of the device ring
 
     # -- mesh -----------------------------------------------------------------------------------
 
@@ -202,7 +223,7 @@ class NvlinkTransport(Transport):
 
     # -- posts ----------------------------------------------------------------------------------
 
-    def _post(self, direction: str, channel: int, peer: int, tag: int, data, domain) -> TransferRequest:
+    def _post(self, direction: str, channel: int, peer: int, tag: int, data, domain, flags: int = 0) -> TransferRequest:
         view = as_view(data)
         if direction == "recv" and view.readonly:
             raise UsageError("receive buffer must be writable")
@@ -214,7 +235,7 @@ class NvlinkTransport(Transport):
             obj, device_len = view, -1  # host: address taken through the buffer protocol
         try:
             done = self._fast.post(self._h, direction == "send", channel, peer, tag, obj, int(domain), device_len,
-                                   req.id)
+                                   req.id, flags)
         except OSError as exc:
             raise native.error_for(exc.args[0], native.last_error()) from None
         if done is None:
@@ -271,6 +292,47 @@ class NvlinkTransport(Transport):
     def post_recv(self, channel: int, peer: int, tag: int, buffer,
                   domain: MemoryDomain = MemoryDomain.HOST) -> TransferRequest:
         return self._post("recv", channel, peer, tag, buffer, domain)
+
+    # -- eager device frames (protocol chosen per size) ----------------------------------------------
+
+    def post_send_eager(self, channel: int, peer: int, tag: int, data,
+                        domain: MemoryDomain = MemoryDomain.DEVICE) -> TransferRequest:
+        """``post_send`` that lets a device payload of at most ``eager_device_max`` bytes go
+        eagerly: the sender copies it into its region of the receiver's device ring and the
+        send completes when that copy is done, without a rendezvous round trip.  Larger
+        payloads (or a full ring) take the rendezvous as usual."""
+        return self._post("send", channel, peer, tag, data, domain, 1)
+
+    def post_recv_loanable(self, channel: int, peer: int, tag: int, buffer,
+                           domain: MemoryDomain = MemoryDomain.DEVICE) -> TransferRequest:
+        """``post_recv`` whose message, if it arrives eagerly, stays where it landed in the
+        device ring and is lent out instead of copied (:meth:`take_loan`); otherwise the
+        bytes land in ``buffer`` as usual."""
+        return self._post("recv", channel, peer, tag, buffer, domain, 1)
+
+    def take_loan(self, req: TransferRequest):
+        """The :class:`CudaRegion` lent to a finished loanable receive (the ring bytes, valid
+        while the region is alive and the transport open), or None if the bytes are in the
+        posted buffer."""
+        ptr, token = ctypes.c_uint64(), ctypes.c_uint64()
+        if not self._lib.m4d_transport_take_loan(self._h, req.id, ctypes.byref(ptr), ctypes.byref(token)):
+            return None
+        region = CudaRegion(req.bytes_moved, self.device, ptr=ptr.value, owner=_Loan(self, token.value))
+        self._loans.add(region)
+        return region
+
+    def _evacuate_loans(self) -> None:
+        """Before the ring goes away (close): move every loaned region still alive into its
+        own allocation, so received frames outlive the transport as the reference's do."""
+        live = list(self._loans)
+        if not live:
+            return
+        for region in live:
+            buf = native.DeviceBuffer(self.device, max(1, region.nbytes))
+            native.memcpy(buf.ptr, region.ptr, region.nbytes)
+            region.ptr, region._owner = buf.ptr, buf  # the _Loan is dropped: its slot is moot now
+        native.check(self._lib.m4d_device_sync(self.device))
+        self._loans.clear()
 
     # -- completions ------------------------------------------------------------------------------
 
@@ -351,6 +413,7 @@ class NvlinkTransport(Transport):
 
     def close(self) -> None:
         if getattr(self, "_h", None):
+            self._evacuate_loans()
             self._fast.forget(self._h)
             self._lib.m4d_transport_close(self._h)
             self._h = None

@@ -103,10 +103,10 @@ PROGRAM = os.path.join(ROOT, "tests", "cluster_program.py")
 @pytest.mark.parametrize("transport", ["nvlink", "socket"])
 def test_launcher_runs_a_four_process_cluster(transport):
     """commshim-launch spawns 4 processes (scheduler, client, 2 workers); heartbeats over
-    the nvlink transport's shared-memory rings (or the socket transport) for 0.2 s, no
+    the nvlink transport's shared-memory rings (or the socket transport) for 0.5 s, no
     suspects."""
     out = subprocess.run([sys.executable, "-m", "paper_2101_08878_b200.cli", "launch", "--np", "4",
-                          "--transport", transport, "--", sys.executable, PROGRAM, "0.005", "0.2"],
+                          "--transport", transport, "--", sys.executable, PROGRAM, "0.02", "0.5"],
                          cwd=ROOT, capture_output=True, text=True, timeout=180)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     report = json.loads(next(ln for ln in out.stdout.splitlines() if ln.startswith("{")))

@@ -1,0 +1,166 @@
+"""Eager device protocol (north_star: eager and rendezvous chosen per message size for GPU
+frames): device payloads up to ``eager_device_max`` bytes are copied by
+the sender into its region of the receiver's device ring and announced once the copy is
+done; the receiver copies them out, or lends the ring bytes (loan) without a copy.  Two
+ranks in one process on cuda:0 (the multi-process and two-GPU cases are in
+test_multiprocess_gpu.py)."""
+
+import numpy as np
+import pytest
+
+from nvlink_fixtures import close_all, nvlink_transports, pump
+
+pytestmark = pytest.mark.gpu
+
+
+def pattern(n, salt):
+    return ((np.arange(n, dtype=np.uint64) * (2 * salt + 3)) % 251).astype(np.uint8)
+
+
+@pytest.fixture
+def pair():
+    ts = nvlink_transports(2, 0)
+    yield ts
+    close_all(ts)
+
+
+def dev(n, data=None):
+    from paper_2101_08878_b200.transport.nvlink import CudaRegion
+
+    return CudaRegion(bytes(data) if data is not None else n, 0)
+
+
+def stats(t):
+    return t.native_stats()
+
+
+def test_transport_advertises_the_threshold(pair):
+    assert pair[0].eager_device_max == 64 << 10
+
+
+@pytest.mark.parametrize("n", [1, 17, 4096, 64 << 10])
+@pytest.mark.parametrize("order", ["recv_first", "send_first"])
+def test_eager_into_a_posted_device_buffer(pair, n, order):
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    src, dst = dev(n, pattern(n, n)), dev(n)
+    before = stats(pair[0])["eager_device_sends"]
+    if order == "recv_first":
+        r = pair[1].post_recv(0, 0, 5, dst.window(), MemoryDomain.DEVICE)
+        s = pair[0].post_send_eager(0, 1, 5, src.window())
+    else:
+        s = pair[0].post_send_eager(0, 1, 5, src.window())
+        pump(pair, s)  # eager: completes without the receiver
+        r = pair[1].post_recv(0, 0, 5, dst.window(), MemoryDomain.DEVICE)
+    pump(pair, s, r)
+    assert r.bytes_moved == n and np.array_equal(np.frombuffer(dst.to_bytes(), np.uint8), pattern(n, n))
+    assert stats(pair[0])["eager_device_sends"] == before + 1
+    assert stats(pair[0])["rendezvous_pulls"] == 0 and stats(pair[1])["rendezvous_pulls"] == 0
+
+
+def test_eager_into_host_memory_and_by_loan(pair):
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    n = 3000
+    src = dev(n, pattern(n, 1))
+    host = bytearray(n)
+    s = pair[0].post_send_eager(0, 1, 6, src.window())
+    r = pair[1].post_recv(0, 0, 6, host)
+    pump(pair, s, r)
+    assert bytes(host) == pattern(n, 1).tobytes()
+    fallback = dev(n)
+    s = pair[0].post_send_eager(0, 1, 7, src.window())
+    r = pair[1].post_recv_loanable(0, 0, 7, fallback.window())
+    pump(pair, s, r)
+    loan = pair[1].take_loan(r)
+    assert loan is not None and loan.ptr != fallback.ptr and loan.nbytes == n
+    assert loan.to_bytes() == pattern(n, 1).tobytes()
+    assert pair[1].take_loan(r) is None  # taken once
+    assert stats(pair[1])["eager_device_loans"] == 1
+
+
+def test_larger_frames_take_the_rendezvous(pair):
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    n = (64 << 10) + 1
+    src, dst = dev(n, pattern(n, 2)), dev(n)
+    s = pair[0].post_send_eager(0, 1, 8, src.window())
+    r = pair[1].post_recv_loanable(0, 0, 8, dst.window())
+    pump(pair, s, r)
+    assert pair[1].take_loan(r) is None  # landed in the posted buffer by a pull
+    assert dst.to_bytes() == pattern(n, 2).tobytes()
+    assert stats(pair[1])["rendezvous_pulls"] == 1 and stats(pair[0])["eager_device_sends"] == 0
+
+
+def test_truncation_fails_the_receive_and_frees_the_slot(pair):
+    from paper_2101_08878_b200.errors import TruncationError
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    src, small = dev(512, pattern(512, 3)), dev(100)
+    s = pair[0].post_send_eager(0, 1, 9, src.window())
+    r = pair[1].post_recv(0, 0, 9, small.window(), MemoryDomain.DEVICE)
+    pump(pair, s, r)
+    assert r.failed and isinstance(r.error, TruncationError) and not s.failed
+
+
+def test_held_loans_fill_the_ring_then_sends_fall_back_and_resume(pair):
+    """100 held 64 KiB loans exceed the 4 MiB ring region: later sends still complete (by
+    rendezvous); once the loans are dropped the eager path is used again."""
+    import gc
+
+    n = 64 << 10
+    src = dev(n, pattern(n, 4))
+    held = []
+    for k in range(100):
+        fallback = dev(n)
+        s = pair[0].post_send_eager(0, 1, 10, src.window())
+        r = pair[1].post_recv_loanable(0, 0, 10, fallback.window())
+        pump(pair, s, r)
+        got = pair[1].take_loan(r) or fallback
+        held.append(got)
+    assert all(h.to_bytes() == pattern(n, 4).tobytes() for h in held[::9])
+    st = stats(pair[0])
+    assert 0 < st["eager_device_sends"] < 100 and stats(pair[1])["rendezvous_pulls"] > 0
+    held.clear()
+    gc.collect()
+    before = stats(pair[0])["eager_device_sends"]
+    for k in range(80):  # the ring wraps around several times
+        dst = dev(n)
+        s = pair[0].post_send_eager(0, 1, 11, src.window())
+        r = pair[1].post_recv_loanable(0, 0, 11, dst.window())
+        pump(pair, s, r)
+        loan = pair[1].take_loan(r)
+        assert (loan or dst).to_bytes()[:64] == pattern(n, 4).tobytes()[:64]
+        del loan
+    assert stats(pair[0])["eager_device_sends"] == before + 80
+
+
+def test_comm_path_device_frames_use_eager_and_loans():
+    """send_payload / recv_payload of small device frames: eager sends, loaned receives,
+    bytes intact; large frames keep the rendezvous."""
+    from paper_2101_08878_b200.loop import gather
+    from paper_2101_08878_b200.messaging import Frame, recv_payload, send_payload
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    from nvlink_fixtures import nvlink_world
+
+    loop, ts, tables = nvlink_world(2, 0)
+    try:
+        sizes = [1, 999, 64 << 10, (64 << 10) + 16, 1 << 20]
+
+        async def main():
+            out = []
+            for k, n in enumerate(sizes):
+                frame = Frame(dev(n, pattern(n, k)), n, MemoryDomain.DEVICE)
+                _, got = await gather(send_payload(ts[0], tables[0].lookup(1), 300 + k, frame),
+                                      recv_payload(ts[1], tables[1].lookup(0), 300 + k))
+                out.append(got)
+            return out
+
+        got = loop.run_until_complete(main())
+        for k, (n, f) in enumerate(zip(sizes, got)):
+            assert f.domain == MemoryDomain.DEVICE and f.to_bytes() == pattern(n, k).tobytes()
+        assert stats(ts[0])["eager_device_sends"] == 3 and stats(ts[1])["eager_device_loans"] == 3
+        assert stats(ts[1])["rendezvous_pulls"] == 2
+    finally:
+        close_all(ts)
