@@ -608,6 +608,9 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
     # the public comm path (send_payload / recv_payload, Listing 2/3) with device frames
     pp = {sz: p2p.pingpong(t, 1 - dist.rank, sz, 1000 if sz < (1 << 20) else 50, True)
           for sz in sorted({1, min(4 << 20, args.max_size), args.max_size})}
+    # the eager device protocol at the transport layer (eager send + loaned receive)
+    eager_lat = {sz: p2p.osu_latency(t, 1 - dist.rank, sz, 1000, True, eager=True)
+                 for sz in (1, 4096, 65536)} if getattr(t, "eager_device_max", 0) else {}
     # host frames (Dask control messages; the reference arm's frames): transport and comm path at 1 B
     host_lat = p2p.osu_latency(t, 1 - dist.rank, 1, 2000, False)
     host_pp = p2p.pingpong(t, 1 - dist.rank, 1, 2000, False)
@@ -632,6 +635,7 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
         "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
         "config": {"workload": "p2p", "sizes": [r["size"] for r in rows], "window": 64},
         "latency_1B_us": rows[0]["osu_latency_us"], "sweep": rows,
+        "device_eager_latency_us": {str(k): v for k, v in eager_lat.items()},
         "host_frames_1B": {"osu_latency_us": host_lat,
                            "comm_path_latency_us": host_pp["mean_s"] * 1e6 if host_pp else None},
         "comm_path": {str(k): {"latency_us": v["mean_s"] * 1e6, "GBps": v["throughput_Bps"] / 1e9}

@@ -130,7 +130,7 @@ typedef struct m4d_completion {
 typedef struct m4d_transport_stats {
     uint64_t sends_completed, recvs_completed, bytes_sent, bytes_received;
     uint64_t eager_bytes;       /* host payload bytes written into rings         */
-    uint64_t nvlink_bytes;      /* device payload bytes pulled peer-to-peer      */
+    uint64_t nvlink_bytes;      /* device payload bytes received peer-to-peer    */
     uint64_t rendezvous_pulls;
     uint64_t unexpected_messages;
     uint64_t pull_kernel_launches; /* SM copy kernels issued for rendezvous pulls  */

@@ -993,7 +993,6 @@ bool try_eager(m4d_transport* t, int q, Req* r) {
     }
     p.dev_prod = pos + need;
     t->stats.eager_device_sends++;
-    t->stats.nvlink_bytes += r->len;
     r->eager_dev = true;
     r->dev_pos = pos;
     r->dev_ev = ev;
@@ -1091,6 +1090,7 @@ void on_eager_dev(m4d_transport* t, int peer, const EagerDevRec* rec) {
     Peer& p = t->peers[peer];
     p.dev_in.push_back(DevSlot{rec->pos, (rec->len + kDevSlotAlign - 1) & ~(kDevSlotAlign - 1), false});
     const bool failed = rec->h.flags & 1;
+    if (!failed) t->stats.nvlink_bytes += rec->len;  // device bytes that reached this rank (as for pulls)
     const uint64_t key = ckey(rec->channel, rec->tag);
     auto q = p.posted.find(key);
     if (q != p.posted.end() && !q->second.empty()) {

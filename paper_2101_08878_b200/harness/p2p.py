@@ -120,24 +120,35 @@ def osu_bw(transport: Transport, peer: int, n: int, window: int, iters: int, dev
     return n * window * iters / elapsed / 1e9
 
 
-def osu_latency(transport: Transport, peer: int, n: int, iters: int, device: bool) -> float:
-    """Transport-layer one-way latency in microseconds (raw posts, RTT / 2)."""
+def osu_latency(transport: Transport, peer: int, n: int, iters: int, device: bool, eager: bool = False) -> float:
+    """Transport-layer one-way latency in microseconds (raw posts, RTT / 2).  ``eager``
+    (device frames): eager sends and loanable receives (the protocol the messaging layer
+    uses for small device frames) instead of plain posts (rendezvous)."""
     me = transport.rank
     dom = MemoryDomain.DEVICE if device else MemoryDomain.HOST
     sbuf = _region(transport, pattern(n), device)
     rbuf = _region(transport, bytes(n), device)
     sv, rv = _window(sbuf, device, n), _window(rbuf, device, n)
+    send = transport.post_send_eager if eager else transport.post_send
+    recv = transport.post_recv_loanable if eager else transport.post_recv
+
+    def receive():
+        req = recv(0, peer, PP_TAG, rv, dom)
+        _wait(transport, req)
+        if eager:
+            transport.take_loan(req)  # dropped at once: the ring slot goes back
+
     warm = max(10, iters // 10)
     start = None
     for it in range(iters + warm):
         if it == warm:
             start = time.perf_counter()
         if me == 0:
-            _wait(transport, transport.post_send(0, peer, PP_TAG, sv, dom))
-            _wait(transport, transport.post_recv(0, peer, PP_TAG, rv, dom))
+            _wait(transport, send(0, peer, PP_TAG, sv, dom))
+            receive()
         else:
-            _wait(transport, transport.post_recv(0, peer, PP_TAG, rv, dom))
-            _wait(transport, transport.post_send(0, peer, PP_TAG, sv, dom))
+            receive()
+            _wait(transport, send(0, peer, PP_TAG, sv, dom))
     return (time.perf_counter() - start) / iters / 2 * 1e6
 
 
