@@ -15,8 +15,9 @@ nothing: the array is fixed, so ``scaling`` is "strong".
 * ``roofline``: the fused kernel's algorithmic bytes / its event-timed
   duration against MEASURED_PEAKS.json (HBM) or the measured 770 GB/s peer
   copy (NVLink), whichever bounds it.
-* ``cpu_baseline``: the oracle (oracle/liboracle.so) on a bounded sample of
-  block pairs with x resident in host memory, all host threads.
+* ``cpu_baseline``: the oracle (oracle/liboracle.so) over the full array with x
+  resident in host memory, all host threads; its block sums are also the
+  full-size parity check of every block and of the checksum.
 
 ``--impl reference`` times the CPU restatement of the path (the reference has
 no operator code) on the same config; under torchrun only
@@ -226,34 +227,32 @@ def emit(line: dict) -> None:
 # -- transpose_sum -------------------------------------------------------------------------------
 
 
-def ts_cpu_sample(n: int, b: int, pairs: int, threads: int, min_seconds: float = 10.0) -> dict:
-    """Oracle (C restatement) on `pairs` output blocks with x resident in host memory,
-    repeated until at least `min_seconds` of CPU work has been timed."""
-    import numpy as np
-
+def ts_cpu_full(n: int, b: int, threads: int, min_seconds: float = 10.0) -> dict:
+    """The oracle (C restatement, all host threads) over the FULL array with x resident in
+    host memory (generated outside the timing, as the GPU's x is): every y block and block
+    sum, repeated until `min_seconds` of compute were timed (at least one pass).  The block
+    sums pin the GPU result at full size."""
     import oracle
 
     nb = n // b
-    rng = np.random.default_rng(7)
-    ids = rng.choice(nb * nb, size=min(pairs, nb * nb), replace=False)
-    a_blocks, bt_blocks, y_blocks = [], [], []
-    for g in ids:
-        i, j = divmod(int(g), nb)
-        a_blocks.append(oracle.gen_block_c(n, i * b, j * b, b))
-        bt_blocks.append(oracle.gen_block_c(n, j * b, i * b, b))
-        y_blocks.append(np.empty((b, b)))
-    oracle.transpose_sum_resident_c(a_blocks, bt_blocks, y_blocks, threads)  # first touch of y (untimed)
-    done = 0
-    t0 = time.perf_counter()
+    x = [oracle.gen_block_c(n, (g // nb) * b, (g % nb) * b, b) for g in range(nb * nb)]
+    a_blocks = x
+    bt_blocks = [x[(g % nb) * nb + g // nb] for g in range(nb * nb)]
+    y_blocks = [np_empty(b) for _ in range(nb * nb)]
+    passes, t0 = 0, time.perf_counter()
     while True:
-        oracle.transpose_sum_resident_c(a_blocks, bt_blocks, y_blocks, threads)
-        done += len(ids)
+        sums = oracle.transpose_sum_resident_c(a_blocks, bt_blocks, y_blocks, threads)
+        passes += 1
         dt = time.perf_counter() - t0
         if dt >= min_seconds:
             break
-    per_block = dt / done
-    return {"seconds": dt, "blocks": len(ids), "passes": done // len(ids), "per_block_s": per_block,
-            "full_ms": per_block * nb * nb * 1e3}
+    return {"seconds": dt, "passes": passes, "ms": dt / passes * 1e3, "sums": sums}
+
+
+def np_empty(b: int):
+    import numpy as np
+
+    return np.empty((b, b))
 
 
 def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
@@ -368,24 +367,37 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
         for h in hosts:
             h.free()
 
-    # -- parity (outside timing): sampled block sums vs the oracle --
+    # -- parity (outside timing) and the CPU baseline --
+    # With the CPU leg: the oracle computes the FULL array on the host (all y blocks and
+    # block sums, every host thread), which is both the baseline and full-size parity of
+    # every block sum and of the checksum.  Without it: 8 sampled blocks.
     parity = None
     cpu = None
     if dist.rank == 0:
+        import math as _m
+
         import oracle
 
-        sample = sorted(res.block_sums)[:: max(1, len(res.block_sums) // 8)][:8]
-        ref = oracle.transpose_sum_blocks_c(n, b, sample, threads=os.cpu_count() or 1)
-        worst = max(abs(res.block_sums[g] - r) / abs(r) for g, r in zip(sample, ref))
-        parity = {"sampled_blocks": len(sample), "max_rel_err": float(worst), "tolerance": 1e-12,
-                  "ok": bool(worst <= 1e-12)}
         if not args.skip_cpu:
             threads = len(os.sched_getaffinity(0))
-            cpu_s = ts_cpu_sample(n, b, args.cpu_pairs, threads, min_seconds=min(10.0, args.cpu_seconds))
-            cpu = {"value": cpu_s["full_ms"], "unit": "ms", "cores": threads, "kind": "port",
-                   "sample": f"oracle C restatement, {cpu_s['blocks']} of {ts.nb ** 2} output blocks x "
-                             f"{cpu_s['passes']} passes (x resident in host RAM), {cpu_s['seconds']:.1f} s, "
-                             f"extrapolated to the full {n}^2 array"}
+            full = ts_cpu_full(n, args.block, threads, min_seconds=min(10.0, args.cpu_seconds))
+            ref_sums = {g: float(v) for g, v in enumerate(full["sums"])}
+            worst = max(abs(res.block_sums[g] - ref_sums[g]) / max(abs(ref_sums[g]), 1e-300) for g in ref_sums)
+            want = _m.fsum(ref_sums[g] for g in sorted(ref_sums))
+            parity = {"blocks": len(ref_sums), "scope": "every block of the full array", "max_rel_err": float(worst),
+                      "checksum_oracle": want, "checksum_rel_err": abs(checksum - want) / abs(want),
+                      "tolerance": 1e-12, "ok": bool(worst <= 1e-12 and abs(checksum - want) <= 1e-12 * abs(want))}
+            cpu = {"value": full["ms"], "unit": "ms", "cores": threads, "kind": "port",
+                   "sample": f"oracle C restatement over the full {n}^2 array (all {ts.nb ** 2} blocks, x resident "
+                             f"in host RAM) x {full['passes']} passes in {full['seconds']:.1f} s"}
+        else:
+            sample = sorted(res.block_sums)[:: max(1, len(res.block_sums) // 8)][:8]
+            ref = oracle.transpose_sum_blocks_c(n, b, sample, threads=os.cpu_count() or 1)
+            worst = max(abs(res.block_sums[g] - r) / abs(r) for g, r in zip(sample, ref))
+            parity = {"blocks": len(sample), "scope": "sampled blocks", "max_rel_err": float(worst),
+                      "tolerance": 1e-12, "ok": bool(worst <= 1e-12)}
+        if not parity["ok"]:
+            raise RuntimeError(f"transpose_sum parity failed: {parity}")
     launches_per_step = native.lib().m4d_ts_launches_per_run(ts._plan)
     ts.close()
     ts.x.free()  # 25.6 GB of pools at N=1: give the HBM back before the next workload
@@ -829,16 +841,14 @@ def reference_p2p(args) -> dict:
 
 def reference_transpose_sum(args) -> dict:
     threads = len(os.sched_getaffinity(0))
-    per_step = []
     budget = max(2.0, args.cpu_seconds / max(1, args.steps))
-    for _ in range(min(args.warmup, 1)):
-        ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads, min_seconds=1.0)
-    for _ in range(args.steps):
-        per_step.append(ts_cpu_sample(args.n, args.block, args.cpu_pairs, threads, min_seconds=budget))
-    value = statistics.mean(s["full_ms"] for s in per_step)
+    full = ts_cpu_full(args.n, args.block, threads, min_seconds=budget * args.steps)
+    value = full["ms"]
     nb = args.n // args.block
-    sample = (f"oracle C restatement (the reference has no operator code), {per_step[0]['blocks']} of "
-              f"{nb * nb} output blocks per step with x resident in host RAM, extrapolated to the full array")
+    sample = (f"oracle C restatement (the reference has no operator code) over the full array (all {nb * nb} "
+              f"blocks, x resident in host RAM), {full['passes']} passes in {full['seconds']:.1f} s")
+    import math as _m
+
     return {
         "impl": "reference",
         "metric": f"x+x.T sum wall time ({args.n}^2 fp64, {args.block}^2 chunks)",
@@ -854,6 +864,7 @@ def reference_transpose_sum(args) -> dict:
         "dtype": "f64",
         "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
         "config": {"workload": "transpose_sum", "dims": args.n, "block": args.block},
+        "checksum": _m.fsum(float(v) for v in full["sums"]),
         "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -902,7 +913,6 @@ def main(argv=None) -> int:
     ap.add_argument("--max-size", type=int, default=64 << 20, help="p2p largest message")
     ap.add_argument("--n", type=int, default=40000)
     ap.add_argument("--block", type=int, default=2000)
-    ap.add_argument("--cpu-pairs", type=int, default=48, help="output blocks in the CPU baseline sample")
     ap.add_argument("--cpu-seconds", type=float, default=30.0, help="CPU-baseline time budget (whole run)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
