@@ -526,7 +526,8 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
     else:
         roof = {"bound": "hbm", "achieved": alg["hbm"] / t_meas / 1e9, "peak": hbm_peak, "unit": "GB/s",
                 "peak_source": peaks["_source"]}
-    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": args.traffic,
+    traffic = args.traffic if args.traffic is not None else recorded_traffic(f"key_merge/{args.rows}/{dist.world}")
+    roof.update({"frac": roof["achieved"] / roof["peak"], "traffic": traffic,
                  "kernel": "whole merge step (partition + shuffle + join kernels)",
                  "algorithmic_bytes_per_step": alg, "t_roof_ms": max(t_hbm, t_nvl) * 1e3, "phases": phase,
                  "trace_ms": trace})
