@@ -136,6 +136,7 @@ typedef struct m4d_transport_stats {
     uint64_t pull_kernel_launches; /* SM copy kernels issued for rendezvous pulls  */
     uint64_t eager_device_sends;   /* device payloads sent by the eager protocol    */
     uint64_t eager_device_loans;   /* eager device messages received by loan        */
+    uint64_t eager_proxy_copies;   /* eager device sends copied by the proxy kernel */
 } m4d_transport_stats;
 
 /* transport_init: publishes this rank and maps the peers that are already up

@@ -31,6 +31,28 @@ struct PullBatch {
 };
 int launch_pull_batch(const PullBatch& batch, cudaStream_t stream, int max_ctas);
 
+// Eager device copies through a resident proxy kernel (pull.cu): the host writes
+// a command into a host-mapped queue, the kernel (one CTA) polls it over PCIe,
+// copies the payload into the peer's device ring and then publishes the
+// command's sequence number in host memory -- no launch, no event per message.
+// A command slot holds three words, each tagged in its top 16 bits with the
+// command's sequence number (so a torn read is detected): src, dst, len.
+constexpr int kProxySlots = 256;
+struct alignas(64) ProxyCmd {
+    uint64_t w[3];
+    uint64_t pad[5];
+};
+struct ProxyQueue {
+    alignas(64) uint64_t head;   // commands consumed (the kernel writes)
+    alignas(64) uint32_t alive;  // a proxy kernel is running (kernel clears it when it idles out)
+    alignas(64) ProxyCmd cmd[kProxySlots];
+};
+constexpr uint64_t kProxyTagShift = 48;
+// Launches the proxy kernel on `stream`.  q: device view of the queue; state:
+// device word holding the commands done (kept across launches); done: device view
+// of the host word that receives each finished command's sequence number.
+int launch_eager_proxy(ProxyQueue* q, uint64_t* state, uint64_t* done, uint64_t idle_ns, cudaStream_t stream);
+
 // m4d_free hook: true when a transport took over the free of an allocation it exported
 // (deferred until every peer that mapped it closed the mapping; transport.cpp).
 bool release_exported(void* ptr);

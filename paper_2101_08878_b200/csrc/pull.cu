@@ -46,9 +46,111 @@ __global__ void __launch_bounds__(512) pull_kernel(m4d::PullBatch batch) {
     }
 }
 
+__device__ __forceinline__ uint64_t ld_relaxed_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_sys32(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr int kProxyThreads = 512;  // 64 KiB: 128 threads 13.4 us RTT, 512 9.6 (tools/probes/proxy_probe.cu)
+
+// Warp 0, lanes 0-2: read the three words of the slot of command `seq`; true (on
+// every lane) when all three carry its tag, the values (untagged) then in w[].
+__device__ __forceinline__ bool proxy_fetch(const m4d::ProxyQueue* q, uint64_t seq, uint64_t* w) {
+    const uint64_t* slot = q->cmd[seq % m4d::kProxySlots].w;
+    const int lane = threadIdx.x;
+    const uint64_t v = lane < 3 ? ld_relaxed_sys(slot + lane) : 0;
+    const bool ok = lane >= 3 || (v >> m4d::kProxyTagShift) == (seq & 0xffff);
+    if (!__all_sync(0xffffffffu, ok)) return false;
+    if (lane < 3) w[lane] = v & ((uint64_t(1) << m4d::kProxyTagShift) - 1);
+    return true;
+}
+
+// The resident eager-copy proxy: one CTA that polls the host-mapped queue,
+// copies each command's payload (into a peer's ring over NVLink) and publishes
+// its sequence number (system-scope release after a system fence), in order.
+// After `idle_ns` without a command it clears q->alive, looks once more
+// (Dekker with the host, which stores the command, fences, then reads alive)
+// and exits.
+__global__ void __launch_bounds__(kProxyThreads) eager_proxy_kernel(m4d::ProxyQueue* q, uint64_t* state,
+                                                                   uint64_t* done, uint64_t idle_ns) {
+    __shared__ uint64_t cmd[3];
+    __shared__ int verdict;  // 1: command in cmd[], 2: exit
+    uint64_t seq = *state;
+    uint64_t idle_since = globaltimer();
+    for (;;) {
+        if (threadIdx.x < 32) {
+            int v = 0;
+            while (!v) {
+                if (proxy_fetch(q, seq + 1, cmd)) {
+                    v = 1;
+                } else if (globaltimer() - idle_since > idle_ns) {
+                    if (threadIdx.x == 0) st_relaxed_sys32(&q->alive, 0);
+                    __syncwarp();
+                    asm volatile("fence.sc.sys;" ::: "memory");
+                    if (proxy_fetch(q, seq + 1, cmd)) {
+                        if (threadIdx.x == 0) st_relaxed_sys32(&q->alive, 1);
+                        v = 1;
+                    } else {
+                        v = 2;
+                    }
+                }
+            }
+            if (threadIdx.x == 0) verdict = v;
+        }
+        __syncthreads();
+        if (verdict == 2) break;
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(cmd[0]);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(cmd[1]);
+        const uint64_t len = cmd[2];
+        __syncthreads();  // cmd[] read by every thread before warp 0 polls again
+        if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
+            const uint64_t body = len / 16;
+            for (uint64_t i = threadIdx.x; i < body; i += kProxyThreads)
+                reinterpret_cast<int4*>(dst)[i] = reinterpret_cast<const int4*>(src)[i];
+            for (uint64_t i = body * 16 + threadIdx.x; i < len; i += kProxyThreads) dst[i] = src[i];
+        } else {
+            for (uint64_t i = threadIdx.x; i < len; i += kProxyThreads) dst[i] = src[i];
+        }
+        __threadfence_system();
+        __syncthreads();
+        ++seq;
+        if (threadIdx.x == 0) {
+            st_release_sys(done, seq);
+            st_relaxed_sys(&q->head, seq);
+        }
+        idle_since = globaltimer();
+    }
+    if (threadIdx.x == 0) *state = seq;
+}
+
 }  // namespace
 
 namespace m4d {
+
+int launch_eager_proxy(ProxyQueue* q, uint64_t* state, uint64_t* done, uint64_t idle_ns, cudaStream_t stream) {
+    eager_proxy_kernel<<<1, kProxyThreads, 0, stream>>>(q, state, done, idle_ns);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? M4D_OK : cuda_fail(e, "eager proxy launch");
+}
 
 int pull_batch() {
     static const int b = [] {

@@ -50,7 +50,7 @@ using m4d::fail;
 namespace {
 
 constexpr uint32_t kSegMagic = 0x4D344453;  // "M4DS"
-constexpr uint32_t kSegVersion = 2;
+constexpr uint32_t kSegVersion = 3;
 constexpr uint64_t kHeaderBytes = 4096;
 // Consumer heads of the eager device rings (one u64 per source rank) live in
 // the segment header from this offset.
@@ -91,6 +91,9 @@ struct SegHeader {
     uint64_t dev_ring_id;  // driver buffer id (the peers' mapping-cache key)
     uint64_t dev_ring_addr;  // its address in the owner process (peers in the same process use it)
     uint8_t dev_ring_handle[64];
+    // eager proxy: sequence number of the last eager device copy this rank's
+    // proxy kernel finished (written by the GPU through a host mapping)
+    alignas(64) std::atomic<uint64_t> proxy_done;
 };
 static_assert(sizeof(SegHeader) <= kDevHeadsOff, "segment header fields overlap the device-ring heads");
 
@@ -134,8 +137,10 @@ struct RtsRec {
     uint8_t handle[64];
 };
 
-// An eager device message: its bytes are already in the receiver's device ring
-// (region of this source) at absolute position pos (ring offset pos % size).
+// An eager device message: its bytes are in the receiver's device ring (region
+// of this source) at absolute position pos (ring offset pos % size) -- already
+// when the record is written, or (flags bit 1, proxy) once the sender's
+// proxy_done reaches seq.
 struct EagerDevRec {
     RecHdr h;
     uint32_t channel, tag;
@@ -143,7 +148,9 @@ struct EagerDevRec {
     uint64_t pos;
     uint32_t domain;
     uint32_t reserved;
+    uint64_t seq;
 };
+constexpr uint16_t kEagerFailed = 1, kEagerProxied = 2;
 
 struct FinRec {
     RecHdr h;
@@ -222,8 +229,10 @@ struct Req {
     RtsRec rts;
     // eager device send: the copy into the peer's ring, published when it is done
     bool eager_dev = false;
+    bool proxied = false;      // copied by the proxy kernel (no event)
     uint64_t dev_pos = 0;
     cudaEvent_t dev_ev = nullptr;
+    uint64_t proxy_seq = 0;
     // receive: an eager device message may complete it by loan (no copy)
     bool loan_ok = false;
     // queue membership
@@ -322,6 +331,25 @@ static uint64_t eager_device_max() {
     return v;
 }
 
+// The resident proxy kernel moves eager device payloads (M4D_EAGER_PROXY=0: copy
+// engine + event per message instead); it exits after M4D_EAGER_PROXY_IDLE_US
+// (default 500) without a command and is relaunched by the next one.
+static bool eager_proxy_enabled() {
+    static const bool v = [] {
+        const char* e = getenv("M4D_EAGER_PROXY");
+        return !e || strcmp(e, "0") != 0;
+    }();
+    return v;
+}
+
+static uint64_t eager_proxy_idle_ns() {
+    static const uint64_t v = [] {
+        const char* e = getenv("M4D_EAGER_PROXY_IDLE_US");
+        return (e && atoll(e) > 0 ? static_cast<uint64_t>(atoll(e)) : uint64_t(500)) * 1000;
+    }();
+    return v;
+}
+
 static uint64_t eager_ring_bytes() {
     static const uint64_t v = [] {
         const char* e = getenv("M4D_EAGER_DEVICE_RING");
@@ -396,6 +424,16 @@ struct m4d_transport {
     uint8_t* dev_ring = nullptr;                                // eager device ring (our inbound regions)
     uint64_t dev_ring_bytes = 0;                                // per source
     cudaStream_t eager_stream = nullptr;                        // eager copies (into peers' rings, out of ours)
+    // eager proxy (pull.cu): host-mapped command queue, its device view, the
+    // kernel's persistent state, the device view of me->proxy_done
+    m4d::ProxyQueue* pq = nullptr;
+    m4d::ProxyQueue* pq_dev = nullptr;
+    uint64_t* proxy_state = nullptr;
+    uint64_t* proxy_done_dev = nullptr;
+    cudaStream_t proxy_stream = nullptr;
+    bool me_registered = false;
+    uint64_t proxy_seq = 0;                                     // commands issued
+    std::deque<Req*> proxy_sends;                               // issued, copy not yet done (seq order)
     std::vector<EagerCopy> eager_copies;
     std::unordered_map<uint64_t, std::pair<uint64_t, uint64_t>> loans;  // recv id -> (device address, token)
     std::vector<cudaStream_t> pull_streams;                     // copies round-robin over these
@@ -407,6 +445,40 @@ struct m4d_transport {
 };
 
 namespace {
+
+// The eager proxy's queue (host, mapped), state word, stream, and the device view
+// of our header (proxy_done).  Failure leaves the copy-engine eager path.
+void setup_proxy(m4d_transport* t) {
+    void* q = nullptr;
+    void* q_dev = nullptr;
+    void* me_dev = nullptr;
+    void* state = nullptr;
+    cudaError_t e = cudaHostAlloc(&q, sizeof(m4d::ProxyQueue), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&q_dev, q, 0);
+    if (e == cudaSuccess) {
+        e = cudaHostRegister(t->me, kHeaderBytes, cudaHostRegisterMapped);
+        t->me_registered = e == cudaSuccess;
+    }
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(&me_dev, t->me, 0);
+    if (e == cudaSuccess) e = cudaMalloc(&state, sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaMemset(state, 0, sizeof(uint64_t));
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&t->proxy_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (q) cudaFreeHost(q);
+        if (state) cudaFree(state);
+        if (t->me_registered) cudaHostUnregister(t->me);
+        t->me_registered = false;
+        t->proxy_stream = nullptr;
+        return;
+    }
+    memset(q, 0, sizeof(m4d::ProxyQueue));
+    t->pq = static_cast<m4d::ProxyQueue*>(q);
+    t->pq_dev = static_cast<m4d::ProxyQueue*>(q_dev);
+    t->proxy_state = static_cast<uint64_t*>(state);
+    const uint64_t off = reinterpret_cast<uint8_t*>(&t->me->proxy_done) - reinterpret_cast<uint8_t*>(t->me);
+    t->proxy_done_dev = reinterpret_cast<uint64_t*>(static_cast<uint8_t*>(me_dev) + off);
+}
 
 std::string seg_name_for(const std::string& session, int rank) { return "/m4d_" + session + "_" + std::to_string(rank); }
 
@@ -538,6 +610,19 @@ int poll_eager_copies(m4d_transport* t) {
         t->spare_events.push_back(c.ev);
         t->eager_copies[i] = t->eager_copies.back();
         t->eager_copies.pop_back();
+        ++n;
+    }
+    return n;
+}
+
+// Sends whose proxy copy finished (me->proxy_done passed their sequence number).
+int poll_proxy_sends(m4d_transport* t) {
+    const uint64_t done = t->me->proxy_done.load(std::memory_order_acquire);
+    int n = 0;
+    while (!t->proxy_sends.empty() && t->proxy_sends.front()->proxy_seq <= done) {
+        Req* r = t->proxy_sends.front();
+        t->proxy_sends.pop_front();
+        complete(t, r, M4D_OK, r->len);
         ++n;
     }
     return n;
@@ -853,9 +938,58 @@ bool flush_fins(m4d_transport* t, Peer& p) {
     return true;
 }
 
+// The proxy kernel is running, or launched now.  Called after a command was
+// stored: store, fence, then read `alive` (the kernel clears alive, fences, then
+// looks for a command once more), so a command is never left without a kernel.
+int ensure_proxy(m4d_transport* t) {
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    volatile uint32_t* alive = &t->pq->alive;
+    if (*alive) return M4D_OK;
+    *alive = 1;
+    cudaSetDevice(t->device);
+    return m4d::launch_eager_proxy(t->pq_dev, t->proxy_state, t->proxy_done_dev, eager_proxy_idle_ns(),
+                                   t->proxy_stream);
+}
+
+// An eager device send through the proxy: the command goes into the queue and
+// the record into the ring at once (in post order with every other record); the
+// receiver takes the record once our proxy_done reaches its sequence number.
+bool push_proxied(m4d_transport* t, Peer& p, Req* r) {
+    const uint64_t seq = t->proxy_seq + 1;
+    if (seq - reinterpret_cast<volatile uint64_t*>(&t->pq->head)[0] > static_cast<uint64_t>(m4d::kProxySlots))
+        return false;  // queue full: the kernel is behind
+    uint8_t* w = p.out.reserve(sizeof(EagerDevRec));
+    if (!w) return false;
+    const uint64_t tag = (seq & 0xffff) << m4d::kProxyTagShift;
+    const uint64_t cap = p.dev_out_cap;
+    const uint64_t pos = r->dev_pos;
+    volatile uint64_t* slot = t->pq->cmd[seq % m4d::kProxySlots].w;
+    slot[0] = reinterpret_cast<uint64_t>(r->ptr) | tag;
+    slot[1] = reinterpret_cast<uint64_t>(p.dev_out + pos % cap) | tag;
+    slot[2] = r->len | tag;
+    t->proxy_seq = seq;
+    const int st = ensure_proxy(t);
+    EagerDevRec* rec = reinterpret_cast<EagerDevRec*>(w);
+    rec->h.bytes = sizeof(EagerDevRec);
+    rec->h.kind = kEagerDev;
+    rec->h.flags = st == M4D_OK ? kEagerProxied : kEagerFailed;
+    rec->channel = r->channel;
+    rec->tag = r->tag;
+    rec->len = r->len;
+    rec->pos = pos;
+    rec->domain = static_cast<uint32_t>(r->domain);
+    rec->reserved = 0;
+    rec->seq = seq;
+    p.out.commit(sizeof(EagerDevRec));
+    r->proxy_seq = seq;
+    r->sent = st == M4D_OK ? r->len : 0;
+    return true;
+}
+
 // Writes as much of the send at the head of the queue as fits; true when the
 // whole send is in the ring.
 bool push_send(m4d_transport* t, Peer& p, Req* r) {
+    if (r->proxied) return push_proxied(t, p, r);
     if (r->eager_dev) {  // publish once the copy into the peer's ring is done
         const cudaError_t e = cudaEventQuery(r->dev_ev);
         if (e == cudaErrorNotReady) return false;
@@ -932,6 +1066,8 @@ int flush_peer(m4d_transport* t, int peer) {
         ++progressed;
         if (r->device && !r->eager_dev) {
             t->awaiting_fin[r->id] = r;
+        } else if (r->proxied && r->sent == r->len) {
+            t->proxy_sends.push_back(r);  // completes once the proxy copied it
         } else if (r->eager_dev && r->sent != r->len) {
             complete(t, r, M4D_ERR_CUDA, 0);
         } else {
@@ -981,6 +1117,18 @@ bool try_eager(m4d_transport* t, int q, Req* r) {
     }
     const uint64_t head = dev_heads(p.seg)[t->rank].load(std::memory_order_acquire);
     if (pos + need - head > cap) return false;  // full: the receiver still holds those slots
+    const uint64_t top = uint64_t(1) << m4d::kProxyTagShift;
+    if (t->pq && reinterpret_cast<uint64_t>(r->ptr) < top && reinterpret_cast<uint64_t>(p.dev_out + off) < top &&
+        r->len < top) {
+        p.dev_prod = pos + need;
+        t->stats.eager_device_sends++;
+        t->stats.eager_proxy_copies++;
+        r->eager_dev = true;
+        r->proxied = true;
+        r->dev_pos = pos;
+        r->started = true;
+        return true;
+    }
     cudaEvent_t ev = grab_event(t);
     if (!ev) return false;
     cudaSetDevice(t->device);
@@ -1145,6 +1293,9 @@ int drain_peer(m4d_transport* t, int peer) {
     while (ring.cursor < tail) {
         const uint64_t pos = ring.cursor % ring.cap;
         const RecHdr* h = reinterpret_cast<const RecHdr*>(ring.data + pos);
+        if (h->kind == kEagerDev && (h->flags & kEagerProxied) &&
+            p.seg->proxy_done.load(std::memory_order_acquire) < reinterpret_cast<const EagerDevRec*>(h)->seq)
+            break;  // its bytes are still on the way: later records wait behind it (FIFO)
         switch (h->kind) {
             case kMsg: on_msg(t, peer, reinterpret_cast<const MsgRec*>(h)); break;
             case kCont: on_cont(t, peer, reinterpret_cast<const ContRec*>(h)); break;
@@ -1418,6 +1569,7 @@ m4d_status m4d_transport_open(const m4d_transport_config* cfg, m4d_transport** o
                 t->me->dev_ring_addr = reinterpret_cast<uint64_t>(ring);
                 memcpy(t->me->dev_ring_handle, handle.data(), 64);
                 t->me->dev_ring_ok.store(1, std::memory_order_release);
+                if (eager_proxy_enabled()) setup_proxy(t.get());
             } else {
                 if (ring) cudaFree(ring);
                 cudaGetLastError();  // no ring: every device send takes the rendezvous
@@ -1579,6 +1731,7 @@ int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
     // sender whose peer stops polling would wait forever.
     if (t->inflight_launches) poll_copies(t);
     if (!t->eager_copies.empty()) poll_eager_copies(t);
+    if (!t->proxy_sends.empty()) poll_proxy_sends(t);
     for (int q = 0; q < t->world; ++q)
         if (q != t->rank) {
             drain_peer(t, q);
@@ -1752,6 +1905,10 @@ m4d_status m4d_transport_close(m4d_transport* t) {
         for (cudaEvent_t e : t->spare_events) cudaEventDestroy(e);
         for (cudaStream_t st : t->pull_streams) cudaStreamDestroy(st);
     }
+    if (t->proxy_stream) {  // the kernel idles out (M4D_EAGER_PROXY_IDLE_US) before the rings go
+        cudaStreamSynchronize(t->proxy_stream);
+        cudaStreamDestroy(t->proxy_stream);
+    }
     for (auto& kv : t->ipc_maps) cudaIpcCloseMemHandle(kv.second.base);
     drop_holds(t, -1);
     if (t->eager_stream) {
@@ -1762,6 +1919,9 @@ m4d_status m4d_transport_close(m4d_transport* t) {
         cudaStreamDestroy(t->eager_stream);
     }
     if (t->dev_ring) cudaFree(t->dev_ring);
+    if (t->pq) cudaFreeHost(t->pq);
+    if (t->proxy_state) cudaFree(t->proxy_state);
+    if (t->me_registered) cudaHostUnregister(t->me);
     for (Peer& p : t->peers)
         if (p.seg) munmap(p.seg, p.seg_len);
     if (t->me) {

@@ -164,3 +164,85 @@ def test_comm_path_device_frames_use_eager_and_loans():
         assert stats(ts[1])["rendezvous_pulls"] == 2
     finally:
         close_all(ts)
+
+
+def test_sends_are_copied_by_the_proxy_kernel(pair):
+    """With the proxy (default) every eager device send is moved by the resident proxy
+    kernel: no copy-engine copy, no event per message."""
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    n = 1000
+    src, dst = dev(n, pattern(n, 2)), dev(n)
+    s = pair[0].post_send_eager(0, 1, 12, src.window())
+    r = pair[1].post_recv(0, 0, 12, dst.window(), MemoryDomain.DEVICE)
+    pump(pair, s, r)
+    assert dst.to_bytes() == pattern(n, 2).tobytes()
+    st = stats(pair[0])
+    assert st["eager_proxy_copies"] == st["eager_device_sends"] == 1
+
+
+def stream_mixed(ts, count=600):
+    """`count` messages 0 -> 1 on one tag, in post order: eager device frames of ragged
+    sizes and misaligned sources (more than the proxy queue's 256 slots in flight),
+    rendezvous frames and host frames interleaved.  Receives posted after all sends, so
+    every kind waits as an unexpected message; FIFO order and bytes must hold."""
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    big = 256 << 10
+    pool = dev(big + 64, pattern(big + 64, 7))
+    want, sends = [], []
+    for k in range(count):
+        kind = k % 10
+        if kind == 9:  # rendezvous (above the eager threshold)
+            n, off = big, 0
+            sends.append(ts[0].post_send(0, 1, 13, pool.window(off, n), MemoryDomain.DEVICE))
+            want.append(("dev", pattern(big + 64, 7)[off:off + n].tobytes()))
+        elif kind == 4:  # host frame
+            payload = bytes([k % 251]) * (1 + k % 300)
+            sends.append(ts[0].post_send(0, 1, 13, payload))
+            want.append(("host", payload))
+        else:
+            n = 1 + (k * 997) % (8 << 10)
+            off = k % 33  # misaligned sources too
+            sends.append(ts[0].post_send_eager(0, 1, 13, pool.window(off, n)))
+            want.append(("dev", pattern(big + 64, 7)[off:off + n].tobytes()))
+    rendezvous = sends[9::10]
+    pump(ts, *[s for k, s in enumerate(sends) if k % 10 != 9], timeout=60)  # complete without the receiver
+    got = []
+    for kind, data in want:
+        if kind == "host":
+            buf = bytearray(len(data))
+            r = ts[1].post_recv(0, 0, 13, buf)
+            pump(ts, r)
+            got.append(bytes(buf[:r.bytes_moved]))
+        else:
+            dst = dev(len(data))
+            r = ts[1].post_recv(0, 0, 13, dst.window(), MemoryDomain.DEVICE)
+            pump(ts, r)
+            got.append(dst.to_bytes()[:r.bytes_moved])
+    pump(ts, *rendezvous)
+    assert [g == w for g, (_, w) in zip(got, want)] == [True] * count
+    return stats(ts[0])
+
+
+def test_proxy_keeps_fifo_order_across_protocols(pair):
+    st = stream_mixed(pair)
+    assert st["eager_proxy_copies"] > 256 and st["eager_proxy_copies"] == st["eager_device_sends"]
+
+
+def test_copy_engine_eager_path_when_the_proxy_is_off():
+    """M4D_EAGER_PROXY=0: the same stream through copy-engine copies and events."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import sys; sys.path.insert(0, 'tests'); import test_eager_device as m, nvlink_fixtures as f\n"
+            "ts = f.nvlink_transports(2, 0)\n"
+            "st = m.stream_mixed(ts, 200)\n"
+            "f.close_all(ts)\n"
+            "assert st['eager_proxy_copies'] == 0 and st['eager_device_sends'] > 100, st\n"
+            "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
+                         env=dict(os.environ, M4D_EAGER_PROXY="0"))
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
