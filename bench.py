@@ -688,16 +688,32 @@ def bench_storm(args, dist: Dist, peaks: dict) -> dict | None:
 
     if dist.world < 2:
         raise SystemExit("--workload storm needs >= 2 ranks (torchrun --nproc-per-node N)")
+    # device frames: a round's received frames hold their device-ring slots until dropped
+    os.environ.setdefault("M4D_EAGER_DEVICE_RING", str(64 << 20))
     t = open_transport(dist, dist.device)
     sampler = ClockSampler(dist.device)
     sampler.start()
-    r = storm.run_worker(storm.namespace_of("paper_2101_08878_b200"), t, dist.allgather_bytes,
-                         conns=args.conns, total=args.frames, rounds=args.steps, warmup=args.warmup)
+    ns = storm.namespace_of("paper_2101_08878_b200")
+    r = storm.run_worker(ns, t, dist.allgather_bytes, conns=args.conns, total=args.frames, rounds=args.steps,
+                         warmup=args.warmup)
+    # the same storm with device frames (cuda:rank -> cuda:peer by the eager device protocol)
+    before = t.native_stats()
+    rd = storm.run_worker(ns, t, dist.allgather_bytes, conns=args.conns, total=args.frames, rounds=args.steps,
+                          warmup=args.warmup, device=dist.device)
+    after = t.native_stats()
     clocks = sampler.stop()
     if dist.rank != 0:
         return None
     line = storm_line(r, args, dist.world)
+    dev_line = storm_line(rd, args, dist.world)
     line.update({
+        "device_frames": {
+            "value": rd.frames_per_s, "unit": "frames/s", "ms_per_step": dev_line["ms_per_step"],
+            "latency_us": dev_line["latency_us"], "verified_frames": rd.verified,
+            "eager_device_sends_rank0": after["eager_device_sends"] - before["eager_device_sends"],
+            "proxy_copies_rank0": after["eager_proxy_copies"] - before["eager_proxy_copies"],
+            "note": "the same frames as device frames: sender proxy kernel copies each into the receiver's "
+                    "device ring over NVLink, the receiver reads it by loan (no host staging)"},
         "gpu_launches": 0,
         "note": "host frames through the nvlink transport's shared-memory rings (eager path); no kernels",
         "roofline": None,

@@ -52,7 +52,12 @@ using post_recv_fn = m4d_status (*)(m4d_transport*, uint32_t, int, uint32_t, voi
                                     m4d_completion*);
 using progress_fn = int (*)(m4d_transport*, m4d_completion*, int);
 
+using take_loan_fn = int (*)(m4d_transport*, uint64_t, uint64_t*, uint64_t*);
+using release_loan_fn = m4d_status (*)(m4d_transport*, uint64_t);
+
 post_send_fn g_send = nullptr;
+take_loan_fn g_take_loan = nullptr;
+release_loan_fn g_release_loan = nullptr;
 post_recv_fn g_recv = nullptr;
 progress_fn g_progress = nullptr;
 
@@ -215,12 +220,12 @@ void on_sub(const std::shared_ptr<Framed>& f, uint64_t sub, int status, uint64_t
 }
 
 PyObject* bind(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
-    if (nargs != 3) {
-        PyErr_SetString(PyExc_TypeError, "bind(post_send, post_recv, progress) takes 3 addresses");
+    if (nargs != 3 && nargs != 5) {
+        PyErr_SetString(PyExc_TypeError, "bind(post_send, post_recv, progress[, take_loan, release_loan])");
         return nullptr;
     }
-    void* p[3];
-    for (int i = 0; i < 3; ++i) {
+    void* p[5];
+    for (int i = 0; i < nargs; ++i) {
         p[i] = PyLong_AsVoidPtr(args[i]);
         if (!p[i]) {
             if (!PyErr_Occurred()) PyErr_SetString(PyExc_ValueError, "null function address");
@@ -230,6 +235,10 @@ PyObject* bind(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     g_send = reinterpret_cast<post_send_fn>(p[0]);
     g_recv = reinterpret_cast<post_recv_fn>(p[1]);
     g_progress = reinterpret_cast<progress_fn>(p[2]);
+    if (nargs == 5) {
+        g_take_loan = reinterpret_cast<take_loan_fn>(p[3]);
+        g_release_loan = reinterpret_cast<release_loan_fn>(p[4]);
+    }
     Py_RETURN_NONE;
 }
 
@@ -484,7 +493,38 @@ PyObject* forget(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     Py_RETURN_NONE;
 }
 
+// loan(handle, req_id) -> (device address, token) of a receive completed by loan, or None
+PyObject* loan(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+    if (nargs != 2 || !g_take_loan) {
+        PyErr_SetString(PyExc_TypeError, "loan(handle, req_id) (bound with take_loan)");
+        return nullptr;
+    }
+    auto* t = static_cast<m4d_transport*>(PyLong_AsVoidPtr(args[0]));
+    const uint64_t id = PyLong_AsUnsignedLongLong(args[1]);
+    if (PyErr_Occurred()) return nullptr;
+    uint64_t ptr = 0, token = 0;
+    if (!g_take_loan(t, id, &ptr, &token)) Py_RETURN_NONE;
+    return Py_BuildValue("(KK)", static_cast<unsigned long long>(ptr), static_cast<unsigned long long>(token));
+}
+
+// unloan(handle, token): hand a loaned ring slot back
+PyObject* unloan(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+    if (nargs != 2 || !g_release_loan) {
+        PyErr_SetString(PyExc_TypeError, "unloan(handle, token) (bound with release_loan)");
+        return nullptr;
+    }
+    auto* t = static_cast<m4d_transport*>(PyLong_AsVoidPtr(args[0]));
+    const uint64_t token = PyLong_AsUnsignedLongLong(args[1]);
+    if (PyErr_Occurred()) return nullptr;
+    g_release_loan(t, token);
+    Py_RETURN_NONE;
+}
+
 PyMethodDef methods[] = {
+    {"loan", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(loan)), METH_FASTCALL,
+     "loan(handle, req_id) -> (device address, token) | None"},
+    {"unloan", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(unloan)), METH_FASTCALL,
+     "unloan(handle, token)"},
     {"bind", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(bind)), METH_FASTCALL,
      "bind(post_send, post_recv, progress): C-ABI function addresses from the ctypes loader"},
     {"post", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(post)), METH_FASTCALL,

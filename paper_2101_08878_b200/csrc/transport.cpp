@@ -333,7 +333,7 @@ static uint64_t eager_device_max() {
 
 // The resident proxy kernel moves eager device payloads (M4D_EAGER_PROXY=0: copy
 // engine + event per message instead); it exits after M4D_EAGER_PROXY_IDLE_US
-// (default 500) without a command and is relaunched by the next one.
+// (default 100) without a command and is relaunched by the next one.
 static bool eager_proxy_enabled() {
     static const bool v = [] {
         const char* e = getenv("M4D_EAGER_PROXY");
@@ -345,7 +345,7 @@ static bool eager_proxy_enabled() {
 static uint64_t eager_proxy_idle_ns() {
     static const uint64_t v = [] {
         const char* e = getenv("M4D_EAGER_PROXY_IDLE_US");
-        return (e && atoll(e) > 0 ? static_cast<uint64_t>(atoll(e)) : uint64_t(500)) * 1000;
+        return (e && atoll(e) > 0 ? static_cast<uint64_t>(atoll(e)) : uint64_t(100)) * 1000;
     }();
     return v;
 }

@@ -20,6 +20,11 @@ pair uses generation ``2c+1``, the reverse direction ``2c+2``.
 
 Payload bytes are deterministic per frame id and checked bit-exactly after
 the timed region.
+
+``device=d`` (this package only): the frames are device frames on cuda:d --
+windows of one pool uploaded before the timed region -- so every frame moves
+GPU to GPU by the transport's eager device protocol (sender proxy-kernel copy
+into the receiver's device ring, received by loan).
 """
 
 from __future__ import annotations
@@ -74,10 +79,32 @@ def namespace_of(package) -> SimpleNamespace:
     msg = importlib.import_module(name + ".messaging")
     ch = importlib.import_module(name + ".channels")
     lp = importlib.import_module(name + ".loop")
-    return SimpleNamespace(Node=ep.Node, Endpoint=ep.Endpoint, build_comm_table=ch.build_comm_table,
-                           Message=msg.Message, Frame=msg.Frame, make_frame=msg.make_frame,
-                           send_payload=msg.send_payload, recv_payload=msg.recv_payload, TaskLoop=lp.TaskLoop,
-                           MonotonicClock=lp.MonotonicClock, gather=lp.gather)
+    ns = SimpleNamespace(Node=ep.Node, Endpoint=ep.Endpoint, build_comm_table=ch.build_comm_table,
+                         Message=msg.Message, Frame=msg.Frame, make_frame=msg.make_frame,
+                         send_payload=msg.send_payload, recv_payload=msg.recv_payload, TaskLoop=lp.TaskLoop,
+                         MonotonicClock=lp.MonotonicClock, gather=lp.gather, device_frames=None)
+    if name == __name__.rsplit(".", 2)[0]:
+        ns.device_frames = _device_frames
+    return ns
+
+
+def _device_frames(blobs: list[bytes], device: int) -> list:
+    """Device frames holding ``blobs``: 256-byte aligned windows of one cuda:device pool
+    (one allocation, one upload)."""
+    from ..messaging import Frame
+    from ..transport import MemoryDomain
+    from ..transport.nvlink import CudaRegion
+
+    offs, at = [], 0
+    for b in blobs:
+        offs.append(at)
+        at += (len(b) + 255) & ~255
+    host = bytearray(max(at, 1))
+    for o, b in zip(offs, blobs):
+        host[o:o + len(b)] = b
+    pool = CudaRegion(bytes(host), device)
+    return [Frame(CudaRegion(len(b), device, ptr=pool.ptr + o, owner=pool), len(b), MemoryDomain.DEVICE)
+            for o, b in zip(offs, blobs)]
 
 
 @dataclass
@@ -96,7 +123,7 @@ class StormWorker:
     """One worker's side of the storm: writers for its outgoing streams, readers for its incoming ones."""
 
     def __init__(self, ns: SimpleNamespace, transport, *, conns: int = 8, total: int = 100_000,
-                 seed: int = STORM_SEED):
+                 seed: int = STORM_SEED, device: int | None = None):
         self.ns, self.t = ns, transport
         self.rank, self.world = transport.rank, transport.world_size
         self.conns, self.total = conns, total
@@ -111,8 +138,14 @@ class StormWorker:
                 origin = "connector" if s == self.rank else "listener"
                 ep = ns.Endpoint(self.node, chan, peer, origin, (s << 20) | (d << 10) | c)
                 (self.out if s == self.rank else self.inc)[(s, d, c)] = (ep, ids)
-        self.frames_out = {k: ns.Frame(payload(k, self.sizes[k]), self.sizes[k])
-                           for _, ids in self.out.values() for k in ids}
+        ids_out = [k for _, ids in self.out.values() for k in ids]
+        if device is None:
+            self.frames_out = {k: ns.Frame(payload(k, self.sizes[k]), self.sizes[k]) for k in ids_out}
+        else:
+            if ns.device_frames is None:
+                raise ValueError("device frames need this package's namespace")
+            frames = ns.device_frames([payload(k, self.sizes[k]) for k in ids_out], device)
+            self.frames_out = dict(zip(ids_out, frames))
         self.sent_ns: dict[int, int] = {}
         self.recv_ns: dict[int, int] = {}
         self.received: dict[int, object] = {}
@@ -194,14 +227,16 @@ def summarise(reports: list[bytes], sizes: list[int], verified: int) -> StormRes
 
 
 def run_worker(ns: SimpleNamespace, transport, sync, *, conns: int = 8, total: int = 100_000,
-               seed: int = STORM_SEED, rounds: int = 1, warmup: int = 0, verify: bool = True) -> StormResult:
+               seed: int = STORM_SEED, rounds: int = 1, warmup: int = 0, verify: bool = True,
+               device: int | None = None) -> StormResult:
     """One worker process: set up, then per round a barrier and the timed storm;
     close, verify, gather.  ``sync(bytes) -> list[bytes]`` is an all-gather over
     the workers (any control plane: torch.distributed gloo, or the transport
     itself).  Returns the :class:`StormResult` on every worker."""
-    w = StormWorker(ns, transport, conns=conns, total=total, seed=seed)
+    w = StormWorker(ns, transport, conns=conns, total=total, seed=seed, device=device)
     loop = ns.TaskLoop(ns.MonotonicClock())
     for r in range(warmup + rounds):
+        w.received = {}  # (device frames: received frames hold ring slots until dropped)
         sync(b"go")
         loop.run_until_complete(w.run(timed=r >= warmup))
     loop.run_until_complete(w.close())
@@ -212,9 +247,9 @@ def run_worker(ns: SimpleNamespace, transport, sync, *, conns: int = 8, total: i
 
 
 def run_local(ns: SimpleNamespace, transports, *, conns: int = 8, total: int = 100_000,
-              seed: int = STORM_SEED, rounds: int = 1) -> StormResult:
+              seed: int = STORM_SEED, rounds: int = 1, device: int | None = None) -> StormResult:
     """Every worker in this process on one executor (tests; in-process worlds)."""
-    workers = [StormWorker(ns, t, conns=conns, total=total, seed=seed) for t in transports]
+    workers = [StormWorker(ns, t, conns=conns, total=total, seed=seed, device=device) for t in transports]
     loop = ns.TaskLoop(ns.MonotonicClock())
 
     async def all_runs():

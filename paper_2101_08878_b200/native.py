@@ -222,7 +222,8 @@ def fast():
     except ImportError as exc:
         raise NativeLibraryMissing(f"_m4dfast extension not built ({exc}): run __graft_entry__.build()") from exc
     addr = [ctypes.cast(getattr(handle, n), ctypes.c_void_p).value
-            for n in ("m4d_transport_post_send", "m4d_transport_post_recv", "m4d_transport_progress")]
+            for n in ("m4d_transport_post_send", "m4d_transport_post_recv", "m4d_transport_progress",
+                      "m4d_transport_take_loan", "m4d_transport_release_loan")]
     _m4dfast.bind(*addr)
     _fast = _m4dfast
     return _fast

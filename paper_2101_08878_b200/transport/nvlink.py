@@ -124,40 +124,60 @@ class _Loan:
         t = self.transport
         try:
             if getattr(t, "_h", None):
-                t._lib.m4d_transport_release_loan(t._h, self.token)
+                t._fast.unloan(t._h, self.token)
         except Exception:
             pass
 
 
 class _RegionPool:
-    """Size-class cache of receive regions so recv_payload does not cudaMalloc per frame."""
+    """Size-class cache of receive regions so recv_payload does not cudaMalloc per frame.
+
+    Classes below SLAB bytes are carved out of 2 MiB slabs (one cudaMalloc per slab,
+    kept until the pool dies), so a storm of small frames whose regions are held by
+    the application costs no allocation per frame -- cudaMalloc / cudaFree also
+    synchronise the device, and with it wait for a running eager proxy kernel to
+    idle out.  Larger classes get their own allocation, cached up to CACHE_BYTES per
+    class."""
+
+    SLAB = 2 << 20
+    CACHE_BYTES = 64 << 20
 
     def __init__(self, device: int):
         self.device = device
         self.free: dict[int, list] = {}
+        self.slabs: list = []
 
     def get(self, n: int) -> CudaRegion:
         size = 1 << max(12, (max(n, 1) - 1).bit_length())
-        bucket = self.free.get(size)
-        buf = bucket.pop() if bucket else native.DeviceBuffer(self.device, size)
-        region = CudaRegion(n, self.device, ptr=buf.ptr, owner=_Lease(self, size, buf))
-        return region
-
-    def put(self, size: int, buf) -> None:
         bucket = self.free.setdefault(size, [])
-        if len(bucket) < 8:
-            bucket.append(buf)
+        if not bucket:
+            if size >= self.SLAB:
+                buf = native.DeviceBuffer(self.device, size)
+                return CudaRegion(n, self.device, ptr=buf.ptr, owner=_Lease(self, size, buf))
+            slab = native.DeviceBuffer(self.device, self.SLAB)
+            self.slabs.append(slab)
+            bucket.extend(slab.ptr + k * size for k in range(self.SLAB // size))
+        item = bucket.pop()
+        ptr = item if isinstance(item, int) else item.ptr
+        return CudaRegion(n, self.device, ptr=ptr, owner=_Lease(self, size, item))
+
+    def put(self, size: int, item) -> None:
+        bucket = self.free.setdefault(size, [])
+        if isinstance(item, int) or len(bucket) < max(2, self.CACHE_BYTES // size):
+            bucket.append(item)
 
 
 class _Lease:
-    __slots__ = ("pool", "size", "buf")
+    """A pooled region's slot (slab address or own DeviceBuffer), back to the pool on death."""
 
-    def __init__(self, pool, size, buf):
-        self.pool, self.size, self.buf = pool, size, buf
+    __slots__ = ("pool", "size", "item")
+
+    def __init__(self, pool, size, item):
+        self.pool, self.size, self.item = pool, size, item
 
     def __del__(self):
         try:
-            self.pool.put(self.size, self.buf)
+            self.pool.put(self.size, self.item)
         except Exception:
             pass
 
@@ -314,10 +334,10 @@ class NvlinkTransport(Transport):
         """The :class:`CudaRegion` lent to a finished loanable receive (the ring bytes, valid
         while the region is alive and the transport open), or None if the bytes are in the
         posted buffer."""
-        ptr, token = ctypes.c_uint64(), ctypes.c_uint64()
-        if not self._lib.m4d_transport_take_loan(self._h, req.id, ctypes.byref(ptr), ctypes.byref(token)):
+        got = self._fast.loan(self._h, req.id)
+        if got is None:
             return None
-        region = CudaRegion(req.bytes_moved, self.device, ptr=ptr.value, owner=_Loan(self, token.value))
+        region = CudaRegion(req.bytes_moved, self.device, ptr=got[0], owner=_Loan(self, got[1]))
         self._loans.add(region)
         return region
 

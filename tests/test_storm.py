@@ -10,6 +10,8 @@ import subprocess
 import sys
 import textwrap
 
+import pytest
+
 from nvlink_fixtures import close_all, new_session, nvlink_transports
 from paper_2101_08878_b200.harness import storm
 
@@ -44,6 +46,64 @@ def test_storm_in_process_nvlink_host_frames():
         close_all(ts)
     assert r.frames == 6000 and r.verified == 3000
     assert r.frames_per_s > 0 and r.p50_us <= r.p99_us <= r.max_us
+
+
+@pytest.mark.gpu
+def test_storm_in_process_device_frames():
+    """Device frames on cuda:0 (eager device protocol: proxy copies, loaned receives)."""
+    ts = nvlink_transports(3, 0)
+    try:
+        r = storm.run_local(storm.namespace_of("paper_2101_08878_b200"), ts, conns=4, total=3000, rounds=2,
+                            device=0)
+        st = [t.native_stats() for t in ts]
+    finally:
+        close_all(ts)
+    assert r.frames == 6000 and r.verified == 3000
+    assert sum(x["eager_device_sends"] for x in st) == 6000
+    assert sum(x["eager_device_loans"] for x in st) == 6000
+
+
+DEVICE_WORKER = textwrap.dedent('''
+    import os, sys
+    sys.path.insert(0, sys.argv[1])
+    from paper_2101_08878_b200 import native
+    from paper_2101_08878_b200.harness import storm
+    from paper_2101_08878_b200.transport import TransportConfig, transport_init
+    rank, world, session = int(sys.argv[2]), int(sys.argv[3]), sys.argv[4]
+    dev = rank % native.device_count()
+    t = transport_init(world, rank, TransportConfig(kind="nvlink", session=session, device=dev, connect_timeout=60))
+    t.wait_ready(60)
+    r = storm.run_worker(storm.namespace_of("paper_2101_08878_b200"), t, storm.transport_sync(t),
+                         conns=4, total=4000, rounds=2, warmup=1, device=dev)
+    st = t.native_stats()
+    print("RESULT", r.frames, r.verified, st["eager_device_sends"], st["eager_proxy_copies"])
+    t.close()
+''')
+
+
+@pytest.mark.gpu
+def test_storm_processes_device_frames():
+    """Three processes (one per GPU when there are enough, else sharing cuda:0): device
+    frames cross processes through CUDA-IPC mapped device rings."""
+    session = new_session()
+    procs = [subprocess.Popen([sys.executable, "-c", DEVICE_WORKER, ROOT, str(r), "3", session],
+                              stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True) for r in range(3)]
+    outs = []
+    for p in procs:
+        try:
+            out, _ = p.communicate(timeout=300)
+        except subprocess.TimeoutExpired:
+            p.kill()
+            out, _ = p.communicate()
+        outs.append((p.returncode, out))
+    sent = 0
+    for rc, out in outs:
+        assert rc == 0, out[-3000:]
+        line = [l for l in out.splitlines() if l.startswith("RESULT")][0].split()
+        assert int(line[1]) == 8000 and int(line[2]) == 4000
+        assert int(line[3]) == int(line[4])  # every eager device send went through the proxy
+        sent += int(line[3])
+    assert sent == 3 * 4000  # three rounds (one warm-up) of 4000 frames, all eager
 
 
 WORKER = textwrap.dedent('''
