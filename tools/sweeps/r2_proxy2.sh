@@ -1,6 +1,6 @@
 #!/bin/bash
 exec > gpurun_out/r2_proxy2.log 2>&1
-bash tools/r2_storm_prof.sh; cat gpurun_out/r2_storm_prof.txt
+bash tools/sweeps/r2_storm_prof.sh; cat gpurun_out/r2_storm_prof.txt
 timeout 900 python -m pytest tests/test_eager_device.py tests/test_storm.py tests/test_multiprocess_gpu.py tests/test_serializers.py tests/test_comm_stack_nvlink.py -x -q 2>&1 | tail -3
 run() { timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port $1 bench.py --gpus 2 --workload p2p --skip-cpu --max-size 4194304; }
 run 29751 > gpurun_out/r2_proxy2_p2p.json 2> gpurun_out/r2_proxy2_p2p.err
