@@ -156,7 +156,10 @@ int m4d_transport_mesh_ready(const m4d_transport* t);
  * without waiting for the receiver; larger ones, or any that find the ring
  * full, take the rendezvous.  For post_recv, bit 1 lets an eager device message
  * complete the receive by LOAN: no copy, the bytes stay in the ring
- * (m4d_transport_take_loan) until m4d_transport_release_loan.  When the
+ * (m4d_transport_take_loan) until m4d_transport_release_loan.  Bit 2 (device
+ * receives): loan only -- ptr may be NULL, `len` is the largest message
+ * accepted; a message that arrives by rendezvous is pulled into a transport
+ * receive slot that is lent the same way.  When the
  * request finishes inside the call, *now receives its completion (status
  * != -1) and it is not reported again by m4d_transport_progress. */
 m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer, uint32_t tag,

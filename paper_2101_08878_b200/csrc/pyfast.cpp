@@ -21,7 +21,15 @@
 //
 //   send_framed(handle, kind, channel, peer, tag, header, frames, max_chunk, req_id)
 //   recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id)
-//   take_framed(req_id) -> (outcome, header bytes, payload bytearray | None, detail)
+//   take_framed(req_id) -> (outcome, header bytes, payload, detail)
+//
+// Device frames: a message whose only frame is a device frame of at most
+// dev_max bytes (the transport's eager device threshold, one chunk) is also
+// done natively.  The sender passes that frame as (address, length) and it
+// goes out as an eager device send; the receiver (recv_framed's dev_max
+// argument) posts a loan-only device receive, and the payload it returns is
+// the loan, (device address, token), of the ring bytes (or of a transport
+// receive slot when the message came by rendezvous).
 //
 // kind 0 is send_payload/recv_payload (messaging.py:295-320 of the reference:
 // a <QBB transfer header, then the payload in max_chunk slices, one tag);
@@ -84,6 +92,10 @@ struct Framed {
     uint64_t header_got = 0;
     std::vector<uint8_t> payload;
     std::vector<Py_buffer> views;  // send: exporters held until the sends complete
+    uint64_t dev_max = 0;          // recv: single device frames up to this size are received by loan
+    bool dev = false;              // recv: the payload is a device frame, lent (loan_ptr, loan_token)
+    bool has_loan = false;
+    uint64_t loan_ptr = 0, loan_token = 0;
     int pending = 0;
     int status = M4D_OK;
     int outcome = kComplete;
@@ -130,15 +142,17 @@ void unqueue(const std::shared_ptr<Framed>& f) {
 void on_sub(const std::shared_ptr<Framed>& f, uint64_t sub, int status, uint64_t bytes);
 
 // Posts one sub-request; an inline completion is handled at once.
-int post_sub(const std::shared_ptr<Framed>& f, bool send, uint32_t tag, void* ptr, uint64_t len, uint64_t offset) {
+int post_sub(const std::shared_ptr<Framed>& f, bool send, uint32_t tag, void* ptr, uint64_t len, uint64_t offset,
+             int on_device = 0) {
     const uint64_t sub = kSubBit | g_next_sub++;
     m4d_completion now;
     g_by_sub[sub] = f;
     f->sub_slot[sub] = f->expect.size();
     f->expect.emplace_back(offset, len);
     ++f->pending;
-    const m4d_status st = send ? g_send(f->t, f->channel, f->peer, tag, ptr, len, 0, 0, sub, &now)
-                               : g_recv(f->t, f->channel, f->peer, tag, ptr, len, 0, 0, sub, &now);
+    const int domain = on_device ? 1 : 0;
+    const m4d_status st = send ? g_send(f->t, f->channel, f->peer, tag, ptr, len, domain, on_device, sub, &now)
+                               : g_recv(f->t, f->channel, f->peer, tag, ptr, len, domain, on_device, sub, &now);
     if (st != M4D_OK) {
         g_by_sub.erase(sub);
         --f->pending;
@@ -158,10 +172,23 @@ void on_header(const std::shared_ptr<Framed>& f, uint64_t got) {
     f->header_got = got;
     f->header.resize(got);
     std::vector<std::pair<uint64_t, int>> frames;  // (length, tag)
+    // A lone device frame small enough for the eager device protocol: one loan-only
+    // device receive (the bytes stay where they land on this GPU).
+    auto device_frame = [&](uint64_t len, int tag) {
+        if (!f->dev_max || !g_take_loan || len == 0 || len > f->dev_max || len > f->max_chunk) {
+            f->outcome = kHeaderOnly;
+            return;
+        }
+        f->dev = true;
+        f->outcome = kComplete;
+        const int st = post_sub(f, false, static_cast<uint32_t>(tag), nullptr, len, 0, 1 | 4);
+        if (st != M4D_OK) f->status = st;
+    };
     if (f->kind == 0) {
-        if (got != 10 || f->header[9] != 0) { f->outcome = kHeaderOnly; return; }
+        if (got != 10) { f->outcome = kHeaderOnly; return; }
         uint64_t len;
         std::memcpy(&len, f->header.data(), 8);
+        if (f->header[9] != 0) { device_frame(len, static_cast<int>(f->tag)); return; }
         frames.emplace_back(len, static_cast<int>(f->tag));
     } else {
         if (got < 4) { f->outcome = kHeaderOnly; return; }
@@ -169,6 +196,12 @@ void on_header(const std::shared_ptr<Framed>& f, uint64_t got) {
         std::memcpy(&count, f->header.data(), 4);
         if (count == kEos) { f->outcome = kEndOfStream; return; }
         if (count > kMaxFrames || got != 4 + 10ull * count) { f->outcome = kHeaderOnly; return; }
+        if (count == 1 && f->header[4 + 9] != 0) {
+            uint64_t len;
+            std::memcpy(&len, f->header.data() + 4, 8);
+            device_frame(len, data_tag(0));
+            return;
+        }
         for (uint32_t i = 0; i < count; ++i) {
             const uint8_t* m = f->header.data() + 4 + 10 * i;
             uint64_t len;
@@ -210,6 +243,19 @@ void on_sub(const std::shared_ptr<Framed>& f, uint64_t sub, int status, uint64_t
         on_header(f, bytes);
         --f->pending;
         if (f->status != M4D_OK) { finish(f, f->status, false, nullptr); return; }
+    } else if (f->recv && f->dev) {
+        uint64_t ptr = 0, token = 0;
+        if (g_take_loan(f->t, sub, &ptr, &token)) {
+            f->has_loan = true;
+            f->loan_ptr = ptr;
+            f->loan_token = token;
+        }
+        if (bytes != f->expect[slot].second && f->outcome == kComplete) {
+            f->outcome = kShortChunk;
+            f->detail[0] = 0;
+            f->detail[1] = static_cast<long long>(f->expect[slot].second);
+            f->detail[2] = static_cast<long long>(bytes);
+        }
     } else if (f->recv && bytes != f->expect[slot].second && f->outcome == kComplete) {
         f->outcome = kShortChunk;
         f->detail[0] = static_cast<long long>(f->expect[slot].first);
@@ -352,8 +398,8 @@ PyObject* inline_result(const std::shared_ptr<Framed>& f) {
 
 // recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id)
 PyObject* recv_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
-    if (nargs != 7 || !g_recv) {
-        PyErr_SetString(PyExc_TypeError, "recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id)");
+    if ((nargs != 7 && nargs != 8) || !g_recv) {
+        PyErr_SetString(PyExc_TypeError, "recv_framed(handle, kind, channel, peer, tag, max_chunk, req_id[, dev_max])");
         return nullptr;
     }
     auto f = std::make_shared<Framed>();
@@ -364,6 +410,7 @@ PyObject* recv_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     f->tag = static_cast<uint32_t>(PyLong_AsUnsignedLong(args[4]));
     f->max_chunk = PyLong_AsUnsignedLongLong(args[5]);
     f->id = PyLong_AsUnsignedLongLong(args[6]);
+    if (nargs == 8) f->dev_max = PyLong_AsUnsignedLongLong(args[7]);
     if (PyErr_Occurred()) return nullptr;
     if (f->max_chunk < 1) f->max_chunk = 1;
     f->recv = true;
@@ -402,29 +449,57 @@ PyObject* send_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
         return nullptr;
     }
     const Py_ssize_t nf = PyTuple_GET_SIZE(frames);
-    f->views.resize(static_cast<size_t>(nf) + 1);
-    Py_ssize_t got = 0;
+    // a frame is a host buffer, or (device address, length): a device frame sent eagerly
+    struct Body {
+        uint8_t* ptr;
+        uint64_t len;
+        bool device;
+    };
+    std::vector<Body> bodies(static_cast<size_t>(nf));
+    for (Py_ssize_t i = 0; i < nf; ++i) {
+        PyObject* item = PyTuple_GET_ITEM(frames, i);
+        if (PyTuple_Check(item)) {
+            if (PyTuple_GET_SIZE(item) != 2) {
+                PyErr_SetString(PyExc_TypeError, "a device frame is (address, length)");
+                return nullptr;
+            }
+            bodies[static_cast<size_t>(i)] = Body{static_cast<uint8_t*>(PyLong_AsVoidPtr(PyTuple_GET_ITEM(item, 0))),
+                                                  PyLong_AsUnsignedLongLong(PyTuple_GET_ITEM(item, 1)), true};
+            if (PyErr_Occurred()) return nullptr;
+        }
+    }
+    f->views.reserve(static_cast<size_t>(nf) + 1);
     auto fail_views = [&]() {
-        for (Py_ssize_t i = 0; i < got; ++i) PyBuffer_Release(&f->views[static_cast<size_t>(i)]);
-        f->views.clear();
+        release_views(*f);
         return nullptr;
     };
-    if (PyObject_GetBuffer(args[5], &f->views[0], PyBUF_SIMPLE) != 0) { f->views.clear(); return nullptr; }
-    got = 1;
-    for (Py_ssize_t i = 0; i < nf; ++i, ++got)
-        if (PyObject_GetBuffer(PyTuple_GET_ITEM(frames, i), &f->views[static_cast<size_t>(i) + 1], PyBUF_SIMPLE) != 0)
+    f->views.emplace_back();
+    if (PyObject_GetBuffer(args[5], &f->views.back(), PyBUF_SIMPLE) != 0) { f->views.clear(); return nullptr; }
+    for (Py_ssize_t i = 0; i < nf; ++i) {
+        Body& b = bodies[static_cast<size_t>(i)];
+        if (b.device) continue;
+        f->views.emplace_back();
+        if (PyObject_GetBuffer(PyTuple_GET_ITEM(frames, i), &f->views.back(), PyBUF_SIMPLE) != 0) {
+            f->views.pop_back();
             return fail_views();
+        }
+        b.ptr = static_cast<uint8_t*>(f->views.back().buf);
+        b.len = static_cast<uint64_t>(f->views.back().len);
+    }
     g_framed[f->id] = f;
     f->pending = 1;  // guard: the composite cannot finish while its sends are still being posted
     const uint32_t header_tag = f->kind == 0 ? f->tag : static_cast<uint32_t>(kTagMessage);
     int st = post_sub(f, true, header_tag, f->views[0].buf, static_cast<uint64_t>(f->views[0].len), 0);
     for (Py_ssize_t i = 0; i < nf && st == M4D_OK && !f->done; ++i) {
-        const Py_buffer& v = f->views[static_cast<size_t>(i) + 1];
+        const Body& b = bodies[static_cast<size_t>(i)];
         const uint32_t tag = f->kind == 0 ? f->tag : static_cast<uint32_t>(data_tag(static_cast<size_t>(i)));
-        const uint64_t len = static_cast<uint64_t>(v.len);
-        for (uint64_t off = 0; off < len && st == M4D_OK && !f->done; off += f->max_chunk) {
-            const uint64_t piece = len - off < f->max_chunk ? len - off : f->max_chunk;
-            st = post_sub(f, true, tag, static_cast<uint8_t*>(v.buf) + off, piece, off);
+        if (b.device) {  // one eager-capable device send (the caller checked it fits one chunk)
+            st = post_sub(f, true, tag, b.ptr, b.len, 0, 1 | 2);
+            continue;
+        }
+        for (uint64_t off = 0; off < b.len && st == M4D_OK && !f->done; off += f->max_chunk) {
+            const uint64_t piece = b.len - off < f->max_chunk ? b.len - off : f->max_chunk;
+            st = post_sub(f, true, tag, b.ptr + off, piece, off);
         }
     }
     --f->pending;
@@ -459,7 +534,17 @@ PyObject* take_framed(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     std::shared_ptr<Framed> f = it->second;
     g_framed.erase(it);
     PyObject* payload = nullptr;
-    if (f->outcome == kComplete) {
+    if (f->dev) {
+        if (f->has_loan && f->outcome == kComplete) {
+            payload = Py_BuildValue("(KK)", static_cast<unsigned long long>(f->loan_ptr),
+                                    static_cast<unsigned long long>(f->loan_token));
+            if (!payload) return nullptr;
+        } else {
+            if (f->has_loan && g_release_loan) g_release_loan(f->t, f->loan_token);
+            Py_INCREF(Py_None);
+            payload = Py_None;
+        }
+    } else if (f->outcome == kComplete) {
         payload = PyByteArray_FromStringAndSize(reinterpret_cast<const char*>(f->payload.data()),
                                                 static_cast<Py_ssize_t>(f->payload.size()));
         if (!payload) return nullptr;

@@ -235,6 +235,9 @@ struct Req {
     uint64_t proxy_seq = 0;
     // receive: an eager device message may complete it by loan (no copy)
     bool loan_ok = false;
+    // loan-only receive (no buffer of its own): a rendezvous message is pulled into a
+    // transport-owned receive slot, which is then lent like an eager message
+    bool loan_only = false;
     // queue membership
     bool in_posted = false;
     bool in_outq = false;
@@ -436,6 +439,11 @@ struct m4d_transport {
     std::deque<Req*> proxy_sends;                               // issued, copy not yet done (seq order)
     std::vector<EagerCopy> eager_copies;
     std::unordered_map<uint64_t, std::pair<uint64_t, uint64_t>> loans;  // recv id -> (device address, token)
+    // receive slots of loan-only receives that arrive by rendezvous: kRecvSlot-byte
+    // slots carved from kRecvSlab allocations; larger messages get their own
+    std::vector<void*> recv_slabs;
+    std::vector<uint8_t*> recv_free;
+    std::unordered_map<uint64_t, void*> recv_big;
     std::vector<cudaStream_t> pull_streams;                     // copies round-robin over these
     size_t next_stream = 0;
     double last_liveness = 0.0;
@@ -526,6 +534,56 @@ cudaEvent_t grab_event(m4d_transport* t) {
         return nullptr;
     }
     return ev;
+}
+
+constexpr uint64_t kRecvSlot = 64 << 10, kRecvSlab = 2 << 20;
+constexpr uint64_t kPoolToken = uint64_t(1) << 63;  // loan token of a receive slot: bit 63 | address
+
+uint8_t* recv_slot_get(m4d_transport* t, uint64_t len) {
+    cudaSetDevice(t->device);
+    if (len > kRecvSlot) {
+        void* p = nullptr;
+        if (cudaMalloc(&p, len) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        t->recv_big[reinterpret_cast<uint64_t>(p)] = p;
+        return static_cast<uint8_t*>(p);
+    }
+    if (t->recv_free.empty()) {
+        void* slab = nullptr;
+        if (cudaMalloc(&slab, kRecvSlab) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        t->recv_slabs.push_back(slab);
+        for (uint64_t off = 0; off < kRecvSlab; off += kRecvSlot) t->recv_free.push_back(static_cast<uint8_t*>(slab) + off);
+    }
+    uint8_t* p = t->recv_free.back();
+    t->recv_free.pop_back();
+    return p;
+}
+
+void recv_slot_put(m4d_transport* t, uint8_t* p) {
+    auto it = t->recv_big.find(reinterpret_cast<uint64_t>(p));
+    if (it != t->recv_big.end()) {
+        cudaFree(it->second);
+        t->recv_big.erase(it);
+        return;
+    }
+    t->recv_free.push_back(p);
+}
+
+// A receive whose rendezvous pull finished (or failed): a loan-only receive lends
+// its slot (or gives it back on failure), then the receive completes.
+void finish_pulled(m4d_transport* t, Req* r, int status, uint64_t bytes) {
+    if (r->loan_only) {
+        if (status == M4D_OK)
+            t->loans[r->id] = std::make_pair(reinterpret_cast<uint64_t>(r->ptr), kPoolToken | reinterpret_cast<uint64_t>(r->ptr));
+        else
+            recv_slot_put(t, r->ptr);
+    }
+    complete(t, r, status, bytes);
 }
 
 // Receiver: the slot at `pos` of `peer`'s region of our ring is free; the head
@@ -789,6 +847,16 @@ void start_pull(m4d_transport* t, int peer, Req* r, const RtsRec& rts) {
         complete(t, r, M4D_ERR_CUDA, 0);
         return;
     }
+    if (r->loan_only) {
+        r->ptr = recv_slot_get(t, rts.len);
+        if (!r->ptr) {
+            pull_done(t, key);
+            m4d::fail(M4D_ERR_CUDA, "no device memory for a %llu-byte receive slot", (unsigned long long)rts.len);
+            queue_fin(t, peer, rts.send_id, M4D_ERR_TRANSFER, 0);
+            complete(t, r, M4D_ERR_CUDA, 0);
+            return;
+        }
+    }
     t->pending_pulls.push_back(PendingPull{r, peer, rts.send_id, static_cast<const uint8_t*>(src), rts.len, key});
     t->stats.rendezvous_pulls++;
     t->stats.nvlink_bytes += rts.len;
@@ -815,7 +883,7 @@ void flush_pulls(m4d_transport* t) {
             PendingPull& pp = t->pending_pulls[i];
             pull_done(t, pp.key);
             queue_fin(t, pp.peer, pp.send_id, M4D_ERR_TRANSFER, 0);
-            complete(t, pp.recv, M4D_ERR_CUDA, 0);
+            finish_pulled(t, pp.recv, M4D_ERR_CUDA, 0);
         }
     };
     std::vector<PendingPull>& v = t->pending_pulls;
@@ -1327,10 +1395,10 @@ int poll_copies(m4d_transport* t) {
                 pull_done(t, c.src);
                 if (e == cudaSuccess) {
                     queue_fin(t, c.peer, c.send_id, M4D_OK, c.bytes);
-                    complete(t, c.recv, M4D_OK, c.bytes);
+                    finish_pulled(t, c.recv, M4D_OK, c.bytes);
                 } else {
                     queue_fin(t, c.peer, c.send_id, M4D_ERR_TRANSFER, 0);
-                    complete(t, c.recv, M4D_ERR_CUDA, 0);
+                    finish_pulled(t, c.recv, M4D_ERR_CUDA, 0);
                 }
                 ++n;
             }
@@ -1685,6 +1753,13 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
     raw->domain = domain;
     raw->device = (on_device & 1) && cap > 0;
     raw->loan_ok = (on_device & 2) != 0;  // an eager device message may complete it by loan
+    raw->loan_only = (on_device & 4) != 0;
+    if (raw->loan_only) {  // no buffer: the transport provides the memory it lends
+        if (!(on_device & 1) || t->device < 0) return fail(M4D_ERR_USAGE, "loan-only receives are device receives");
+        raw->loan_ok = true;
+        raw->device = true;
+        raw->ptr = nullptr;
+    }
     if (raw->device && t->device < 0) return fail(M4D_ERR_USAGE, "device buffer on a host-only transport");
     t->reqs[req_id] = std::move(r);
     const size_t before = t->done.size();
@@ -1875,6 +1950,10 @@ int m4d_transport_take_loan(m4d_transport* t, uint64_t req_id, uint64_t* ptr, ui
 }
 
 m4d_status m4d_transport_release_loan(m4d_transport* t, uint64_t token) {
+    if (token & kPoolToken) {
+        recv_slot_put(t, reinterpret_cast<uint8_t*>(token & ~kPoolToken));
+        return M4D_OK;
+    }
     const int peer = static_cast<int>(token >> 48);
     if (peer < 0 || peer >= t->world || peer == t->rank) return fail(M4D_ERR_USAGE, "invalid loan token");
     dev_release(t, peer, token & ((uint64_t(1) << 48) - 1));
@@ -1919,6 +1998,8 @@ m4d_status m4d_transport_close(m4d_transport* t) {
         cudaStreamDestroy(t->eager_stream);
     }
     if (t->dev_ring) cudaFree(t->dev_ring);
+    for (void* slab : t->recv_slabs) cudaFree(slab);
+    for (auto& kv : t->recv_big) cudaFree(kv.second);
     if (t->pq) cudaFreeHost(t->pq);
     if (t->proxy_state) cudaFree(t->proxy_state);
     if (t->me_registered) cudaHostUnregister(t->me);

@@ -24,6 +24,7 @@ torchrun rendezvous).  Ranks may also share one process (test mode).
 from __future__ import annotations
 
 import ctypes
+import struct
 import os
 import weakref
 
@@ -286,11 +287,13 @@ class NvlinkTransport(Transport):
         return self._track(req)
 
     def post_recv_framed(self, kind: int, channel: int, peer: int, tag: int, max_chunk: int) -> TransferRequest:
-        """One request that receives a whole framed transfer (see :meth:`take_framed`)."""
+        """One request that receives a whole framed transfer (see :meth:`take_framed`).  A
+        transfer whose only frame is a device frame of at most ``eager_device_max`` bytes
+        is received natively too, by loan."""
         self._check_route(channel, peer)
         req = TransferRequest(self, "recv", channel, peer, tag, _Extent(0), MemoryDomain.HOST)
         try:
-            done = self._fast.recv_framed(self._h, kind, channel, peer, tag, max_chunk, req.id)
+            done = self._fast.recv_framed(self._h, kind, channel, peer, tag, max_chunk, req.id, self.eager_device_max)
         except OSError as exc:
             raise native.error_for(exc.args[0], native.last_error()) from None
         if done is None:
@@ -300,10 +303,20 @@ class NvlinkTransport(Transport):
         return self._track(req)
 
     def take_framed(self, req: TransferRequest):
-        """(outcome, header bytes, payload bytearray or None, (offset, expected, actual)) of a
-        finished receive composite: outcome 0 = all host frames received, 1 = header only (the
-        caller finishes the transfer), 2 = end of stream, 3 = a slice came short."""
-        return self._fast.take_framed(req.id)
+        """(outcome, header bytes, payload, (offset, expected, actual)) of a finished receive
+        composite: outcome 0 = the frames were received (payload: a bytearray of the host
+        frames, or the :class:`CudaRegion` lent for a lone device frame), 1 = header only
+        (the caller finishes the transfer), 2 = end of stream, 3 = a slice came short."""
+        outcome, raw, payload, detail = self._fast.take_framed(req.id)
+        if isinstance(payload, tuple):  # a lone device frame, lent (ring bytes or a receive slot)
+            nbytes = struct.unpack_from("<Q", raw, 0 if len(raw) == 10 else 4)[0]
+            payload = self._lent(payload[0], payload[1], nbytes)
+        return outcome, raw, payload, detail
+
+    def _lent(self, ptr: int, token: int, nbytes: int) -> CudaRegion:
+        region = CudaRegion(nbytes, self.device, ptr=ptr, owner=_Loan(self, token))
+        self._loans.add(region)
+        return region
 
     def post_send(self, channel: int, peer: int, tag: int, data,
                   domain: MemoryDomain = MemoryDomain.HOST) -> TransferRequest:
@@ -337,9 +350,7 @@ class NvlinkTransport(Transport):
         got = self._fast.loan(self._h, req.id)
         if got is None:
             return None
-        region = CudaRegion(req.bytes_moved, self.device, ptr=got[0], owner=_Loan(self, got[1]))
-        self._loans.add(region)
-        return region
+        return self._lent(got[0], got[1], req.bytes_moved)
 
     def _evacuate_loans(self) -> None:
         """Before the ring goes away (close): move every loaned region still alive into its

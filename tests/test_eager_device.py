@@ -246,3 +246,54 @@ def test_copy_engine_eager_path_when_the_proxy_is_off():
     out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
                          env=dict(os.environ, M4D_EAGER_PROXY="0"))
     assert out.returncode == 0 and "ok" in out.stdout, out.stdout[-2000:] + out.stderr[-2000:]
+
+
+def test_framed_device_frames_fall_back_to_receive_slots_when_the_ring_is_full():
+    """The native composites receive a lone small device frame by a loan-only receive:
+    eager frames are lent from the ring; once held frames fill the ring, later ones come by
+    rendezvous into transport receive slots, which are lent the same way and recycled."""
+    from paper_2101_08878_b200.loop import gather
+    from paper_2101_08878_b200.messaging import Frame, Message, read_message, recv_payload, send_payload, \
+        write_message
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    from nvlink_fixtures import nvlink_world
+
+    loop, ts, tables = nvlink_world(2, 0)
+    try:
+        n = 60 << 10
+        src = [dev(n, pattern(n, k)) for k in range(4)]
+
+        async def one(k, held):
+            frame = Frame(src[k % 4], n, MemoryDomain.DEVICE)
+            if k % 2:
+                _, got = await gather(send_payload(ts[0], tables[0].lookup(1), 40, frame),
+                                      recv_payload(ts[1], tables[1].lookup(0), 40))
+            else:
+                _, msg = await gather(write_message(ts[0], tables[0].lookup(1), Message([frame])),
+                                      read_message(ts[1], tables[1].lookup(0)))
+                got = msg.frames[0]
+            assert got.domain == MemoryDomain.DEVICE
+            held.append((k, got))
+
+        held = []
+
+        async def run(count):
+            for k in range(count):
+                await one(k, held)
+
+        loop.run_until_complete(run(100))  # 100 x 60 KiB held > the 4 MiB ring region
+        assert all(f.to_bytes() == pattern(n, k % 4).tobytes() for k, f in held)
+        st = stats(ts[1])
+        assert st["rendezvous_pulls"] > 0 and st["eager_device_loans"] > 0
+        assert st["eager_device_loans"] + st["rendezvous_pulls"] == 100
+        held.clear()
+        import gc
+
+        gc.collect()
+        before = stats(ts[1])["rendezvous_pulls"]
+        loop.run_until_complete(run(40))  # slots and ring given back: eager again
+        assert stats(ts[1])["rendezvous_pulls"] == before
+        assert all(f.to_bytes() == pattern(n, k % 4).tobytes() for k, f in held)
+    finally:
+        close_all(ts)
