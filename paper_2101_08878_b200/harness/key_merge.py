@@ -372,40 +372,43 @@ class KeyMerge:
         t, P, me, C, lib = self.transport, self.world, self.rank, self.coarse_push, native.lib()
         if self._peer_recv is None:
             await self._connect_push()
-        plan_streams = [self.stream, self.plan_stream]  # the two sides' plans run side by side
+        # Side 0's plan runs alone, so its push starts as early as possible; side 1's plan
+        # runs on the plan stream beside that push (the push leaves SMs free, M4D_PUSH_SMS),
+        # and its run tables are exchanged while side 0's rows move.
+        plan_streams = [self.stream, self.plan_stream]
+        width = P * (C + 1)
+        runs_in = [None, None]
         for side in range(2):
             native.set_device(self.device)  # ranks of one process may sit on different GPUs
             native.check(lib.m4d_partition_owner_plan(
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.rank_bounds[side].ptr,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, plan_streams[side].handle))
-        self.launches += 10
-        blob = b""
-        for side in range(2):  # my rows per (owner, coarse run), relative to each owner's segment
+            self.launches += 5
             b = self._read_bounds(self.rank_bounds[side], P * C, plan_streams[side])
-            if side == 1:
-                self._tp("plans_done")
-            blob += struct.pack(f"<{P * (C + 1)}q", *[b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)])
-        width = P * (C + 1)
-        tables = [struct.unpack(f"<{2 * width}q", x) for x in await allgather(t, blob, EXCHANGE_TAG + 2)]
-        runs_in = [[tables[src][side * width + me * (C + 1):side * width + (me + 1) * (C + 1)] for src in range(P)]
-                   for side in range(2)]
-        for side in range(2):
-            for d in range(P):
-                if sum(tables[src][side * width + d * (C + 1) + C] for src in range(P)) > self._peer_cap[side][d]:
-                    return None
-        self._mark("owner_plan_and_tables_ms")
-        for side in range(2):
+            self._tp(f"plan{side}_done", plan_streams[side])
+            # my rows per (owner, coarse run), relative to each owner's segment
+            blob = struct.pack(f"<{width}q", *[b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)])
+            tables = [struct.unpack(f"<{width}q", x) for x in await allgather(t, blob, EXCHANGE_TAG + 2 + 7 * side)]
+            runs_in[side] = [tables[src][me * (C + 1):(me + 1) * (C + 1)] for src in range(P)]
+            if any(sum(tables[src][d * (C + 1) + C] for src in range(P)) > self._peer_cap[side][d] for d in range(P)):
+                # a receive buffer is too small: every rank sees the same tables and falls back
+                # together, once side 0's pushes (if any) have landed everywhere
+                if side == 1:
+                    self.pushed[0].synchronize()
+                    await allgather(t, b"\x00", EXCHANGE_TAG + 10)
+                return None
             dest = (ctypes.c_uint64 * P)()
             for d in range(P):  # my segment in owner d's buffer: after the rows of lower sources
-                before = sum(tables[src][side * width + d * (C + 1) + C] for src in range(me))
+                before = sum(tables[src][d * (C + 1) + C] for src in range(me))
                 dest[d] = self._peer_recv[side][d] + before * 16
             self._tp(f"push{side}_start")
-            native.set_device(self.device)  # ranks of one process may sit on different GPUs
+            native.set_device(self.device)
             native.check(lib.m4d_partition_owner_push(
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
             self.pushed[side].record(self.stream)
             self._tp(f"push{side}_end")
+        self._mark("owner_plan_push_ms")
         self.launches += 2
         out = []
         for side in range(2):
