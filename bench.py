@@ -647,7 +647,11 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
         "n_gpus": 2, "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
         "config": {"workload": "p2p", "sizes": [r["size"] for r in rows], "window": 64},
-        "latency_1B_us": rows[0]["osu_latency_us"], "sweep": rows,
+        # 1 B device frame, transport layer: the protocol the transport picks for that size
+        # (eager when the ring exists), the rendezvous figure beside it
+        "latency_1B_us": eager_lat.get(1, rows[0]["osu_latency_us"]),
+        "latency_1B_protocol": "eager" if 1 in eager_lat else "rendezvous",
+        "rendezvous_latency_1B_us": rows[0]["osu_latency_us"], "sweep": rows,
         "device_eager_latency_us": {str(k): v for k, v in eager_lat.items()},
         "host_frames_1B": {"osu_latency_us": host_lat,
                            "comm_path_latency_us": host_pp["mean_s"] * 1e6 if host_pp else None},
