@@ -137,6 +137,7 @@ typedef struct m4d_transport_stats {
     uint64_t eager_device_sends;   /* device payloads sent by the eager protocol    */
     uint64_t eager_device_loans;   /* eager device messages received by loan        */
     uint64_t eager_proxy_copies;   /* eager device sends copied by the proxy kernel */
+    uint64_t eager_proxy_launches; /* proxy kernel launches (it exits when idle)     */
 } m4d_transport_stats;
 
 /* transport_init: publishes this rank and maps the peers that are already up

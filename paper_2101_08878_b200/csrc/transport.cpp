@@ -1015,6 +1015,7 @@ int ensure_proxy(m4d_transport* t) {
     if (*alive) return M4D_OK;
     *alive = 1;
     cudaSetDevice(t->device);
+    t->stats.eager_proxy_launches++;
     return m4d::launch_eager_proxy(t->pq_dev, t->proxy_state, t->proxy_done_dev, eager_proxy_idle_ns(),
                                    t->proxy_stream);
 }

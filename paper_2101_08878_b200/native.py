@@ -101,7 +101,8 @@ class TransportStats(ctypes.Structure):
     _fields_ = [(name, ctypes.c_uint64) for name in (
         "sends_completed", "recvs_completed", "bytes_sent", "bytes_received", "eager_bytes",
         "nvlink_bytes", "rendezvous_pulls", "unexpected_messages", "pull_kernel_launches",
-        "eager_device_sends", "eager_device_loans", "eager_proxy_copies")]
+        "eager_device_sends", "eager_device_loans", "eager_proxy_copies",
+        "eager_proxy_launches")]
 
 
 # name -> (restype, argtypes); every symbol include/m4d.h declares.

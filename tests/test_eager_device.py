@@ -297,3 +297,36 @@ def test_framed_device_frames_fall_back_to_receive_slots_when_the_ring_is_full()
         assert all(f.to_bytes() == pattern(n, k % 4).tobytes() for k, f in held)
     finally:
         close_all(ts)
+
+
+def test_proxy_kernel_stays_up_under_traffic_and_exits_when_idle(pair):
+    """Back-to-back eager sends are served by one proxy launch; after the idle timeout
+    (M4D_EAGER_PROXY_IDLE_US, 100 us) the kernel has exited and the next send relaunches it."""
+    import time
+
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    n = 256
+    src, dst = dev(n, pattern(n, 5)), dev(n)
+
+    def one():
+        s = pair[0].post_send_eager(0, 1, 14, src.window())
+        r = pair[1].post_recv(0, 0, 14, dst.window(), MemoryDomain.DEVICE)
+        pump(pair, s, r)
+        assert dst.to_bytes() == pattern(n, 5).tobytes()
+
+    one()
+    first = stats(pair[0])["eager_proxy_launches"]
+    assert first >= 1
+    for _ in range(50):  # far less than 100 us apart
+        s = pair[0].post_send_eager(0, 1, 15, src.window())
+        pump(pair, s)
+    busy = stats(pair[0])["eager_proxy_launches"] - first
+    assert busy <= 2  # the kernel stayed up (a launch or so if the host was slow)
+    time.sleep(0.05)  # far beyond the idle timeout
+    before = stats(pair[0])["eager_proxy_launches"]
+    one()
+    assert stats(pair[0])["eager_proxy_launches"] == before + 1
+    for _ in range(50):  # drain tag 15
+        r = pair[1].post_recv(0, 0, 15, dst.window(), MemoryDomain.DEVICE)
+        pump(pair, r)
