@@ -103,6 +103,17 @@ __global__ void generate_kernel(int64_t* keys, int64_t* vals, int64_t row0, int6
     }
 }
 
+// L2 bulk prefetch of elements [a, min(a + count, end)) of an array (16-byte
+// aligned pieces only; a no-op on anything else).
+template <typename T>
+__device__ __forceinline__ void l2_prefetch(const T* p, int64_t a, int64_t count, int64_t end) {
+    const int64_t z = a + count < end ? a + count : end;
+    if (z <= a) return;
+    const uint32_t b = static_cast<uint32_t>((static_cast<uint64_t>(z - a) * sizeof(T)) & ~uint64_t(15));
+    if (b && (reinterpret_cast<uintptr_t>(p + a) & 15) == 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + a), "r"(b) : "memory");
+}
+
 // Key of row i: SoA input (vals != null) or 16-byte (key, payload) pairs.
 __device__ __forceinline__ int64_t key_at(const int64_t* keys, const int64_t* vals, int64_t i) {
     return vals ? __ldcs(keys + i) : __ldcs(keys + 2 * i);
@@ -357,6 +368,24 @@ struct PushTargets {
     longlong2* seg[kMaxPushOwners];
 };
 
+// L2 bulk prefetch of rows [r0, min(r0 + rows, hi)) of SoA columns (or 16-byte pairs).
+__device__ __forceinline__ void l2_prefetch_rows(const int64_t* keys, const int64_t* vals, int64_t r0, int64_t hi,
+                                                 int rows) {
+    const int64_t r1 = r0 + rows < hi ? r0 + rows : hi;
+    if (r1 <= r0) return;
+    auto pf = [](const void* p, uint64_t bytes) {
+        const uint32_t b = static_cast<uint32_t>(bytes & ~uint64_t(15));
+        if (b && (reinterpret_cast<uintptr_t>(p) & 15) == 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(b) : "memory");
+    };
+    if (vals) {
+        pf(keys + r0, static_cast<uint64_t>(r1 - r0) * 8);
+        pf(vals + r0, static_cast<uint64_t>(r1 - r0) * 8);
+    } else {
+        pf(keys + 2 * r0, static_cast<uint64_t>(r1 - r0) * 16);
+    }
+}
+
 template <int kT, bool kPush, bool kBulk>
 __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile_scatter_kernel(const int64_t* __restrict__ keys,
                                                                        const int64_t* __restrict__ vals, int64_t n,
@@ -364,7 +393,7 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
                                                                        const int64_t* __restrict__ offsets,
                                                                        longlong2* __restrict__ out,
                                                                        const __grid_constant__ PushTargets push,
-                                                                       bool atomic_rank) {
+                                                                       bool atomic_rank, int tile_prefetch) {
     constexpr int kTileRows = kT * kRowsPerThread;
     extern __shared__ __align__(16) unsigned char tsm[];
     longlong2* stage = reinterpret_cast<longlong2*>(tsm);
@@ -393,7 +422,12 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         }
     }
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
+    const int pf = tile_prefetch;  // tiles prefetched ahead
+    if (pf && threadIdx.x == 0) l2_prefetch_rows(keys, vals, lo, hi, pf * kTileRows);
     for (int64_t tile = lo; tile < hi; tile += kTileRows) {
+        // the next tile(s) stream into L2 while this one is ranked, staged and copied out
+        if (pf && threadIdx.x == 0 && tile + pf * kTileRows < hi)
+            l2_prefetch_rows(keys, vals, tile + pf * kTileRows, hi, kTileRows);
         // 1-2. load (warp w owns rows [tile + 256 w, tile + 256 w + 256)) and rank each
         // row among the warp's rows of its bucket.  Full tiles and 256 buckets (the
         // common case) run without per-row bounds or bit-count checks.
@@ -507,7 +541,7 @@ template <bool kPacked>
 __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__ keys,
                                                      const int64_t* __restrict__ vals, int64_t n, int64_t run,
                                                      int log2b, int b1, int groups, uint32_t* __restrict__ hist_top,
-                                                     unsigned long long* __restrict__ hist_grp) {
+                                                     unsigned long long* __restrict__ hist_grp, bool pf) {
     extern __shared__ uint32_t h2[];  // 2^log2b 16-bit counters
     __shared__ uint32_t top[256];
     __shared__ int overflow;
@@ -519,7 +553,14 @@ __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__
     if (threadIdx.x == 0) overflow = 0;
     __syncthreads();
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
-    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
+    auto prefetch = [&](int64_t a) {  // keys only: a SoA key column, or the pairs
+        if (vals) l2_prefetch(keys, a, chunk, hi);
+        else l2_prefetch(reinterpret_cast<const longlong2*>(keys), a, chunk, hi);
+    };
+    if (pf && threadIdx.x == 0) prefetch(lo);
+    for (int64_t base = lo; base < hi; base += chunk) {
+        if (pf && threadIdx.x == 0) prefetch(base + chunk);
         int64_t k[kRowsPerThread];
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u) {
@@ -619,11 +660,15 @@ __global__ void exclusive_scan_u64_kernel(const unsigned long long* __restrict__
 }
 
 // Second-level scatter of rows [lo, hi) of `in` by the low bits of their local
-// partition id, through per-partition cursors in shared memory.
+// partition id, through per-partition cursors in shared memory.  pf: thread 0
+// prefetches the next chunk into L2 while the CTA scatters this one.
 __device__ __forceinline__ void scatter_by_low_bits(const longlong2* __restrict__ in, int64_t lo, int64_t hi,
                                                     uint32_t* cursor, int log2b, uint32_t mask,
-                                                    longlong2* __restrict__ out) {
-    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+                                                    longlong2* __restrict__ out, bool pf) {
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
+    if (pf && threadIdx.x == 0) l2_prefetch(in, lo, chunk, hi);
+    for (int64_t base = lo; base < hi; base += chunk) {
+        if (pf && threadIdx.x == 0) l2_prefetch(in, base + chunk, chunk, hi);
         longlong2 row[kRowsPerThread];
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u) {
@@ -649,7 +694,8 @@ __device__ __forceinline__ void scatter_by_low_bits(const longlong2* __restrict_
 __global__ void __launch_bounds__(1024)
     scatter_pass2_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ offs, int ctas, int64_t n,
                          const unsigned long long* __restrict__ grp_before, int groups,
-                         const int64_t* __restrict__ bounds, int log2b, int b1, longlong2* __restrict__ out) {
+                         const int64_t* __restrict__ bounds, int log2b, int b1, longlong2* __restrict__ out,
+                         bool pf) {
     extern __shared__ uint32_t cursor[];  // 2^(log2b - b1)
     const int sub = 1 << (log2b - b1);
     const int seg = blockIdx.x / groups, g = blockIdx.x % groups;
@@ -663,7 +709,7 @@ __global__ void __launch_bounds__(1024)
     const int64_t entries = static_cast<int64_t>(ctas) << b1;
     const int64_t i0 = static_cast<int64_t>(seg) * ctas + k0, i1 = static_cast<int64_t>(seg) * ctas + k1;
     const int64_t lo = i0 < entries ? offs[i0] : n, hi = i1 < entries ? offs[i1] : n;
-    scatter_by_low_bits(in, lo, hi, cursor, log2b, static_cast<uint32_t>(sub - 1), out);
+    scatter_by_low_bits(in, lo, hi, cursor, log2b, static_cast<uint32_t>(sub - 1), out, pf);
 }
 
 // Receiver side of the owner+coarse exchange (M4D_PART_OWNER_COARSE): S
@@ -683,7 +729,7 @@ __device__ __forceinline__ void piece_range(const int64_t* __restrict__ runs, in
 
 __global__ void __launch_bounds__(1024) runs_hist_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ runs,
                                                          int sources, int groups, int log2b, int cbits,
-                                                         unsigned long long* __restrict__ hist_grp) {
+                                                         unsigned long long* __restrict__ hist_grp, bool pf) {
     extern __shared__ uint32_t h[];  // 2^(log2b - cbits)
     const int sub = 1 << (log2b - cbits), buckets = 1 << log2b;
     const int g = blockIdx.x % groups, piece = blockIdx.x / groups;  // piece = c * sources + src
@@ -692,7 +738,10 @@ __global__ void __launch_bounds__(1024) runs_hist_kernel(const longlong2* __rest
     __syncthreads();
     int64_t a, z;
     piece_range(runs, piece, g, groups, &a, &z);
-    for (int64_t base = a; base < z; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
+    if (pf && threadIdx.x == 0) l2_prefetch(in, a, chunk, z);
+    for (int64_t base = a; base < z; base += chunk) {
+        if (pf && threadIdx.x == 0) l2_prefetch(in, base + chunk, chunk, z);
         int64_t k[kRowsPerThread];
 #pragma unroll
         for (int u = 0; u < kRowsPerThread; ++u) {
@@ -712,7 +761,7 @@ __global__ void __launch_bounds__(1024) runs_hist_kernel(const longlong2* __rest
 __global__ void __launch_bounds__(1024)
     runs_pass2_kernel(const longlong2* __restrict__ in, const int64_t* __restrict__ runs, int sources, int groups,
                       const unsigned long long* __restrict__ grp_before, const int64_t* __restrict__ bounds,
-                      int log2b, int cbits, longlong2* __restrict__ out) {
+                      int log2b, int cbits, longlong2* __restrict__ out, bool pf) {
     extern __shared__ uint32_t cursor[];  // 2^(log2b - cbits)
     const int sub = 1 << (log2b - cbits), buckets = 1 << log2b;
     const int g = blockIdx.x % groups, piece = blockIdx.x / groups;
@@ -723,7 +772,7 @@ __global__ void __launch_bounds__(1024)
     __syncthreads();
     int64_t a, z;
     piece_range(runs, piece, g, groups, &a, &z);
-    scatter_by_low_bits(in, a, z, cursor, log2b, static_cast<uint32_t>(sub - 1), out);
+    scatter_by_low_bits(in, a, z, cursor, log2b, static_cast<uint32_t>(sub - 1), out, pf);
 }
 
 __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int buckets, int ctas, int64_t total,
@@ -1034,6 +1083,21 @@ static bool tile_rank_atomic() {
     return a;
 }
 
+// L2 bulk prefetch of the next chunk in every streaming partition pass (tile
+// scatter, histograms, pass 2, the receiver split), M4D_L2_PF (default 1; 0
+// off): the loads of a chunk then hit L2 instead of waiting on HBM.  Measured at
+// 1e8 rows/side (tools/sweeps/r2_stream_pf*.sh): merge step 4.81 -> 4.62 ms
+// (N=1); the tile scatter alone gives 0.16 ms of it.  Prefetching the tile
+// scatter 2 or 3 tiles ahead is slower (4.78 / 4.93 ms: the lines are evicted
+// before use), so the distance stays one chunk.
+static int l2_pf() {
+    static const int a = [] {
+        const char* v = getenv("M4D_L2_PF");
+        return v && atoi(v) <= 0 ? 0 : 1;
+    }();
+    return a;
+}
+
 template <int kT, bool kPush, bool kBulk>
 static cudaError_t launch_tile_scatter_t(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
                                          int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
@@ -1043,7 +1107,8 @@ static cudaError_t launch_tile_scatter_t(int ctas, cudaStream_t s, const int64_t
                                                static_cast<int>(tile_smem<kT>()));
     if (e != cudaSuccess) return e;
     tile_scatter_kernel<kT, kPush, kBulk><<<ctas, kT, tile_smem<kT>(), s>>>(keys, vals, n, run, mode, buckets, log2b,
-                                                                          offs, out, push, tile_rank_atomic());
+                                                                          offs, out, push, tile_rank_atomic(),
+                                                                          l2_pf());
     return cudaGetLastError();
 }
 
@@ -1201,7 +1266,7 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
         M4D_CUDA_TRY(cudaMemsetAsync(hist_grp, 0, groups * buckets * sizeof(unsigned long long), s));
         (packed ? hist2_kernel<true> : hist2_kernel<false>)<<<ctas, 1024, hist_smem, s>>>(keys, vals, n, run, log2b, b1,
-                                                                                        groups, hist, hist_grp);
+                                                                                        groups, hist, hist_grp, l2_pf());
         scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
         scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
         scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
@@ -1210,7 +1275,8 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, groups, buckets, hist_all);
         exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
         scatter_pass2_kernel<<<fan * groups, 1024, (buckets >> b1) * sizeof(uint32_t), s>>>(
-            tmp, offs, ctas, n, hist_grp, groups, bounds, log2b, b1, reinterpret_cast<longlong2*>(out_pairs));
+            tmp, offs, ctas, n, hist_grp, groups, bounds, log2b, b1, reinterpret_cast<longlong2*>(out_pairs),
+            l2_pf());
         M4D_CUDA_TRY(cudaGetLastError());
         return M4D_OK;
     }
@@ -1336,12 +1402,12 @@ m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t*
     const int ctas = coarse * sources * groups;
     const size_t sub_smem = static_cast<size_t>(buckets >> cbits) * sizeof(uint32_t);
     runs_hist_kernel<<<ctas, runs_threads(), sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
-                                                  log2b, cbits, hist_grp);
+                                                  log2b, cbits, hist_grp, l2_pf());
     group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, sources * groups, buckets, hist_all);
     exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
     runs_pass2_kernel<<<ctas, runs_threads(), sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs, sources, groups,
                                                    hist_grp, bounds, log2b, cbits,
-                                                   reinterpret_cast<longlong2*>(out_pairs));
+                                                   reinterpret_cast<longlong2*>(out_pairs), l2_pf());
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }
