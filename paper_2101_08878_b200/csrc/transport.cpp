@@ -435,6 +435,7 @@ struct m4d_transport {
     uint64_t* proxy_done_dev = nullptr;
     cudaStream_t proxy_stream = nullptr;
     bool me_registered = false;
+    bool proxy_broken = false;                                  // a launch failed: copy engine from then on
     uint64_t proxy_seq = 0;                                     // commands issued
     std::deque<Req*> proxy_sends;                               // issued, copy not yet done (seq order)
     std::vector<EagerCopy> eager_copies;
@@ -1038,6 +1039,12 @@ bool push_proxied(m4d_transport* t, Peer& p, Req* r) {
     slot[2] = r->len | tag;
     t->proxy_seq = seq;
     const int st = ensure_proxy(t);
+    if (st != M4D_OK) {
+        // no kernel: void the command (a later kernel must never run it -- the receiver
+        // frees the slot of a failed record) and send eager copies by the copy engine
+        slot[2] = r->len | ((seq + 1) & 0xffff) << m4d::kProxyTagShift;
+        t->proxy_broken = true;
+    }
     EagerDevRec* rec = reinterpret_cast<EagerDevRec*>(w);
     rec->h.bytes = sizeof(EagerDevRec);
     rec->h.kind = kEagerDev;
@@ -1187,7 +1194,7 @@ bool try_eager(m4d_transport* t, int q, Req* r) {
     const uint64_t head = dev_heads(p.seg)[t->rank].load(std::memory_order_acquire);
     if (pos + need - head > cap) return false;  // full: the receiver still holds those slots
     const uint64_t top = uint64_t(1) << m4d::kProxyTagShift;
-    if (t->pq && reinterpret_cast<uint64_t>(r->ptr) < top && reinterpret_cast<uint64_t>(p.dev_out + off) < top &&
+    if (t->pq && !t->proxy_broken && reinterpret_cast<uint64_t>(r->ptr) < top && reinterpret_cast<uint64_t>(p.dev_out + off) < top &&
         r->len < top) {
         p.dev_prod = pos + need;
         t->stats.eager_device_sends++;
