@@ -795,7 +795,7 @@ __global__ void bucket_bounds_kernel(const int64_t* __restrict__ offsets, int bu
 // (re-walking only rows with several matches); (4) the warp emits the stage
 // with all 32 lanes: coalesced output stores, full-width row hashes.
 // Indices are 32-bit offsets from the partition start.
-template <int kJoinThreads, int kSlotBits, int kChunk, int kStage, int kMinBlocks>
+template <int kJoinThreads, int kSlotBits, int kChunk, int kStage, int kMinBlocks, int kKeep>
 __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
     join_kernel(const longlong2* __restrict__ build, const int64_t* __restrict__ loff,
                 const longlong2* __restrict__ probe, const int64_t* __restrict__ roff, int64_t* __restrict__ ok,
@@ -878,20 +878,27 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
                 const int j = base + u * T + threadIdx.x;
                 r[u] = j < pn ? prow[j].x : 0;
             }
-            uint32_t info[kPer];  // first matching build row | min(matches, 0xffff) << 16
+            // first matching build row | min(matches, 0xffff) << 16, and the second and
+            // third matches (16 bits each): with duplicate keys (Poisson(1) copies per key
+            // here) 42 % of the matched rows have two or more, and keeping two more
+            // indices leaves a re-walk below to the 3 % with four or more
+            uint32_t info[kPer], second[kPer];
             uint32_t mine = 0;
 #pragma unroll
             for (int u = 0; u < kPer; ++u) {  // (1) count
                 info[u] = 0;
+                second[u] = 0;
                 if (base + u * T + static_cast<int>(threadIdx.x) >= pn) continue;
-                uint32_t c = 0, first = 0;
+                uint32_t c = 0, first = 0, sec = 0;
                 const uint32_t h0 = head[slot_of<kSlotBits>(r[u])];
                 for (uint32_t i = h0 == kEmpty ? kNil : h0; i != kNil; i = link[i])
                     if (bkey[i] == r[u]) {
+                        if (kKeep > 1) sec = c == 1 ? i : (kKeep > 2 && c == 2) ? sec | i << 16 : sec;
                         first = c ? first : i;
                         ++c;
                     }
                 info[u] = first | (c < 0xffffu ? c : 0xffffu) << 16;
+                second[u] = sec;
                 mine += c;
             }
             uint32_t incl = mine;
@@ -915,9 +922,17 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
                         if (!c) continue;
                         const uint32_t loc = static_cast<uint32_t>(u * T + threadIdx.x) << kIdxBits;
                         const uint32_t first = info[u] & 0xffffu;
-                        if (c == 1) {
+                        if (c <= static_cast<uint32_t>(kKeep)) {
                             if (e >= win && e < win + kStage) stage[e - win] = loc | first;
                             ++e;
+                            if (kKeep > 1 && c >= 2) {
+                                if (e >= win && e < win + kStage) stage[e - win] = loc | (second[u] & 0xffffu);
+                                ++e;
+                            }
+                            if (kKeep > 2 && c == 3) {
+                                if (e >= win && e < win + kStage) stage[e - win] = loc | (second[u] >> 16);
+                                ++e;
+                            }
                             continue;
                         }
                         for (uint32_t i = first; i != kNil; i = link[i]) {
@@ -1353,6 +1368,19 @@ static int join_pf_ahead() {
     return v;
 }
 
+// Matches per probe row the count walk keeps, so staging them needs no second walk
+// of the chain (M4D_JOIN_KEEP = 1..3, default 2).  Same box, 1e8 rows/side
+// (tools/sweeps/r2_join_second.sh): f = 0.3 join 1.58 / 1.52 / 1.54 ms, f = 1.0
+// 2.50 / 2.47 / 2.38 ms for 1 / 2 / 3.
+static int join_keep() {
+    static const int v = [] {
+        const char* e = getenv("M4D_JOIN_KEEP");
+        const int x = e ? atoi(e) : 2;
+        return x < 1 ? 1 : x > 3 ? 3 : x;
+    }();
+    return v;
+}
+
 static int join_grid(int parts, int per_sm) {
     static const bool persist = [] {
         const char* v = getenv("M4D_JOIN_PERSIST");
@@ -1435,17 +1463,19 @@ m4d_status m4d_hash_join(const int64_t* lpairs, const int64_t* lbounds, const in
         const longlong2* lp = reinterpret_cast<const longlong2*>(lpairs);
         const longlong2* rp = reinterpret_cast<const longlong2*>(rpairs);
         if (join_small()) {
-            auto k = join_kernel<kSmallThreads, kSmallSlotBits, kSmallChunk, kSmallStage, 2>;
+            auto k = join_kernel<kSmallThreads, kSmallSlotBits, kSmallChunk, kSmallStage, 2, 3>;
             M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmallSmem)));
             k<<<join_grid(parts, 2), kSmallThreads, kSmallSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals,
                                                                      out_rvals, capacity, result, result + 1, parts, join_pf(),
                                                                      join_pf_ahead());
         } else {
-            auto k = join_kernel<kJoinThreads, kSlotBits, kChunk, kStage, 1>;
+            auto k = join_keep() == 1 ? join_kernel<kJoinThreads, kSlotBits, kChunk, kStage, 1, 1>
+                     : join_keep() == 2 ? join_kernel<kJoinThreads, kSlotBits, kChunk, kStage, 1, 2>
+                                        : join_kernel<kJoinThreads, kSlotBits, kChunk, kStage, 1, 3>;
             M4D_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kJoinSmem)));
             k<<<join_grid(parts, 1), kJoinThreads, kJoinSmem, s>>>(lp, lbounds, rp, rbounds, out_keys, out_lvals,
                                                                    out_rvals, capacity, result, result + 1, parts, join_pf(),
-                                                                     join_pf_ahead());
+                                                                   join_pf_ahead());
         }
     }
     M4D_CUDA_TRY(cudaGetLastError());
