@@ -35,6 +35,15 @@ __global__ void pull_tiles(Srcs s, double* dst, int tiles_per_src, int pitch) {
     }
 }
 
+// push: every GPU stores its own buffer into each peer's out buffer (its own region
+// there), grid split evenly over destinations -- the write-side mirror of pull_linear
+__global__ void push_linear(Srcs d, const int4* src, size_t n16, int self_slot) {
+    const int dst = blockIdx.x % d.n;
+    const size_t cta = blockIdx.x / d.n, ctas = gridDim.x / d.n;
+    int4* out = const_cast<int4*>(d.p[dst]) + (size_t)self_slot * n16;
+    for (size_t i = cta * blockDim.x + threadIdx.x; i < n16; i += ctas * blockDim.x) out[i] = src[i];
+}
+
 int main() {
     int G = 0;
     CK(cudaGetDeviceCount(&G));
@@ -49,8 +58,9 @@ int main() {
         for (int q = 0; q < G; ++q) if (q != d) cudaDeviceEnablePeerAccess(q, 0);
     }
     const int tiles = (int)(bytes / (2000 * 2000 * 8)) * 31 * 31;
-    for (int mode = 0; mode < 6; ++mode) {
-        const char* names[] = {"linear all-peers", "linear one-peer", "linear local", "tiles all-peers", "tiles one-peer", "tiles local"};
+    for (int mode = 0; mode < 8; ++mode) {
+        const char* names[] = {"linear all-peers", "linear one-peer", "linear local", "tiles all-peers", "tiles one-peer",
+                               "tiles local", "push all-peers", "push one-peer"};
         std::vector<cudaEvent_t> a(G), b(G);
         for (int rep = 0; rep < 2; ++rep) {
             for (int d = 0; d < G; ++d) {
@@ -61,14 +71,18 @@ int main() {
                 CK(cudaSetDevice(d));
                 cudaEventCreate(&a[d]); cudaEventCreate(&b[d]);
                 Srcs s{}; s.n = 0;
-                const int kind = mode % 3;
-                if (kind == 0) { for (int q = 0; q < G; ++q) if (q != d) s.p[s.n++] = buf[q]; }
+                const int kind = mode >= 6 ? (mode == 6 ? 0 : 1) : mode % 3;
+                if (mode >= 6) {  // destinations: the peers' out buffers
+                    if (kind == 0) { for (int q = 0; q < G; ++q) if (q != d) s.p[s.n++] = out[q]; }
+                    else { s.p[s.n++] = out[d ^ 1]; }
+                } else if (kind == 0) { for (int q = 0; q < G; ++q) if (q != d) s.p[s.n++] = buf[q]; }
                 else if (kind == 1) { s.p[s.n++] = buf[d ^ 1]; }
                 else { s.p[s.n++] = buf[d]; }
                 const int grid = 296 / s.n * s.n;
                 cudaEventRecord(a[d]);
                 for (int k = 0; k < 4; ++k) {
-                    if (mode < 3) pull_linear<<<grid, 512>>>(s, out[d], bytes / 16 / s.n);
+                    if (mode >= 6) push_linear<<<grid, 512>>>(s, buf[d], bytes / 16 / G, d);
+                    else if (mode < 3) pull_linear<<<grid, 512>>>(s, out[d], bytes / 16 / s.n);
                     else pull_tiles<<<grid, 256>>>(s, reinterpret_cast<double*>(out[d]), tiles / s.n, 2000);
                 }
                 cudaEventRecord(b[d]);
@@ -78,7 +92,8 @@ int main() {
                 CK(cudaSetDevice(d));
                 CK(cudaEventSynchronize(b[d]));
                 float ms; cudaEventElapsedTime(&ms, a[d], b[d]);
-                const double moved = mode < 3 ? 4.0 * (bytes / 16 / (mode % 3 == 0 ? G - 1 : 1)) * 16 * (mode % 3 == 0 ? G - 1 : 1)
+                const double moved = mode >= 6 ? 4.0 * (bytes / 16 / G) * 16 * (mode == 6 ? G - 1 : 1)
+                                   : mode < 3 ? 4.0 * (bytes / 16 / (mode % 3 == 0 ? G - 1 : 1)) * 16 * (mode % 3 == 0 ? G - 1 : 1)
                                               : 4.0 * (tiles / (mode % 3 == 0 ? G - 1 : 1)) * (mode % 3 == 0 ? G - 1 : 1) * 64.0 * 64 * 8;
                 const double gbs = moved / (ms * 1e-3) / 1e9;
                 worst = gbs < worst ? gbs : worst; sum += gbs;
