@@ -417,10 +417,8 @@ def bench_transpose_sum(args, dist: Dist, peaks: dict) -> dict | None:
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
-        "config": {"workload": "transpose_sum", "dims": n, "block": b, "workers": dist.world,
-                   "ownership": "round-robin row-major (SPEC.md:447)",
-                   "l2": "inputs (25.6 GB x+y) far larger than the 126 MB L2; no flush needed",
-                   "checksum": checksum},
+        "config": ts_config(n, b, dist.world),
+        "checksum": checksum,
         "gpu_launches": launches,
         "roofline": roof,
         "e2e": e2e,
@@ -592,15 +590,35 @@ def bench_key_merge(args, dist: Dist, peaks: dict) -> dict | None:
         "value": step_ms, "unit": "ms", "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_ms, "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
         "dtype": "int64", "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
-        "config": {"workload": "key_merge", "rows_per_side_per_gpu": args.rows, "fraction": args.fraction,
-                   "partitions": km.parts, "digest": list(digest),
-                   "l2": "inputs (3.2 GB per GPU) far larger than the 126 MB L2"},
+        "config": km_config(args), "partitions": km.parts, "digest": list(digest),
         "gpu_launches": launches, "roofline": roof, "e2e": e2e, "cpu_baseline": cpu, "parity": parity,
         "clocks": clocks, "wall_ms_per_step": wall,
     }
 
 
 # -- p2p ---------------------------------------------------------------------------------------------
+
+
+def _l2_note(nbytes: float, what: str) -> str:
+    if nbytes > 8 * 126e6:
+        return f"{what} ({nbytes / 1e9:.1f} GB) far larger than the 126 MB L2; no flush needed"
+    return f"{what} ({nbytes / 1e6:.0f} MB) not flushed between steps (small case)"
+
+
+def ts_config(n: int, b: int, world: int) -> dict:
+    """The transpose_sum workload as both arms name it (identical dicts)."""
+    return {"workload": "transpose_sum", "dims": n, "block": b, "workers": world,
+            "ownership": "round-robin row-major (SPEC.md:447)", "l2": _l2_note(2 * n * n * 8, "inputs x+y")}
+
+
+def km_config(args) -> dict:
+    """The key_merge workload as both arms name it (identical dicts)."""
+    return {"workload": "key_merge", "rows_per_side_per_gpu": args.rows, "fraction": args.fraction,
+            "l2": _l2_note(2 * args.rows * 16, "inputs per GPU")}
+
+
+def p2p_config(args) -> dict:
+    return {"workload": "p2p", "sizes": f"1 B - {args.max_size} B, x4 steps", "window": 64}
 
 
 def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
@@ -642,10 +660,10 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
     best = max(big, key=lambda r: r["osu_bw_GBps"]) if big else rows[-1]
     top = pp[args.max_size]
     return {
-        "metric": "p2p GB/s (osu_bw, device frames, >= 4 MiB)", "value": best["osu_bw_GBps"], "unit": "GB/s",
+        "metric": "p2p GB/s (osu_bw, >= 4 MiB)", "value": best["osu_bw_GBps"], "unit": "GB/s",
         "n_gpus": 2, "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
-        "config": {"workload": "p2p", "sizes": [r["size"] for r in rows], "window": 64},
+        "config": p2p_config(args), "frames": "device (cuda:0 <-> cuda:1)",
         # 1 B device frame, transport layer: the protocol the transport picks for that size
         # (eager when the ring exists), the rendezvous figure beside it
         "latency_1B_us": eager_lat.get(1, rows[0]["osu_latency_us"]),
@@ -849,7 +867,7 @@ def reference_p2p(args) -> dict:
         "impl": "reference", "metric": "p2p GB/s (osu_bw, >= 4 MiB)", "value": ref["value"], "unit": "GB/s",
         "n_gpus": 2, "steps": 1, "warmup": 1, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic byte pattern, verified once per size",
-        "config": {"workload": "p2p", "sizes": [r["size"] for r in ref["sweep"]], "frames": "host (socket)"},
+        "config": p2p_config(args), "frames": "host (reference SocketTransport)",
         "latency_1B_us": ref["latency_1B_us"], "sweep": ref["sweep"], "comm_path": ref["comm_path"],
         "cpu_baseline": {"value": ref["value"], "unit": "GB/s", "cores": 2, "kind": "reference",
                          "sample": ref["sample"]},
@@ -883,7 +901,7 @@ def reference_transpose_sum(args) -> dict:
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
-        "config": {"workload": "transpose_sum", "dims": args.n, "block": args.block},
+        "config": ts_config(args.n, args.block, int(os.environ.get("WORLD_SIZE", "1"))),
         "checksum": _m.fsum(float(v) for v in full["sums"]),
         "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -905,7 +923,7 @@ def reference_key_merge(args) -> dict:
         "value": value, "unit": "ms", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": value, "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
         "data": "synthetic (splitmix64 generator, BASELINE.md §3)",
-        "config": {"workload": "key_merge", "rows_per_side_per_gpu": args.rows, "fraction": args.fraction},
+        "config": km_config(args),
         "cpu_baseline": {"value": value, "unit": "ms", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "digest": list(per[0]["digest"]),
@@ -978,7 +996,8 @@ def main(argv=None) -> int:
             if line is not None and km is not None:
                 line["key_merge"] = {k: km[k] for k in ("metric", "value", "unit", "ms_per_step", "higher_is_better",
                                                         "scaling", "dtype", "config", "gpu_launches", "roofline",
-                                                        "e2e", "cpu_baseline", "parity", "clocks", "wall_ms_per_step")}
+                                                        "e2e", "cpu_baseline", "parity", "clocks", "wall_ms_per_step",
+                                                        "partitions", "digest")}
     finally:
         if getattr(dist, "transport", None) is not None:
             dist.barrier()
