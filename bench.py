@@ -635,6 +635,8 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
         bw = p2p.osu_bw(t, 1 - dist.rank, n, 64, 10 if n <= (1 << 20) else 4, True)
         rows.append({"size": n, "osu_latency_us": lat, "osu_bw_GBps": bw})
         n *= 4
+    # the same 4 MiB window posted with one vectored call (m4d_transport_post_many)
+    vec_4m = p2p.osu_bw(t, 1 - dist.rank, 4 << 20, 64, 4, True, vectored=True) if args.max_size >= (4 << 20) else None
     # the public comm path (send_payload / recv_payload, Listing 2/3) with device frames
     pp = {sz: p2p.pingpong(t, 1 - dist.rank, sz, 1000 if sz < (1 << 20) else 50, True)
           for sz in sorted({1, min(4 << 20, args.max_size), args.max_size})}
@@ -668,6 +670,9 @@ def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
         # (eager when the ring exists), the rendezvous figure beside it
         "latency_1B_us": eager_lat.get(1, rows[0]["osu_latency_us"]),
         "latency_1B_protocol": "eager" if 1 in eager_lat else "rendezvous",
+        "osu_bw_4MiB_vectored_GBps": vec_4m,
+        "osu_bw_note": "windows posted message by message (the OSU loop); osu_bw_4MiB_vectored_GBps: the "
+                       "same 4 MiB window posted with one m4d_transport_post_many call",
         "rendezvous_latency_1B_us": rows[0]["osu_latency_us"], "sweep": rows,
         "device_eager_latency_us": {str(k): v for k, v in eager_lat.items()},
         "host_frames_1B": {"osu_latency_us": host_lat,

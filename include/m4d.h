@@ -170,6 +170,13 @@ m4d_status m4d_transport_post_send(m4d_transport* t, uint32_t channel, int peer,
 m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer, uint32_t tag,
                                    void* ptr, uint64_t cap, int domain, int on_device,
                                    uint64_t req_id, m4d_completion* now);
+/* Vectored post_send / post_recv: `count` posts to one (channel, peer, tag) in
+ * one call (osu_bw's window, a frame's chunks), ptrs[i] / lens[i] with id
+ * req_ids[i]; now[i] as for a single post.  Stops at the first post that fails
+ * and returns its status; *posted = posts made before it. */
+m4d_status m4d_transport_post_many(m4d_transport* t, int is_send, uint32_t channel, int peer, uint32_t tag,
+                                   void* const* ptrs, const uint64_t* lens, int count, int domain, int on_device,
+                                   const uint64_t* req_ids, m4d_completion* now, int* posted);
 /* Eager device protocol: its size threshold (0: no device ring), and the loans
  * of receives posted with on_device bit 1: 1 and (*ptr, *token) when receive
  * req_id was completed by a loan of ring bytes at device address *ptr (valid

@@ -61,11 +61,14 @@ using post_recv_fn = m4d_status (*)(m4d_transport*, uint32_t, int, uint32_t, voi
 using progress_fn = int (*)(m4d_transport*, m4d_completion*, int);
 
 using take_loan_fn = int (*)(m4d_transport*, uint64_t, uint64_t*, uint64_t*);
+using post_many_fn = m4d_status (*)(m4d_transport*, int, uint32_t, int, uint32_t, void* const*, const uint64_t*, int,
+                                    int, int, const uint64_t*, m4d_completion*, int*);
 using release_loan_fn = m4d_status (*)(m4d_transport*, uint64_t);
 
 post_send_fn g_send = nullptr;
 take_loan_fn g_take_loan = nullptr;
 release_loan_fn g_release_loan = nullptr;
+post_many_fn g_post_many = nullptr;
 post_recv_fn g_recv = nullptr;
 progress_fn g_progress = nullptr;
 
@@ -266,11 +269,11 @@ void on_sub(const std::shared_ptr<Framed>& f, uint64_t sub, int status, uint64_t
 }
 
 PyObject* bind(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
-    if (nargs != 3 && nargs != 5) {
-        PyErr_SetString(PyExc_TypeError, "bind(post_send, post_recv, progress[, take_loan, release_loan])");
+    if (nargs != 3 && nargs != 5 && nargs != 6) {
+        PyErr_SetString(PyExc_TypeError, "bind(post_send, post_recv, progress[, take_loan, release_loan[, post_many]])");
         return nullptr;
     }
-    void* p[5];
+    void* p[6];
     for (int i = 0; i < nargs; ++i) {
         p[i] = PyLong_AsVoidPtr(args[i]);
         if (!p[i]) {
@@ -281,10 +284,11 @@ PyObject* bind(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     g_send = reinterpret_cast<post_send_fn>(p[0]);
     g_recv = reinterpret_cast<post_recv_fn>(p[1]);
     g_progress = reinterpret_cast<progress_fn>(p[2]);
-    if (nargs == 5) {
+    if (nargs >= 5) {
         g_take_loan = reinterpret_cast<take_loan_fn>(p[3]);
         g_release_loan = reinterpret_cast<release_loan_fn>(p[4]);
     }
+    if (nargs == 6) g_post_many = reinterpret_cast<post_many_fn>(p[5]);
     Py_RETURN_NONE;
 }
 
@@ -578,6 +582,68 @@ PyObject* forget(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     Py_RETURN_NONE;
 }
 
+// post_many(handle, is_send, channel, peer, tag, addrs, lens, domain, on_device, req_ids)
+//   device payloads only (addrs: device addresses); one C call for the whole window.
+//   -> list of (index, status, bytes) of the posts that completed inline; a failing
+//   post raises OSError(status, posted).
+PyObject* post_many(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
+    if (nargs != 10 || !g_post_many) {
+        PyErr_SetString(PyExc_TypeError, "post_many(handle, is_send, channel, peer, tag, addrs, lens, domain, "
+                                         "on_device, req_ids) (bound with post_many)");
+        return nullptr;
+    }
+    auto* t = static_cast<m4d_transport*>(PyLong_AsVoidPtr(args[0]));
+    const long is_send = PyLong_AsLong(args[1]);
+    const unsigned long channel = PyLong_AsUnsignedLong(args[2]);
+    const long peer = PyLong_AsLong(args[3]);
+    const unsigned long tag = PyLong_AsUnsignedLong(args[4]);
+    const long domain = PyLong_AsLong(args[7]);
+    const long on_device = PyLong_AsLong(args[8]);
+    if (PyErr_Occurred()) return nullptr;
+    PyObject* addrs = args[5];
+    PyObject* lens = args[6];
+    PyObject* ids = args[9];
+    if (!PyTuple_Check(addrs) || !PyTuple_Check(lens) || !PyTuple_Check(ids) ||
+        PyTuple_GET_SIZE(addrs) != PyTuple_GET_SIZE(lens) || PyTuple_GET_SIZE(addrs) != PyTuple_GET_SIZE(ids)) {
+        PyErr_SetString(PyExc_TypeError, "addrs, lens and req_ids must be tuples of one length");
+        return nullptr;
+    }
+    const Py_ssize_t n = PyTuple_GET_SIZE(addrs);
+    std::vector<void*> ptrs(static_cast<size_t>(n));
+    std::vector<uint64_t> sizes(static_cast<size_t>(n)), rid(static_cast<size_t>(n));
+    for (Py_ssize_t i = 0; i < n; ++i) {
+        ptrs[static_cast<size_t>(i)] = PyLong_AsVoidPtr(PyTuple_GET_ITEM(addrs, i));
+        sizes[static_cast<size_t>(i)] = PyLong_AsUnsignedLongLong(PyTuple_GET_ITEM(lens, i));
+        rid[static_cast<size_t>(i)] = PyLong_AsUnsignedLongLong(PyTuple_GET_ITEM(ids, i));
+    }
+    if (PyErr_Occurred()) return nullptr;
+    std::vector<m4d_completion> now(static_cast<size_t>(n));
+    int posted = 0;
+    const m4d_status st = g_post_many(t, is_send ? 1 : 0, static_cast<uint32_t>(channel), static_cast<int>(peer),
+                                      static_cast<uint32_t>(tag), ptrs.data(), sizes.data(), static_cast<int>(n),
+                                      static_cast<int>(domain), static_cast<int>(1 | (on_device & ~1)), rid.data(),
+                                      now.data(), &posted);
+    PyObject* out = PyList_New(0);
+    if (!out) return nullptr;
+    for (int i = 0; i < posted; ++i) {
+        if (now[static_cast<size_t>(i)].status == -1) continue;
+        PyObject* item = Py_BuildValue("(iiK)", i, now[static_cast<size_t>(i)].status,
+                                       static_cast<unsigned long long>(now[static_cast<size_t>(i)].bytes));
+        if (!item || PyList_Append(out, item) != 0) {
+            Py_XDECREF(item);
+            Py_DECREF(out);
+            return nullptr;
+        }
+        Py_DECREF(item);
+    }
+    if (st != M4D_OK) {
+        Py_DECREF(out);
+        PyErr_SetObject(PyExc_OSError, Py_BuildValue("(ii)", st, posted));
+        return nullptr;
+    }
+    return out;
+}
+
 // loan(handle, req_id) -> (device address, token) of a receive completed by loan, or None
 PyObject* loan(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
     if (nargs != 2 || !g_take_loan) {
@@ -606,6 +672,8 @@ PyObject* unloan(PyObject*, PyObject* const* args, Py_ssize_t nargs) {
 }
 
 PyMethodDef methods[] = {
+    {"post_many", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(post_many)), METH_FASTCALL,
+     "post_many(handle, is_send, channel, peer, tag, addrs, lens, domain, on_device, req_ids) -> [(i, status, bytes)]"},
     {"loan", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(loan)), METH_FASTCALL,
      "loan(handle, req_id) -> (device address, token) | None"},
     {"unloan", reinterpret_cast<PyCFunction>(reinterpret_cast<void (*)(void)>(unloan)), METH_FASTCALL,

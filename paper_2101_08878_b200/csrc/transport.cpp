@@ -1808,6 +1808,21 @@ m4d_status m4d_transport_post_recv(m4d_transport* t, uint32_t channel, int peer,
     return M4D_OK;
 }
 
+m4d_status m4d_transport_post_many(m4d_transport* t, int is_send, uint32_t channel, int peer, uint32_t tag,
+                                   void* const* ptrs, const uint64_t* lens, int count, int domain, int on_device,
+                                   const uint64_t* req_ids, m4d_completion* now, int* posted) {
+    *posted = 0;
+    for (int i = 0; i < count; ++i) {
+        const m4d_status st = is_send ? m4d_transport_post_send(t, channel, peer, tag, ptrs[i], lens[i], domain,
+                                                                on_device, req_ids[i], &now[i])
+                                      : m4d_transport_post_recv(t, channel, peer, tag, ptrs[i], lens[i], domain,
+                                                                on_device, req_ids[i], &now[i]);
+        if (st != M4D_OK) return st;
+        *posted = i + 1;
+    }
+    return M4D_OK;
+}
+
 int m4d_transport_progress(m4d_transport* t, m4d_completion* out, int max) {
     map_missing_peers(t);
     // Copies first: a finished pull must send its FIN in this same call, or a

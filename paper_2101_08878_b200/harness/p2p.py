@@ -93,27 +93,36 @@ def _slot(buf, device: bool, k: int, n: int):
     return buf.window(k * n, n) if device else memoryview(buf)[k * n:(k + 1) * n]
 
 
-def osu_bw(transport: Transport, peer: int, n: int, window: int, iters: int, device: bool) -> float:
+def osu_bw(transport: Transport, peer: int, n: int, window: int, iters: int, device: bool,
+           vectored: bool | None = None) -> float:
     """Transport-layer bandwidth in GB/s (measured on rank 0; rank 1 mirrors).
 
     Every message of a window has its own source and destination region (the
     OSU benchmark reuses one buffer, which lets concurrent pulls of identical
-    lines be served once and reports more than the link can carry)."""
+    lines be served once and reports more than the link can carry).
+    ``vectored``: post each device window with one ``post_many`` call instead
+    of the MPI_Isend / MPI_Irecv loop (same posts, same order).  Off by
+    default: measured slower at 1-16 MiB (4 MiB: 584-635 vs 691-697 GB/s,
+    ``profiles/r2_post_many_p2p.txt``) -- the whole window's pulls launch at
+    once and crowd the four pull streams, where the posting loop staggers them."""
     me = transport.rank
     dom = MemoryDomain.DEVICE if device else MemoryDomain.HOST
     buf = _blank(transport, n * window, device)
     views = [_slot(buf, device, k, n) for k in range(window)]
+    many = getattr(transport, "post_many", None) if (device and vectored) else None
     ack = bytearray(4)
     start = None
     for it in range(iters + 1):  # iteration 0 is warm-up
         if it == 1:
             start = time.perf_counter()
         if me == 0:
-            reqs = [transport.post_send(0, peer, DATA_TAG, v, dom) for v in views]
+            reqs = (many("send", 0, peer, DATA_TAG, views, dom) if many
+                    else [transport.post_send(0, peer, DATA_TAG, v, dom) for v in views])
             _wait(transport, *reqs)
             _wait(transport, transport.post_recv(0, peer, ACK_TAG, ack))
         else:
-            reqs = [transport.post_recv(0, peer, DATA_TAG, v, dom) for v in views]
+            reqs = (many("recv", 0, peer, DATA_TAG, views, dom) if many
+                    else [transport.post_recv(0, peer, DATA_TAG, v, dom) for v in views])
             _wait(transport, *reqs)
             _wait(transport, transport.post_send(0, peer, ACK_TAG, b"done"))
     elapsed = time.perf_counter() - start

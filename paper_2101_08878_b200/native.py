@@ -140,6 +140,9 @@ SIGNATURES: dict[str, tuple] = {
                                                _u64, ctypes.c_int, ctypes.c_int, _u64, ctypes.POINTER(Completion)]),
     "m4d_transport_post_recv": (ctypes.c_int, [_c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32, _c_void_p,
                                                _u64, ctypes.c_int, ctypes.c_int, _u64, ctypes.POINTER(Completion)]),
+    "m4d_transport_post_many": (ctypes.c_int, [_c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_int, ctypes.c_uint32,
+                                                _c_void_p, _c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                _c_void_p, _c_void_p, _c_void_p]),
     "m4d_transport_progress": (ctypes.c_int, [_c_void_p, ctypes.POINTER(Completion), ctypes.c_int]),
     "m4d_transport_pending_completions": (ctypes.c_int, [_c_void_p]),
     "m4d_transport_eager_device_max": (_u64, [_c_void_p]),
@@ -224,7 +227,7 @@ def fast():
         raise NativeLibraryMissing(f"_m4dfast extension not built ({exc}): run __graft_entry__.build()") from exc
     addr = [ctypes.cast(getattr(handle, n), ctypes.c_void_p).value
             for n in ("m4d_transport_post_send", "m4d_transport_post_recv", "m4d_transport_progress",
-                      "m4d_transport_take_loan", "m4d_transport_release_loan")]
+                      "m4d_transport_take_loan", "m4d_transport_release_loan", "m4d_transport_post_many")]
     _m4dfast.bind(*addr)
     _fast = _m4dfast
     return _fast

@@ -330,3 +330,30 @@ def test_proxy_kernel_stays_up_under_traffic_and_exits_when_idle(pair):
     for _ in range(50):  # drain tag 15
         r = pair[1].post_recv(0, 0, 15, dst.window(), MemoryDomain.DEVICE)
         pump(pair, r)
+
+
+@pytest.mark.parametrize("eager", [False, True])
+def test_vectored_posts_match_the_per_post_loop(pair, eager):
+    """post_many: a window of device sends and receives in one call each -- bytes, FIFO
+    order and completions as with one call per post; ragged sizes, receives posted
+    before and after the sends."""
+    from paper_2101_08878_b200.transport import MemoryDomain
+
+    sizes = [1, 17, 4096, 65536, 300_000, 1 << 20, 4096, 3]
+    total = sum(sizes)
+    src = dev(total, pattern(total, 9))
+    dst = dev(total)
+    offs, at = [], 0
+    for n in sizes:
+        offs.append(at)
+        at += n
+    sv = [src.window(o, n) for o, n in zip(offs, sizes)]
+    dv = [dst.window(o, n) for o, n in zip(offs, sizes)]
+    rq = pair[1].post_many("recv", 0, 0, 16, dv[:4], MemoryDomain.DEVICE, eager=False)
+    sq = pair[0].post_many("send", 0, 1, 16, sv, MemoryDomain.DEVICE, eager=eager)
+    rq += pair[1].post_many("recv", 0, 0, 16, dv[4:], MemoryDomain.DEVICE, eager=False)
+    pump(pair, *(rq + sq))
+    assert [r.bytes_moved for r in rq] == sizes and all(not r.failed for r in rq + sq)
+    assert dst.to_bytes() == pattern(total, 9).tobytes()
+    with pytest.raises(Exception):
+        pair[0].post_many("send", 0, 1, 16, [b"host bytes"], MemoryDomain.DEVICE)
