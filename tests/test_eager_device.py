@@ -322,7 +322,7 @@ def test_proxy_kernel_stays_up_under_traffic_and_exits_when_idle(pair):
         s = pair[0].post_send_eager(0, 1, 15, src.window())
         pump(pair, s)
     busy = stats(pair[0])["eager_proxy_launches"] - first
-    assert busy <= 2  # the kernel stayed up (a launch or so if the host was slow)
+    assert busy <= 10  # the kernel stayed up (50 sends; a few relaunches only if the host stalled > 100 us)
     time.sleep(0.05)  # far beyond the idle timeout
     before = stats(pair[0])["eager_proxy_launches"]
     one()
