@@ -306,6 +306,18 @@ size_t m4d_partition_scratch_bytes(int64_t n, int buckets);
 m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
                          int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
                          void* stream);
+/* Counted receiver split (the push shuffle): each sender counts its rows per
+ * (owner, local partition) -- out_counts[world][buckets], buckets a power of
+ * two, world * buckets * 4 <= m4d_fine_count_smem_limit() -- and hands owner d
+ * its row d; the owner's m4d_partition_runs_counted then splits the received
+ * runs with those counts (fine_in[sources][buckets]) instead of counting them
+ * again.  Same output as m4d_partition_runs. */
+size_t m4d_fine_count_smem_limit(void);
+m4d_status m4d_partition_fine_counts(const int64_t* keys, const int64_t* vals, int64_t n, int world, int buckets,
+                                     uint32_t* out_counts, void* stream);
+m4d_status m4d_partition_runs_counted(const int64_t* in_pairs, int64_t n, const int64_t* runs_host, int coarse,
+                                      int sources, int buckets, const uint32_t* fine_in, int64_t* out_pairs,
+                                      int64_t* bounds, void* scratch, size_t scratch_bytes, void* stream);
 /* Receiver side of an M4D_PART_OWNER_COARSE exchange: in_pairs holds `sources`
  * segments, each made of `coarse` runs in coarse-bucket order; runs_host (host
  * memory, int64[coarse][sources][2]) gives each run's [start, end) row in

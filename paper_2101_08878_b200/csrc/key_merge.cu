@@ -994,6 +994,60 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
     }
 }
 
+// Sender side of the counted receiver split: rows per (owner, local partition)
+// of this rank's table -- what every owner's split would otherwise count from
+// the received rows.  Shared-memory counters for all owners x partitions.
+__global__ void __launch_bounds__(1024) fine_count_kernel(const int64_t* __restrict__ keys,
+                                                          const int64_t* __restrict__ vals, int64_t n, int world,
+                                                          int log2b, uint32_t* __restrict__ out, int pf) {
+    extern __shared__ uint32_t fc[];  // world << log2b
+    const int total = world << log2b;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) fc[i] = 0;
+    __syncthreads();
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
+    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
+    auto prefetch = [&](int64_t a) {
+        if (vals) l2_prefetch(keys, a, chunk, hi);
+        else l2_prefetch(reinterpret_cast<const longlong2*>(keys), a, chunk, hi);
+    };
+    if (pf && threadIdx.x == 0) prefetch(lo);
+    for (int64_t base = lo; base < hi; base += chunk) {
+        if (pf && threadIdx.x == 0) prefetch(base + chunk);
+        int64_t k[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            k[u] = i < hi ? key_at(keys, vals, i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            if (base + u * blockDim.x + threadIdx.x >= hi) continue;
+            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(k[u]));
+            const uint32_t owner = __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(world));
+            const uint32_t p = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b));
+            atomicAdd(&fc[owner << log2b | p], 1u);
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < total; i += blockDim.x)
+        if (fc[i]) atomicAdd(out + i, fc[i]);
+}
+
+// Receiver side: per-source counts (fine[src][b]) -> rows of earlier sources per
+// partition (grp_before[src][b]) and per-partition totals.
+__global__ void fine_prefix_kernel(const uint32_t* __restrict__ fine, int sources, int buckets,
+                                   unsigned long long* __restrict__ grp_before, unsigned long long* __restrict__ hist_all) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < buckets; b += gridDim.x * blockDim.x) {
+        unsigned long long run = 0;
+        for (int src = 0; src < sources; ++src) {
+            grp_before[static_cast<int64_t>(src) * buckets + b] = run;
+            run += fine[static_cast<int64_t>(src) * buckets + b];
+        }
+        hist_all[b] = run;
+    }
+}
+
 int log2_exact(int v) {
     int l = 0;
     while ((1 << l) < v) ++l;
@@ -1439,6 +1493,54 @@ m4d_status m4d_partition_runs(const int64_t* in_pairs, int64_t n, const int64_t*
     M4D_CUDA_TRY(cudaGetLastError());
     return M4D_OK;
 }
+
+m4d_status m4d_partition_fine_counts(const int64_t* keys, const int64_t* vals, int64_t n, int world, int buckets,
+                                     uint32_t* out_counts, void* stream) {
+    const int log2b = log2_exact(buckets);
+    if (n < 0 || world < 1 || log2b < 1) return fail(M4D_ERR_USAGE, "invalid fine-count request");
+    const size_t smem = static_cast<size_t>(world) * buckets * sizeof(uint32_t);
+    if (smem > m4d_fine_count_smem_limit()) return fail(M4D_ERR_USAGE, "%d owners x %d partitions exceed the counters a CTA holds", world, buckets);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    M4D_CUDA_TRY(cudaMemsetAsync(out_counts, 0, smem, s));
+    if (!n) return M4D_OK;
+    M4D_CUDA_TRY(cudaFuncSetAttribute(fine_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int dev = 0, sms = 148;
+    M4D_CUDA_TRY(cudaGetDevice(&dev));
+    M4D_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    fine_count_kernel<<<sms, 1024, smem, s>>>(keys, vals, n, world, log2b, out_counts, l2_pf());
+    M4D_CUDA_TRY(cudaGetLastError());
+    return M4D_OK;
+}
+
+size_t m4d_fine_count_smem_limit(void) { return 200 * 1024; }
+
+m4d_status m4d_partition_runs_counted(const int64_t* in_pairs, int64_t n, const int64_t* runs_host, int coarse,
+                                      int sources, int buckets, const uint32_t* fine_in, int64_t* out_pairs,
+                                      int64_t* bounds, void* scratch, size_t scratch_bytes, void* stream) {
+    const int log2b = log2_exact(buckets), cbits = log2_exact(coarse);
+    if (n < 0 || n >= (int64_t(1) << 32)) return fail(M4D_ERR_USAGE, "partition of %lld rows outside [0, 2^32)", (long long)n);
+    if (log2b < 0 || buckets > (1 << 15)) return fail(M4D_ERR_USAGE, "partition count %d must be a power of two <= 32768", buckets);
+    if (cbits < 0 || coarse > buckets || coarse > 256) return fail(M4D_ERR_USAGE, "coarse run count %d invalid", coarse);
+    if (sources < 1 || sources > 256) return fail(M4D_ERR_USAGE, "source count %d outside [1, 256]", sources);
+    if (scratch_bytes < m4d_partition_runs_scratch_bytes(sources, buckets, coarse))
+        return fail(M4D_ERR_USAGE, "partition scratch too small");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    char* base = static_cast<char*>(scratch);
+    unsigned long long* grp_before = reinterpret_cast<unsigned long long*>(base);                // [sources][buckets]
+    unsigned long long* hist_all = grp_before + static_cast<int64_t>(sources) * buckets;        // [buckets]
+    int64_t* runs = reinterpret_cast<int64_t*>(grp_before + (static_cast<int64_t>(sources) * kMaxRunGroups + 1) * buckets);
+    const size_t run_bytes = 2 * static_cast<size_t>(coarse) * sources * sizeof(int64_t);
+    M4D_CUDA_TRY(cudaMemcpyAsync(runs, runs_host, run_bytes, cudaMemcpyHostToDevice, s));
+    fine_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(fine_in, sources, buckets, grp_before, hist_all);
+    exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
+    const size_t sub_smem = static_cast<size_t>(buckets >> cbits) * sizeof(uint32_t);
+    runs_pass2_kernel<<<coarse * sources, runs_threads(), sub_smem, s>>>(reinterpret_cast<const longlong2*>(in_pairs), runs,
+                                                                       sources, 1, grp_before, bounds, log2b, cbits,
+                                                                       reinterpret_cast<longlong2*>(out_pairs), l2_pf());
+    M4D_CUDA_TRY(cudaGetLastError());
+    return M4D_OK;
+}
+
 
 int m4d_join_partition_rows(void) {
     // M4D_JOIN_PART_ROWS overrides the target rows per partition (the small join

@@ -82,9 +82,9 @@ class _Columns:
 class _Pairs:
     """(key, payload) 16-byte pairs: the internal layout of partitioned / shuffled rows."""
 
-    def __init__(self, device: int, capacity: int):
+    def __init__(self, device: int, capacity: int, extra_bytes: int = 0):
         self.capacity = max(1, int(capacity))
-        self.buf = native.DeviceBuffer(device, self.capacity * 16)
+        self.buf = native.DeviceBuffer(device, self.capacity * 16 + extra_bytes)  # extra: after the rows
         self.ptr = self.buf.ptr
 
 
@@ -125,7 +125,17 @@ class KeyMerge:
         slack = self.n + int(6 * math.sqrt(max(self.n, 1))) + 4096
         self.inputs = [_Columns(device, self.n), _Columns(device, self.n)]
         self.sendbuf = [_Pairs(device, self.n), _Pairs(device, self.n)] if world > 1 else None
-        self.recv = [_Pairs(device, slack), _Pairs(device, slack)] if world > 1 else None
+        # M4D_MERGE_FINE=1 (default, push shuffle): senders count side 1's rows per (owner,
+        # partition) beside push 0 and hand each owner its counts after its rows in the
+        # receive buffer, so side 1's receiver split needs no histogram pass
+        lib = native.lib()
+        self.fine = (world > 1 and (shuffle or _SHUFFLE) == "push" and os.environ.get("M4D_MERGE_FINE", "1") != "0"
+                     and self.parts > 1 and world * self.parts * 4 <= lib.m4d_fine_count_smem_limit())
+        fine_bytes = world * self.parts * 4 if self.fine else 0
+        self.recv = [_Pairs(device, slack), _Pairs(device, slack, fine_bytes)] if world > 1 else None
+        if self.fine:
+            self.fine_out = native.DeviceBuffer(device, fine_bytes)
+            self.fine_done = native.Event()
         self.parted = [_Pairs(device, slack), _Pairs(device, slack)]
         self.bounds = [native.DeviceBuffer(device, (max(self.parts, world) + 1) * 8) for _ in range(2)]
         lib = native.lib()
@@ -299,8 +309,11 @@ class KeyMerge:
         sends = [b[d * C] for d in range(P)] + [b[P * C]]
         return self._post_side(side, sends, incoming), runs_in
 
-    def _finish_side(self, side: int, runs_in: list, coarse: int | None = None, stream=None) -> int:
-        """Split the received source segments (each C coarse runs) into the local partitions."""
+    def _finish_side(self, side: int, runs_in: list, coarse: int | None = None, stream=None,
+                     counted: bool = False) -> int:
+        """Split the received source segments (each C coarse runs) into the local partitions.
+        ``counted``: the senders' per-partition counts follow the rows in the receive
+        buffer (push shuffle, side 1), so no histogram pass over the rows."""
         import numpy as np
 
         P, C = self.world, coarse or self.coarse
@@ -312,6 +325,13 @@ class KeyMerge:
         total = int(starts[-1])
         native.set_device(self.device)  # ranks of one process may sit on different GPUs
         scratch, nbytes = (self.scratch, self.scratch_bytes) if side == 0 else self.split_scratch1
+        if counted:  # the senders' counts, after the rows
+            fine_in = self.recv[1].ptr + self.recv[1].capacity * 16
+            native.check(native.lib().m4d_partition_runs_counted(
+                self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts, fine_in, self.parted[side].ptr,
+                self.bounds[side].ptr, scratch.ptr, nbytes, (stream or self.stream).handle))
+            self.launches += 3
+            return total
         native.check(native.lib().m4d_partition_runs(self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts,
                                                      self.parted[side].ptr, self.bounds[side].ptr, scratch.ptr,
                                                      nbytes, (stream or self.stream).handle))
@@ -384,6 +404,16 @@ class KeyMerge:
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.rank_bounds[side].ptr,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, plan_streams[side].handle))
             self.launches += 5
+            if side == 1 and self.fine:
+                # my side-1 rows per (owner, partition), into each owner's receive buffer after its rows
+                parts, stream = self.parts, plan_streams[1]
+                native.check(lib.m4d_partition_fine_counts(self.inputs[1].keys.ptr, self.inputs[1].vals.ptr, self.n, P,
+                                                           parts, self.fine_out.ptr, stream.handle))
+                for d in range(P):
+                    dst = self._peer_recv[1][d] + self._peer_cap[1][d] * 16 + me * parts * 4
+                    native.memcpy(dst, self.fine_out.ptr + d * parts * 4, parts * 4, stream)
+                self.fine_done.record(stream)
+                self.launches += 1
             b = self._read_bounds(self.rank_bounds[side], P * C, plan_streams[side])
             self._tp(f"plan{side}_done", plan_streams[side])
             # my rows per (owner, coarse run), relative to each owner's segment
@@ -413,10 +443,13 @@ class KeyMerge:
         out = []
         for side in range(2):
             self.pushed[side].synchronize()  # my rows for side `side` are in every owner's buffer
+            if side == 1 and self.fine:
+                self.fine_done.synchronize()  # ... and so are my side-1 counts
             await allgather(t, b"\x01", EXCHANGE_TAG + 6 + side)  # ... and every peer's rows in mine
             self._mark(f"side{side}_push_ms")
             self._tp(f"split{side}_start", self.split_streams[side])
-            out.append(self._finish_side(side, runs_in[side], C, self.split_streams[side]))
+            out.append(self._finish_side(side, runs_in[side], C, self.split_streams[side],
+                                         counted=side == 1 and self.fine))
             self._tp(f"split{side}_end", self.split_streams[side])
         for side in range(2):  # the join waits for both splits
             if self.split_streams[side] is not self.stream:

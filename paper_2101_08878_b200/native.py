@@ -170,6 +170,11 @@ SIGNATURES: dict[str, tuple] = {
     "m4d_partition_owner_push": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
                                                 _c_void_p, _size, _c_void_p]),
     "m4d_partition_launches": (ctypes.c_int, [ctypes.c_int]),
+    "m4d_fine_count_smem_limit": (_size, []),
+    "m4d_partition_fine_counts": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
+                                                 _c_void_p]),
+    "m4d_partition_runs_counted": (ctypes.c_int, [_c_void_p, _i64, _c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                  _c_void_p, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "m4d_join_partition_rows": (ctypes.c_int, []),
     "m4d_hash_join": (ctypes.c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, ctypes.c_int,
                                      _c_void_p, _c_void_p, _c_void_p, _i64, _c_void_p, _c_void_p]),

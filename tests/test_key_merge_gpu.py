@@ -306,3 +306,21 @@ def test_tuning_knobs_keep_the_digest(env):
     assert out.returncode == 0, out.stderr[-2000:]
     got = tuple(int(x) for x in out.stdout.strip().splitlines()[-1].strip("[]").split(","))
     assert got == tuple(oracle.key_merge_c(rows, 1, 0.3))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("fine", ["0", "1"])
+def test_counted_receiver_split_matches_the_oracle(world, fine):
+    """M4D_MERGE_FINE: side 1's receiver split with the senders' per-partition counts (no
+    histogram pass) and without; both equal to the oracle, over two steps."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _VARIANT_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), rows=200_000, world=world)
+    code = code.replace("run_world(200000, %d, 0.3)" % world, "run_world(200000, %d, 0.3, steps=2)" % world)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                         env=dict(os.environ, M4D_MERGE_FINE=fine))
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert eval(out.stdout.strip().splitlines()[-1]) == list(oracle.key_merge_c(200_000, world, 0.3))
