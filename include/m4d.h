@@ -307,8 +307,8 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
                          int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
                          void* stream);
 /* Counted receiver split (the push shuffle): each sender counts its rows per
- * (owner, local partition) -- out_counts[world][buckets], buckets a power of
- * two, world * buckets * 4 <= m4d_fine_count_smem_limit() -- and hands owner d
+ * (owner, local partition) -- out_counts[world][buckets] (32-bit), buckets a power
+ * of two, world * buckets * 2 <= m4d_fine_count_smem_limit() -- and hands owner d
  * its row d; the owner's m4d_partition_runs_counted then splits the received
  * runs with those counts (fine_in[sources][buckets]) instead of counting them
  * again.  Same output as m4d_partition_runs. */

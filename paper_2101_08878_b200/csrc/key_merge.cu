@@ -996,13 +996,16 @@ __global__ void __launch_bounds__(kJoinThreads, kMinBlocks)
 
 // Sender side of the counted receiver split: rows per (owner, local partition)
 // of this rank's table -- what every owner's split would otherwise count from
-// the received rows.  Shared-memory counters for all owners x partitions.
+// the received rows.  16-bit shared-memory counters, two per word, for all
+// owners x partitions (8 x 8192 in 128 KB); the increment that takes a counter
+// to 0x8000 moves 0x8000 to the global count, so a half never carries into its
+// neighbour and any skew stays exact.
 __global__ void __launch_bounds__(1024) fine_count_kernel(const int64_t* __restrict__ keys,
                                                           const int64_t* __restrict__ vals, int64_t n, int world,
                                                           int log2b, uint32_t* __restrict__ out, int pf) {
-    extern __shared__ uint32_t fc[];  // world << log2b
+    extern __shared__ uint32_t fc[];  // (world << log2b) / 2 words
     const int total = world << log2b;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) fc[i] = 0;
+    for (int i = threadIdx.x; i < total / 2; i += blockDim.x) fc[i] = 0;
     __syncthreads();
     const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
     const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -1026,12 +1029,19 @@ __global__ void __launch_bounds__(1024) fine_count_kernel(const int64_t* __restr
             const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(k[u]));
             const uint32_t owner = __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(world));
             const uint32_t p = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b));
-            atomicAdd(&fc[owner << log2b | p], 1u);
+            const uint32_t idx = owner << log2b | p, sh = (idx & 1u) * 16u;
+            const uint32_t old = atomicAdd(&fc[idx >> 1], 1u << sh);
+            if (((old >> sh) & 0xffffu) == 0x7fffu) {  // this increment reached 0x8000: spill it
+                atomicSub(&fc[idx >> 1], 0x8000u << sh);
+                atomicAdd(out + idx, 0x8000u);
+            }
         }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < total; i += blockDim.x)
-        if (fc[i]) atomicAdd(out + i, fc[i]);
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const uint32_t c = (fc[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+        if (c) atomicAdd(out + i, c);
+    }
 }
 
 // Receiver side: per-source counts (fine[src][b]) -> rows of earlier sources per
@@ -1498,10 +1508,10 @@ m4d_status m4d_partition_fine_counts(const int64_t* keys, const int64_t* vals, i
                                      uint32_t* out_counts, void* stream) {
     const int log2b = log2_exact(buckets);
     if (n < 0 || world < 1 || log2b < 1) return fail(M4D_ERR_USAGE, "invalid fine-count request");
-    const size_t smem = static_cast<size_t>(world) * buckets * sizeof(uint32_t);
+    const size_t smem = static_cast<size_t>(world) * buckets * sizeof(uint16_t);
     if (smem > m4d_fine_count_smem_limit()) return fail(M4D_ERR_USAGE, "%d owners x %d partitions exceed the counters a CTA holds", world, buckets);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    M4D_CUDA_TRY(cudaMemsetAsync(out_counts, 0, smem, s));
+    M4D_CUDA_TRY(cudaMemsetAsync(out_counts, 0, static_cast<size_t>(world) * buckets * sizeof(uint32_t), s));
     if (!n) return M4D_OK;
     M4D_CUDA_TRY(cudaFuncSetAttribute(fine_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int dev = 0, sms = 148;

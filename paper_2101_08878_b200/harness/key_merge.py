@@ -130,7 +130,7 @@ class KeyMerge:
         # receive buffer, so side 1's receiver split needs no histogram pass
         lib = native.lib()
         self.fine = (world > 1 and (shuffle or _SHUFFLE) == "push" and os.environ.get("M4D_MERGE_FINE", "1") != "0"
-                     and self.parts > 1 and world * self.parts * 4 <= lib.m4d_fine_count_smem_limit())
+                     and self.parts > 1 and world * self.parts * 2 <= lib.m4d_fine_count_smem_limit())
         fine_bytes = world * self.parts * 4 if self.fine else 0
         self.recv = [_Pairs(device, slack), _Pairs(device, slack, fine_bytes)] if world > 1 else None
         if self.fine:

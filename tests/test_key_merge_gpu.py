@@ -324,3 +324,27 @@ def test_counted_receiver_split_matches_the_oracle(world, fine):
                          env=dict(os.environ, M4D_MERGE_FINE=fine))
     assert out.returncode == 0, out.stderr[-2000:]
     assert eval(out.stdout.strip().splitlines()[-1]) == list(oracle.key_merge_c(200_000, world, 0.3))
+
+
+def test_fine_counts_exact_under_extreme_skew():
+    """m4d_partition_fine_counts' 16-bit shared counters spill to the global count:
+    one key repeated 6M times (every CTA of the first three quarters sees ~54K rows of
+    one (owner, partition) counter, so it spills) and a spread remainder count exactly
+    (numpy reference of the same hash)."""
+    from paper_2101_08878_b200 import native
+
+    n, world, parts = 8_000_000, 4, 8192
+    keys = np.full(n, 123456789, dtype=np.int64)
+    keys[6_000_000:] = np.arange(2_000_000, dtype=np.int64) * 7919
+    vals = np.arange(n, dtype=np.int64)
+    d_k, d_v = native.DeviceBuffer(0, n * 8), native.DeviceBuffer(0, n * 8)
+    out = native.DeviceBuffer(0, world * parts * 4)
+    native.memcpy(d_k.ptr, keys.ctypes.data, n * 8)
+    native.memcpy(d_v.ptr, vals.ctypes.data, n * 8)
+    native.check(native.lib().m4d_partition_fine_counts(d_k.ptr, d_v.ptr, n, world, parts, out.ptr, None))
+    got = np.frombuffer(native.to_host(out.ptr, world * parts * 4), dtype=np.uint32)
+    h = oracle.splitmix64_np(keys.view(np.uint64))
+    owner = ((h >> np.uint64(32)) * np.uint64(world)) >> np.uint64(32)
+    p = (h & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - 13)
+    want = np.bincount((owner * np.uint64(parts) + p).astype(np.int64), minlength=world * parts)
+    assert np.array_equal(got.astype(np.int64), want)
