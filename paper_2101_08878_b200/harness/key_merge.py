@@ -314,15 +314,8 @@ class KeyMerge:
         """Split the received source segments (each C coarse runs) into the local partitions.
         ``counted``: the senders' per-partition counts follow the rows in the receive
         buffer (push shuffle, side 1), so no histogram pass over the rows."""
-        import numpy as np
-
         P, C = self.world, coarse or self.coarse
-        starts = np.cumsum([0] + [r[C] for r in runs_in])
-        runs = np.empty((C, P, 2), dtype=np.int64)
-        for src, r in enumerate(runs_in):
-            for c in range(C):
-                runs[c, src] = (starts[src] + r[c], starts[src] + r[c + 1])
-        total = int(starts[-1])
+        runs, total = runs_in if isinstance(runs_in, tuple) else self._runs_table(runs_in, C)
         native.set_device(self.device)  # ranks of one process may sit on different GPUs
         scratch, nbytes = (self.scratch, self.scratch_bytes) if side == 0 else self.split_scratch1
         if counted:  # the senders' counts, after the rows
@@ -337,6 +330,18 @@ class KeyMerge:
                                                      nbytes, (stream or self.stream).handle))
         self.launches += 4
         return total
+
+    def _runs_table(self, runs_in: list, C: int):
+        """(C x P x 2 run bounds, total rows) of the received source segments: source src's
+        coarse run c is rows [start_src + r[c], start_src + r[c + 1]) of the receive buffer."""
+        import numpy as np
+
+        r = np.asarray(runs_in, dtype=np.int64)  # [P][C + 1], relative to each source's segment
+        starts = np.concatenate(([0], np.cumsum(r[:, C])))[:-1]
+        runs = np.empty((C, self.world, 2), dtype=np.int64)
+        runs[:, :, 0] = (starts[:, None] + r[:, :C]).T
+        runs[:, :, 1] = (starts[:, None] + r[:, 1:]).T
+        return np.ascontiguousarray(runs), int(r[:, C].sum())
 
     async def _shuffle_and_partition(self) -> list[int]:
         """Owner pass, NVLink exchange and local partition of both sides, pipelined: side 1's
@@ -419,7 +424,7 @@ class KeyMerge:
             # my rows per (owner, coarse run), relative to each owner's segment
             blob = struct.pack(f"<{width}q", *[b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)])
             tables = [struct.unpack(f"<{width}q", x) for x in await allgather(t, blob, EXCHANGE_TAG + 2 + 7 * side)]
-            runs_in[side] = [tables[src][me * (C + 1):(me + 1) * (C + 1)] for src in range(P)]
+            runs_in[side] = self._runs_table([tables[src][me * (C + 1):(me + 1) * (C + 1)] for src in range(P)], C)
             if any(sum(tables[src][d * (C + 1) + C] for src in range(P)) > self._peer_cap[side][d] for d in range(P)):
                 # a receive buffer is too small: every rank sees the same tables and falls back
                 # together, once side 0's pushes (if any) have landed everywhere
