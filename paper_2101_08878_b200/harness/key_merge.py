@@ -409,8 +409,12 @@ class KeyMerge:
                 self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, self.rank_bounds[side].ptr,
                 self.push_scratch[side].ptr, self.push_scratch_bytes, plan_streams[side].handle))
             self.launches += 5
+            b = self._read_bounds(self.rank_bounds[side], P * C, plan_streams[side])
+            self._tp(f"plan{side}_done", plan_streams[side])
             if side == 1 and self.fine:
-                # my side-1 rows per (owner, partition), into each owner's receive buffer after its rows
+                # my side-1 rows per (owner, partition), into each owner's receive buffer after
+                # its rows (queued after the plan's read-back, so the run-table exchange below
+                # does not wait for it; it runs beside push 0)
                 parts, stream = self.parts, plan_streams[1]
                 native.check(lib.m4d_partition_fine_counts(self.inputs[1].keys.ptr, self.inputs[1].vals.ptr, self.n, P,
                                                            parts, self.fine_out.ptr, stream.handle))
@@ -419,8 +423,6 @@ class KeyMerge:
                     native.memcpy(dst, self.fine_out.ptr + d * parts * 4, parts * 4, stream)
                 self.fine_done.record(stream)
                 self.launches += 1
-            b = self._read_bounds(self.rank_bounds[side], P * C, plan_streams[side])
-            self._tp(f"plan{side}_done", plan_streams[side])
             # my rows per (owner, coarse run), relative to each owner's segment
             blob = struct.pack(f"<{width}q", *[b[d * C + c] - b[d * C] for d in range(P) for c in range(C + 1)])
             tables = [struct.unpack(f"<{width}q", x) for x in await allgather(t, blob, EXCHANGE_TAG + 2 + 7 * side)]
