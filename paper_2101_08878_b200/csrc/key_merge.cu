@@ -119,6 +119,63 @@ __device__ __forceinline__ int64_t key_at(const int64_t* keys, const int64_t* va
     return vals ? __ldcs(keys + i) : __ldcs(keys + 2 * i);
 }
 
+// Calls fn(key) for every row of [lo, hi), spread over the CTA, kRowsPerThread
+// loads in flight per thread.  A 16-byte aligned SoA key column is read two keys
+// per load (an odd first / last row on its own); pf: thread 0 prefetches the next
+// chunk into L2.  For the counting passes, which need only the keys.
+template <typename Fn>
+__device__ __forceinline__ void for_each_key(const int64_t* __restrict__ keys, const int64_t* __restrict__ vals,
+                                             int64_t lo, int64_t hi, bool pf, Fn fn) {
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
+    if (vals && (reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
+        int64_t a = lo, z = hi;
+        if (a < z && (a & 1)) {
+            if (threadIdx.x == 0) fn(__ldcs(keys + a));
+            ++a;
+        }
+        if (a < z && ((z - a) & 1)) {
+            if (threadIdx.x == 0) fn(__ldcs(keys + z - 1));
+            --z;
+        }
+        const longlong2* kp = reinterpret_cast<const longlong2*>(keys + a);
+        const int64_t np = (z - a) / 2;
+        if (pf && threadIdx.x == 0) l2_prefetch(keys, a, 2 * chunk, z);
+        for (int64_t pb = 0; pb < np; pb += chunk) {
+            if (pf && threadIdx.x == 0) l2_prefetch(keys, a + 2 * (pb + chunk), 2 * chunk, z);
+            longlong2 v[kRowsPerThread];
+#pragma unroll
+            for (int u = 0; u < kRowsPerThread; ++u) {
+                const int64_t i = pb + u * blockDim.x + threadIdx.x;
+                v[u] = i < np ? __ldcs(kp + i) : make_longlong2(0, 0);
+            }
+#pragma unroll
+            for (int u = 0; u < kRowsPerThread; ++u)
+                if (pb + u * blockDim.x + threadIdx.x < np) {
+                    fn(v[u].x);
+                    fn(v[u].y);
+                }
+        }
+        return;
+    }
+    auto prefetch = [&](int64_t a) {  // keys only: a SoA key column, or the pairs
+        if (vals) l2_prefetch(keys, a, chunk, hi);
+        else l2_prefetch(reinterpret_cast<const longlong2*>(keys), a, chunk, hi);
+    };
+    if (pf && threadIdx.x == 0) prefetch(lo);
+    for (int64_t base = lo; base < hi; base += chunk) {
+        if (pf && threadIdx.x == 0) prefetch(base + chunk);
+        int64_t k[kRowsPerThread];
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            k[u] = i < hi ? key_at(keys, vals, i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u)
+            if (base + u * blockDim.x + threadIdx.x < hi) fn(k[u]);
+    }
+}
+
 // hist[b * ctas + cta] = rows of scatter CTA cta's run that fall in bucket b.
 // `split` histogram CTAs share one scatter run (grid = ctas * split, so a
 // grid sized for 1024-thread scatter CTAs still fills every SM); with
@@ -134,17 +191,8 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(const int64_t* __res
     const int64_t r0 = cta * run, r1 = r0 + run < n ? r0 + run : n;
     const int64_t len = r1 > r0 ? r1 - r0 : 0;
     const int64_t lo = r0 + len * part / split, hi = r0 + len * (part + 1) / split;
-    for (int64_t base = lo; base < hi; base += static_cast<int64_t>(blockDim.x) * kRowsPerThread) {
-        int64_t k[kRowsPerThread];
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {  // all loads first: kRowsPerThread in flight
-            const int64_t i = base + u * blockDim.x + threadIdx.x;
-            k[u] = i < hi ? key_at(keys, vals, i) : 0;
-        }
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u)
-            if (base + u * blockDim.x + threadIdx.x < hi) atomicAdd(&h[bucket_of(k[u], mode, buckets, log2b)], 1u);
-    }
+    for_each_key(keys, vals, lo, hi, false,
+                 [&](int64_t key) { atomicAdd(&h[bucket_of(key, mode, buckets, log2b)], 1u); });
     __syncthreads();
     for (int b = threadIdx.x; b < buckets; b += blockDim.x) {
         uint32_t* dst = hist + static_cast<int64_t>(b) * ctas + cta;
@@ -553,11 +601,6 @@ __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__
     if (threadIdx.x == 0) overflow = 0;
     __syncthreads();
     const int64_t lo = blockIdx.x * run, hi = lo + run < n ? lo + run : n;
-    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
-    auto prefetch = [&](int64_t a) {  // keys only: a SoA key column, or the pairs
-        if (vals) l2_prefetch(keys, a, chunk, hi);
-        else l2_prefetch(reinterpret_cast<const longlong2*>(keys), a, chunk, hi);
-    };
     auto count_key = [&](int64_t key) {
         const uint32_t b = bucket_of(key, M4D_PART_LOCAL, buckets, log2b);
         if (kPacked) {
@@ -568,51 +611,7 @@ __global__ void __launch_bounds__(1024) hist2_kernel(const int64_t* __restrict__
             atomicAdd(&h2[b], 1u);
         }
     };
-    if (vals && (reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
-        // SoA key column: two keys per 16-byte load (twice the bytes in flight per thread);
-        // an odd first / last row of the range is counted on its own
-        int64_t a = lo, z = hi;
-        if (a < z && (a & 1)) {
-            if (threadIdx.x == 0) count_key(__ldcs(keys + a));
-            ++a;
-        }
-        if (a < z && ((z - a) & 1)) {
-            if (threadIdx.x == 0) count_key(__ldcs(keys + z - 1));
-            --z;
-        }
-        const longlong2* kp = reinterpret_cast<const longlong2*>(keys + a);
-        const int64_t np = (z - a) / 2;
-        if (pf && threadIdx.x == 0) l2_prefetch(keys, a, 2 * chunk, z);
-        for (int64_t pb = 0; pb < np; pb += chunk) {
-            if (pf && threadIdx.x == 0) l2_prefetch(keys, a + 2 * (pb + chunk), 2 * chunk, z);
-            longlong2 v[kRowsPerThread];
-#pragma unroll
-            for (int u = 0; u < kRowsPerThread; ++u) {
-                const int64_t i = pb + u * blockDim.x + threadIdx.x;
-                v[u] = i < np ? __ldcs(kp + i) : make_longlong2(0, 0);
-            }
-#pragma unroll
-            for (int u = 0; u < kRowsPerThread; ++u)
-                if (pb + u * blockDim.x + threadIdx.x < np) {
-                    count_key(v[u].x);
-                    count_key(v[u].y);
-                }
-        }
-    } else {
-        if (pf && threadIdx.x == 0) prefetch(lo);
-        for (int64_t base = lo; base < hi; base += chunk) {
-            if (pf && threadIdx.x == 0) prefetch(base + chunk);
-            int64_t k[kRowsPerThread];
-#pragma unroll
-            for (int u = 0; u < kRowsPerThread; ++u) {
-                const int64_t i = base + u * blockDim.x + threadIdx.x;
-                k[u] = i < hi ? key_at(keys, vals, i) : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < kRowsPerThread; ++u)
-                if (base + u * blockDim.x + threadIdx.x < hi) count_key(k[u]);
-        }
-    }
+    for_each_key(keys, vals, lo, hi, pf, count_key);
     __syncthreads();
     if (!overflow) {
         auto count = [&](int b) -> uint32_t { return kPacked ? (h2[b >> 1] >> ((b & 1) << 4)) & 0xffffu : h2[b]; };
@@ -1040,36 +1039,19 @@ __global__ void __launch_bounds__(1024) fine_count_kernel(const int64_t* __restr
     const int total = world << log2b;
     for (int i = threadIdx.x; i < total / 2; i += blockDim.x) fc[i] = 0;
     __syncthreads();
-    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
     const int64_t per = (n + gridDim.x - 1) / gridDim.x;
     const int64_t lo = blockIdx.x * per, hi = lo + per < n ? lo + per : n;
-    auto prefetch = [&](int64_t a) {
-        if (vals) l2_prefetch(keys, a, chunk, hi);
-        else l2_prefetch(reinterpret_cast<const longlong2*>(keys), a, chunk, hi);
-    };
-    if (pf && threadIdx.x == 0) prefetch(lo);
-    for (int64_t base = lo; base < hi; base += chunk) {
-        if (pf && threadIdx.x == 0) prefetch(base + chunk);
-        int64_t k[kRowsPerThread];
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            const int64_t i = base + u * blockDim.x + threadIdx.x;
-            k[u] = i < hi ? key_at(keys, vals, i) : 0;
+    for_each_key(keys, vals, lo, hi, pf != 0, [&](int64_t key) {
+        const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(key));
+        const uint32_t owner = __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(world));
+        const uint32_t p = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b));
+        const uint32_t idx = owner << log2b | p, sh = (idx & 1u) * 16u;
+        const uint32_t old = atomicAdd(&fc[idx >> 1], 1u << sh);
+        if (((old >> sh) & 0xffffu) == 0x7fffu) {  // this increment reached 0x8000: spill it
+            atomicSub(&fc[idx >> 1], 0x8000u << sh);
+            atomicAdd(out + idx, 0x8000u);
         }
-#pragma unroll
-        for (int u = 0; u < kRowsPerThread; ++u) {
-            if (base + u * blockDim.x + threadIdx.x >= hi) continue;
-            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(k[u]));
-            const uint32_t owner = __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(world));
-            const uint32_t p = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b));
-            const uint32_t idx = owner << log2b | p, sh = (idx & 1u) * 16u;
-            const uint32_t old = atomicAdd(&fc[idx >> 1], 1u << sh);
-            if (((old >> sh) & 0xffffu) == 0x7fffu) {  // this increment reached 0x8000: spill it
-                atomicSub(&fc[idx >> 1], 0x8000u << sh);
-                atomicAdd(out + idx, 0x8000u);
-            }
-        }
-    }
+    });
     __syncthreads();
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
         const uint32_t c = (fc[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
