@@ -27,6 +27,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "m4d_internal.h"
@@ -206,7 +207,11 @@ __global__ void __launch_bounds__(kHistThreads) hist_kernel(const int64_t* __res
 // Exclusive scan of hist (bucket-major) in place: three phases over tiles.
 constexpr int kScanTile = 4096;
 
-__global__ void scan_reduce_kernel(const uint32_t* __restrict__ v, int64_t n, int64_t* __restrict__ tile_sums) {
+// gate (all three): a scan launched for the exact fallback of a speculative pass 1
+// returns at once unless *gate is set.
+__global__ void scan_reduce_kernel(const uint32_t* __restrict__ v, int64_t n, int64_t* __restrict__ tile_sums,
+                                   const int* __restrict__ gate) {
+    if (gate && !*gate) return;
     __shared__ int64_t part[32];
     const int64_t lo = blockIdx.x * static_cast<int64_t>(kScanTile);
     int64_t s = 0;
@@ -221,7 +226,8 @@ __global__ void scan_reduce_kernel(const uint32_t* __restrict__ v, int64_t n, in
     }
 }
 
-__global__ void scan_tiles_kernel(int64_t* tile_sums, int64_t tiles, int64_t* total) {
+__global__ void scan_tiles_kernel(int64_t* tile_sums, int64_t tiles, int64_t* total, const int* __restrict__ gate) {
+    if (gate && !*gate) return;
     // one warp: sequential over tiles in chunks of 32 with a warp scan
     int64_t carry = 0;
     const int lane = threadIdx.x;
@@ -239,7 +245,8 @@ __global__ void scan_tiles_kernel(int64_t* tile_sums, int64_t tiles, int64_t* to
 }
 
 __global__ void scan_apply_kernel(const uint32_t* __restrict__ v, int64_t n, const int64_t* __restrict__ tile_sums,
-                                  int64_t* __restrict__ out) {
+                                  int64_t* __restrict__ out, const int* __restrict__ gate) {
+    if (gate && !*gate) return;
     // 1024 threads x 4 elements = one tile; block scan with warp shuffles
     __shared__ int64_t warp_tot[32];
     const int64_t lo = blockIdx.x * static_cast<int64_t>(kScanTile);
@@ -376,11 +383,29 @@ __device__ __forceinline__ void load_and_rank(const int64_t* __restrict__ keys, 
 // lanes), instead of 8 ballots + leader election.  Rows of one warp that share a
 // bucket are ordered by the hardware's atomic serialisation, so the order inside
 // a partition is not tied to input order (the join's result is a multiset).
-template <bool kFull>
+// Full-id counts of the speculative pass 1 (kSpec): 16-bit shared counters, two per
+// word; the increment that takes one to 0x8000 moves 0x8000 to the global count.
+struct FullCounts {
+    uint32_t* smem;                 // (1 << log2full) / 2 words
+    unsigned long long* global;     // this CTA's group row of the per-group full-id histogram
+    int shift;                      // 32 - log2full
+};
+
+__device__ __forceinline__ void count_full(const FullCounts& fc, uint32_t low) {
+    const uint32_t id = low >> fc.shift, sh = (id & 1u) * 16u;
+    const uint32_t old = atomicAdd(&fc.smem[id >> 1], 1u << sh);
+    if (((old >> sh) & 0xffffu) == 0x7fffu) {
+        atomicSub(&fc.smem[id >> 1], 0x8000u << sh);
+        atomicAdd(fc.global + id, 0x8000ull);
+    }
+}
+
+template <bool kFull, bool kSpec = false>
 __device__ __forceinline__ void load_and_rank_atomic(const int64_t* __restrict__ keys, const int64_t* __restrict__ vals,
                                                      int64_t tile, int rem, int w, int lane, int mode, int buckets,
                                                      int log2b, uint16_t* wb, longlong2 (&row)[kRowsPerThread],
-                                                     uint32_t (&bk)[kRowsPerThread], uint16_t (&off)[kRowsPerThread]) {
+                                                     uint32_t (&bk)[kRowsPerThread], uint16_t (&off)[kRowsPerThread],
+                                                     const FullCounts& fc = FullCounts{}) {
 #pragma unroll
     for (int u = 0; u < kRowsPerThread; ++u) {
         const int r = w * 256 + u * 32 + lane;
@@ -398,7 +423,13 @@ __device__ __forceinline__ void load_and_rank_atomic(const int64_t* __restrict__
 #pragma unroll
     for (int u = 0; u < kRowsPerThread; ++u) {
         const bool live = kFull || w * 256 + u * 32 + lane < rem;
-        bk[u] = live ? bucket_of(row[u].x, mode, buckets, log2b) : 0xffffffffu;
+        if (kSpec) {  // mode LOCAL: the top log2b bits of the hash's low word, and the full id
+            const uint32_t low = live ? static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(row[u].x))) : 0u;
+            bk[u] = live ? low >> (32 - log2b) : 0xffffffffu;
+            if (live) count_full(fc, low);
+        } else {
+            bk[u] = live ? bucket_of(row[u].x, mode, buckets, log2b) : 0xffffffffu;
+        }
         if (live) {
             const uint32_t sh = (bk[u] & 1u) * 16u;
             off[u] = static_cast<uint16_t>(atomicAdd(&wb32[bk[u] >> 1], 1u << sh) >> sh);
@@ -434,14 +465,34 @@ __device__ __forceinline__ void l2_prefetch_rows(const int64_t* keys, const int6
     }
 }
 
-template <int kT, bool kPush, bool kBulk>
+// Speculative pass 1 of the two-pass LOCAL partition (kSpec), and the gate of
+// its exact fallback.  kSpec: no histogram pass ran before; CTA c writes bucket
+// b's rows into its own region of `cap` rows at (b * ctas + c) * cap, counts
+// every row by its full partition id (per-group histogram for pass 2), writes
+// its exact per-bucket counts to counts[b * ctas + c] (the layout the
+// histogram pass produces), and raises *overflow if any region would take more
+// than cap rows (rows past cap are not stored).  gate: a kernel launched as the
+// exact fallback returns at once unless *gate is set.
+struct SpecArgs {
+    int64_t cap = 0;
+    int log2full = 0;
+    int groups = 1;
+    unsigned long long* hist_grp = nullptr;  // [groups][1 << log2full]
+    uint32_t* counts = nullptr;              // [buckets][ctas]
+    int* overflow = nullptr;
+    const int* gate = nullptr;
+};
+
+template <int kT, bool kPush, bool kBulk, bool kSpec = false>
 __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile_scatter_kernel(const int64_t* __restrict__ keys,
                                                                        const int64_t* __restrict__ vals, int64_t n,
                                                                        int64_t run, int mode, int buckets, int log2b,
                                                                        const int64_t* __restrict__ offsets,
                                                                        longlong2* __restrict__ out,
                                                                        const __grid_constant__ PushTargets push,
-                                                                       bool atomic_rank, int tile_prefetch) {
+                                                                       bool atomic_rank, int tile_prefetch,
+                                                                       const SpecArgs spec) {
+    if (spec.gate && !*spec.gate) return;  // exact fallback of a speculative pass 1 that did not overflow
     constexpr int kTileRows = kT * kRowsPerThread;
     extern __shared__ __align__(16) unsigned char tsm[];
     longlong2* stage = reinterpret_cast<longlong2*>(tsm);
@@ -451,12 +502,28 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
     __shared__ uint32_t tstart[kTileBuckets + 1];
     __shared__ uint32_t dbase[kTileBuckets];  // global row of a tile row r in bucket b: dbase[b] + r
     __shared__ uint32_t scan_tmp[kTileBuckets / 32];
+    __shared__ uint32_t lim[kSpec ? kTileBuckets : 1];  // kSpec: end of bucket b's region
     constexpr int kW = kT / 32;
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     int nbits = 0;
     while ((1 << nbits) < buckets) ++nbits;
-    for (int b = threadIdx.x; b < kTileBuckets; b += blockDim.x)
-        gcur[b] = b < buckets ? static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]) : 0u;
+    FullCounts fc{};
+    if (kSpec) {
+        fc.smem = reinterpret_cast<uint32_t*>(wbase + kW * kTileBuckets);
+        fc.global = spec.hist_grp + (static_cast<int64_t>(blockIdx.x) * spec.groups / gridDim.x << spec.log2full);
+        fc.shift = 32 - spec.log2full;
+        for (int i = threadIdx.x; i < (1 << spec.log2full) / 2; i += blockDim.x) fc.smem[i] = 0;
+    }
+    for (int b = threadIdx.x; b < kTileBuckets; b += blockDim.x) {
+        if (kSpec) {
+            const uint32_t r0 = static_cast<uint32_t>((static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * spec.cap);
+            gcur[b] = b < buckets ? r0 : 0u;
+            lim[b] = b < buckets ? r0 + static_cast<uint32_t>(spec.cap) : 0u;
+        } else {
+            gcur[b] = b < buckets ? static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]) : 0u;
+        }
+    }
+    if (kSpec) __syncthreads();  // full-id counters zeroed before any rank
     // kPush: bucket b = (owner d, coarse c) writes row j of the local order to
     // seg[d] + (j - start of d's segment), so each owner's rows land contiguous
     // in its receive buffer, C coarse runs in order.  (Shared only when used.)
@@ -486,7 +553,12 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         for (int b = lane; b < kTileBuckets; b += 32) wb[b] = 0;
         __syncwarp();
         const int rem = hi - tile < kTileRows ? static_cast<int>(hi - tile) : kTileRows;
-        if (atomic_rank) {
+        if (kSpec) {  // (atomic ranking only)
+            if (rem == kTileRows)
+                load_and_rank_atomic<true, true>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, wb, row, bk, off, fc);
+            else
+                load_and_rank_atomic<false, true>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, wb, row, bk, off, fc);
+        } else if (atomic_rank) {
             if (rem == kTileRows)
                 load_and_rank_atomic<true>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, wb, row, bk, off);
             else
@@ -552,9 +624,11 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         if (kBulk) {
             if (threadIdx.x < kTileBuckets) {
                 const int b = threadIdx.x;
-                if (total) {
+                uint32_t keep = total;
+                if (kSpec) keep = gstart >= lim[b] ? 0u : (lim[b] - gstart < total ? lim[b] - gstart : total);
+                if (keep) {
                     longlong2* dst = (kPush ? bptr[b] : out) + gstart;
-                    m4d::ptx::bulk_s2g(dst, stage + tst, total * static_cast<uint32_t>(sizeof(longlong2)));
+                    m4d::ptx::bulk_s2g(dst, stage + tst, keep * static_cast<uint32_t>(sizeof(longlong2)));
                 }
                 m4d::ptx::bulk_commit();
             }
@@ -564,12 +638,27 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
                 const uint32_t b = sbucket[r];
                 if (kPush)
                     bptr[b][dbase[b] + r] = stage[r];
-                else
+                else if (!kSpec || dbase[b] + r < lim[b])
                     out[dbase[b] + r] = stage[r];
             }
         }
     }
     if (kBulk && threadIdx.x < kTileBuckets) m4d::ptx::bulk_wait_all();
+    if (kSpec) {
+        // exact per-bucket counts (what the histogram pass would have produced), the
+        // overflow flag, and this CTA's full-id counts into its group's histogram
+        if (threadIdx.x < buckets) {
+            const int b = threadIdx.x;
+            const uint32_t r0 = lim[b] - static_cast<uint32_t>(spec.cap);
+            spec.counts[static_cast<int64_t>(b) * gridDim.x + blockIdx.x] = gcur[b] - r0;
+            if (gcur[b] > lim[b]) atomicExch(spec.overflow, 1);
+        }
+        __syncthreads();  // every rank's count_full is done
+        for (int i = threadIdx.x; i < (1 << spec.log2full); i += blockDim.x) {
+            const uint32_t c = (fc.smem[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+            if (c) atomicAdd(fc.global + i, static_cast<unsigned long long>(c));
+        }
+    }
 }
 
 // ---- two-pass LOCAL partition (buckets > kSinglePassMax) -------------------------------
@@ -742,6 +831,92 @@ __global__ void __launch_bounds__(1024)
     const int64_t i0 = static_cast<int64_t>(seg) * ctas + k0, i1 = static_cast<int64_t>(seg) * ctas + k1;
     const int64_t lo = i0 < entries ? offs[i0] : n, hi = i1 < entries ? offs[i1] : n;
     scatter_by_low_bits(in, lo, hi, cursor, log2b, static_cast<uint32_t>(sub - 1), out, pf);
+}
+
+// Pass 2 after a speculative pass 1: one CTA per (segment, group of pass-1
+// CTAs) as above, but the group's rows sit in one region per pass-1 CTA --
+// (seg * ctas + c) * cap when pass 1 fit its regions, offs[seg * ctas + c] when
+// *overflow sent it through the exact fallback -- holding counts[seg * ctas + c]
+// rows each.  The CTA walks the regions as one virtual row range.
+constexpr int kMaxRegions = 1024;
+
+__global__ void __launch_bounds__(1024)
+    spec_pass2_kernel(const longlong2* __restrict__ in, const uint32_t* __restrict__ counts,
+                      const int64_t* __restrict__ offs, const int* __restrict__ overflow, int64_t cap, int ctas,
+                      const unsigned long long* __restrict__ grp_before, int groups,
+                      const int64_t* __restrict__ bounds, int log2b, int b1, longlong2* __restrict__ out, bool pf) {
+    extern __shared__ uint32_t cursor[];  // 2^(log2b - b1)
+    __shared__ int64_t rstart[kMaxRegions];
+    __shared__ uint32_t rpre[kMaxRegions + 1];
+    const int sub = 1 << (log2b - b1);
+    const int seg = blockIdx.x / groups, g = blockIdx.x % groups;
+    const int buckets = 1 << log2b;
+    for (int k = threadIdx.x; k < sub; k += blockDim.x) {
+        const int b = seg * sub + k;
+        cursor[k] = static_cast<uint32_t>(bounds[b] + static_cast<int64_t>(grp_before[static_cast<int64_t>(g) * buckets + b]));
+    }
+    const int k0 = (g * ctas + groups - 1) / groups, k1 = ((g + 1) * ctas + groups - 1) / groups;
+    const int nreg = k1 - k0;
+    const bool exact = *overflow != 0;
+    const int64_t idx0 = static_cast<int64_t>(seg) * ctas + k0;
+    for (int k = threadIdx.x; k < nreg; k += blockDim.x) rstart[k] = exact ? offs[idx0 + k] : (idx0 + k) * cap;
+    if (threadIdx.x < 32) {  // exclusive prefix of the region counts
+        const int lane = threadIdx.x;
+        uint32_t carry = 0;
+        for (int base = 0; base < nreg; base += 32) {
+            const uint32_t c = base + lane < nreg ? counts[idx0 + base + lane] : 0u;
+            uint32_t incl = c;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (base + lane < nreg) rpre[base + lane] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (lane == 0) rpre[nreg] = carry;
+    }
+    __syncthreads();
+    const int64_t total = rpre[nreg];
+    const uint32_t mask = static_cast<uint32_t>(sub - 1);
+    const int64_t chunk = static_cast<int64_t>(blockDim.x) * kRowsPerThread;
+    // region of virtual row i: the last r with rpre[r] <= i
+    auto region = [&](int64_t i) {
+        int lo = 0, hi = nreg - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (rpre[mid] <= i) lo = mid; else hi = mid - 1;
+        }
+        return lo;
+    };
+    auto prefetch = [&](int64_t v0) {  // the pieces of virtual rows [v0, v0 + chunk)
+        if (v0 >= total) return;
+        const int64_t v1 = v0 + chunk < total ? v0 + chunk : total;
+        for (int r = region(v0); r < nreg && rpre[r] < v1; ++r) {
+            const int64_t a = v0 > rpre[r] ? v0 : rpre[r], z = v1 < rpre[r + 1] ? v1 : rpre[r + 1];
+            if (z > a) l2_prefetch(in, rstart[r] + (a - rpre[r]), z - a, rstart[r] + (z - rpre[r]));
+        }
+    };
+    if (pf && threadIdx.x == 0) prefetch(0);
+    for (int64_t base = 0; base < total; base += chunk) {
+        if (pf && threadIdx.x == 0) prefetch(base + chunk);
+        longlong2 row[kRowsPerThread];
+        int r = base + threadIdx.x < total ? region(base + threadIdx.x) : 0;
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            const int64_t i = base + u * blockDim.x + threadIdx.x;
+            if (i < total) {
+                while (r + 1 < nreg && rpre[r + 1] <= i) ++r;
+                row[u] = __ldcs(in + rstart[r] + (i - rpre[r]));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kRowsPerThread; ++u) {
+            if (base + u * blockDim.x + threadIdx.x >= total) continue;
+            const uint64_t h = m4d_splitmix64(static_cast<uint64_t>(row[u].x));
+            const uint32_t b2 = static_cast<uint32_t>((h & 0xffffffffull) >> (32 - log2b)) & mask;
+            out[atomicAdd(&cursor[b2], 1u)] = row[u];
+        }
+    }
 }
 
 // Receiver side of the owner+coarse exchange (M4D_PART_OWNER_COARSE): S
@@ -1192,43 +1367,76 @@ static int l2_pf() {
     return a;
 }
 
-template <int kT, bool kPush, bool kBulk>
+template <int kT, bool kPush, bool kBulk, bool kSpec = false>
 static cudaError_t launch_tile_scatter_t(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
                                          int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
-                                         longlong2* out, const PushTargets& push) {
-    const cudaError_t e = cudaFuncSetAttribute(tile_scatter_kernel<kT, kPush, kBulk>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                               static_cast<int>(tile_smem<kT>()));
+                                         longlong2* out, const PushTargets& push, const SpecArgs& spec) {
+    const size_t smem = tile_smem<kT>() + (kSpec ? (size_t(1) << spec.log2full) / 2 * sizeof(uint32_t) : 0);
+    const cudaError_t e = cudaFuncSetAttribute(tile_scatter_kernel<kT, kPush, kBulk, kSpec>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    tile_scatter_kernel<kT, kPush, kBulk><<<ctas, kT, tile_smem<kT>(), s>>>(keys, vals, n, run, mode, buckets, log2b,
-                                                                          offs, out, push, tile_rank_atomic(),
-                                                                          l2_pf());
+    tile_scatter_kernel<kT, kPush, kBulk, kSpec><<<ctas, kT, smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+                                                                        out, push, tile_rank_atomic(), l2_pf(), spec);
     return cudaGetLastError();
 }
 
 template <int kT>
 static cudaError_t launch_tile_scatter_k(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
                                          int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
-                                         longlong2* out, const PushTargets* push) {
+                                         longlong2* out, const PushTargets* push, const SpecArgs& spec, bool speculative) {
     static const PushTargets none{};
+    if (speculative)
+        return tile_bulk(false) ? launch_tile_scatter_t<kT, false, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec)
+                                : launch_tile_scatter_t<kT, false, false, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec);
     if (tile_bulk(push != nullptr))
-        return push ? launch_tile_scatter_t<kT, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push)
-                    : launch_tile_scatter_t<kT, false, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none);
-    return push ? launch_tile_scatter_t<kT, true, false>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push)
-                : launch_tile_scatter_t<kT, false, false>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none);
+        return push ? launch_tile_scatter_t<kT, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push, spec)
+                    : launch_tile_scatter_t<kT, false, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec);
+    return push ? launch_tile_scatter_t<kT, true, false>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push, spec)
+                : launch_tile_scatter_t<kT, false, false>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec);
 }
 
+// spec / speculative: see SpecArgs (the speculative pass 1, or the gate of its exact fallback).
 static cudaError_t launch_tile_scatter(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
                                        int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
-                                       longlong2* out, const PushTargets* push = nullptr) {
+                                       longlong2* out, const PushTargets* push = nullptr,
+                                       const SpecArgs& spec = SpecArgs{}, bool speculative = false) {
     switch (push ? push_tile_threads() : tile_threads()) {
-        case 256: return launch_tile_scatter_k<256>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push);
-        case 1024: return launch_tile_scatter_k<1024>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push);
-        default: return launch_tile_scatter_k<512>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push);
+        case 256: return launch_tile_scatter_k<256>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push, spec, speculative);
+        case 1024: return launch_tile_scatter_k<1024>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push, spec, speculative);
+        default: return launch_tile_scatter_k<512>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, push, spec, speculative);
     }
 }
 
 static int pass1_bits(int log2b) { return log2b > 8 ? 8 : log2b; }
+
+// Speculative pass 1 (M4D_PASS1 = spec | hist, default spec): the two-pass LOCAL
+// partition skips the histogram pass; pass 1 writes into fixed regions of
+// spec_cap rows per (bucket, CTA) -- the mean plus six standard deviations plus
+// 32 rows, at most the CTA's rows -- and an exact fallback (scan + the usual
+// pass 1, gated on the overflow flag, so skew costs one more pass but never a
+// wrong result) runs only when a region overflowed.  Up to 8192 partitions
+// (16 KB of full-id counters keeps two 512-thread CTAs per SM).
+static bool pass1_spec() {
+    static const bool on = [] {
+        const char* v = getenv("M4D_PASS1");
+        return !(v && strcmp(v, "hist") == 0);
+    }();
+    return on;
+}
+
+static int64_t spec_cap(int64_t n, int ctas, int fan) {
+    const int64_t run = (n + ctas - 1) / ctas;
+    const double mean = static_cast<double>(run) / fan;
+    int64_t cap = static_cast<int64_t>(std::ceil(mean + 6.0 * std::sqrt(mean) + 32.0));
+    return cap > run ? (run > 0 ? run : 1) : cap;
+}
+
+static bool spec_applies(int64_t n, int ctas, int fan, int log2b) {
+    if (!pass1_spec() || !tile_rank_atomic() || log2b > 13 || fan > kTileBuckets) return false;
+    if ((ctas + kPass2Groups - 1) / kPass2Groups > kMaxRegions) return false;
+    const int64_t run = (n + ctas - 1) / ctas;
+    return static_cast<int64_t>(fan) * ctas * spec_cap(n, ctas, fan) + run < (int64_t(1) << 32);
+}
 
 // Single-pass partition (hist -> scan -> scatter) into `buckets` buckets; the
 // bucket function gets (mode, buckets, log2b) as bucket_of documents.  The
@@ -1268,9 +1476,9 @@ static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int
         const int split = (4 * 148 + ctas - 1) / ctas;
         if (split > 1) M4D_CUDA_TRY(cudaMemsetAsync(hist, 0, entries * sizeof(uint32_t), s));
         hist_kernel<<<ctas * split, kHistThreads, hist_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, split, hist);
-        scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
-        scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
-        scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
+        scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, nullptr);
+        scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total, nullptr);
+        scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs, nullptr);
         bucket_bounds_kernel<<<(buckets + 256) / 256, 256, 0, s>>>(offs, buckets, ctas, n, bounds);
     }
     if (phases & kScatter) {
@@ -1312,8 +1520,13 @@ size_t m4d_partition_scratch_bytes(int64_t n, int buckets) {
     const int64_t entries = ctas * fan;
     const int64_t tiles = (entries + kScanTile - 1) / kScanTile;
     size_t bytes = entries * sizeof(uint32_t) + entries * sizeof(int64_t) + (tiles + 1) * sizeof(int64_t) + 512;
-    if (buckets > kSinglePassMax)  // per-group + global histograms, pass-1 pairs
-        bytes += (kMaxGroups + 1) * (buckets * sizeof(unsigned long long) + 256) + static_cast<size_t>(n) * 16 + 256;
+    if (buckets > kSinglePassMax) {  // per-group + global histograms, overflow flag, pass-1 pairs
+        int64_t rows = n;
+        const int lb = log2_exact(buckets);
+        if (lb > 0 && spec_applies(n, static_cast<int>(ctas), static_cast<int>(fan), lb))
+            rows = std::max<int64_t>(n, fan * ctas * spec_cap(n, static_cast<int>(ctas), static_cast<int>(fan)));
+        bytes += (kMaxGroups + 1) * (buckets * sizeof(unsigned long long) + 256) + 256 + static_cast<size_t>(rows) * 16 + 256;
+    }
     return bytes;
 }
 
@@ -1347,12 +1560,41 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         base += (buckets * sizeof(unsigned long long) + 255) & ~size_t(255);
         unsigned long long* hist_grp = reinterpret_cast<unsigned long long*>(base);
         base += (kMaxGroups * buckets * sizeof(unsigned long long) + 255) & ~size_t(255);
+        int* overflow = reinterpret_cast<int*>(base);
+        base += 256;
         longlong2* tmp = reinterpret_cast<longlong2*>(base);
         static const int groups = [] {
             const char* v = getenv("M4D_PASS2_GROUPS");
             const int g = v ? atoi(v) : kPass2Groups;
             return g < 1 ? 1 : g > kMaxGroups ? kMaxGroups : g;
         }();
+        if (spec_applies(n, ctas, fan, log2b)) {
+            // speculative pass 1 (no histogram pass), its gated exact fallback, pass 2 over the regions
+            SpecArgs sa;
+            sa.cap = spec_cap(n, ctas, fan);
+            sa.log2full = log2b;
+            sa.groups = groups;
+            sa.hist_grp = hist_grp;
+            sa.counts = hist;
+            sa.overflow = overflow;
+            M4D_CUDA_TRY(cudaMemsetAsync(hist_grp, 0, groups * buckets * sizeof(unsigned long long), s));
+            M4D_CUDA_TRY(cudaMemsetAsync(overflow, 0, sizeof(int), s));
+            M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, M4D_PART_LOCAL, fan, b1, nullptr, tmp, nullptr,
+                                             sa, true));
+            scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, overflow);
+            scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total, overflow);
+            scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs, overflow);
+            SpecArgs gate;
+            gate.gate = overflow;
+            M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, M4D_PART_LOCAL, fan, b1, offs, tmp, nullptr, gate));
+            group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, groups, buckets, hist_all);
+            exclusive_scan_u64_kernel<<<1, 1024, 0, s>>>(hist_all, buckets, bounds, n);
+            spec_pass2_kernel<<<fan * groups, 1024, (buckets >> b1) * sizeof(uint32_t), s>>>(
+                tmp, hist, offs, overflow, sa.cap, ctas, hist_grp, groups, bounds, log2b, b1,
+                reinterpret_cast<longlong2*>(out_pairs), l2_pf());
+            M4D_CUDA_TRY(cudaGetLastError());
+            return M4D_OK;
+        }
         const bool packed = buckets > (1 << 15);
         const size_t hist_smem = packed ? (buckets + 1) / 2 * sizeof(uint32_t) : buckets * sizeof(uint32_t);
         M4D_CUDA_TRY(cudaFuncSetAttribute(hist2_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxParts * 2));
@@ -1361,9 +1603,9 @@ m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, in
         M4D_CUDA_TRY(cudaMemsetAsync(hist_grp, 0, groups * buckets * sizeof(unsigned long long), s));
         (packed ? hist2_kernel<true> : hist2_kernel<false>)<<<ctas, 1024, hist_smem, s>>>(keys, vals, n, run, log2b, b1,
                                                                                         groups, hist, hist_grp, l2_pf());
-        scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums);
-        scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total);
-        scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs);
+        scan_reduce_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, nullptr);
+        scan_tiles_kernel<<<1, 32, 0, s>>>(tile_sums, tiles, total, nullptr);
+        scan_apply_kernel<<<static_cast<unsigned>(tiles), 1024, 0, s>>>(hist, entries, tile_sums, offs, nullptr);
         // pass 1: by the top b1 bits of the partition id (mode LOCAL with 2^b1 buckets == those bits)
         M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, M4D_PART_LOCAL, fan, b1, offs, tmp));
         group_prefix_kernel<<<(buckets + 255) / 256, 256, 0, s>>>(hist_grp, groups, buckets, hist_all);

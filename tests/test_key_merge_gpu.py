@@ -154,6 +154,57 @@ def test_partition_bounds_under_extreme_skew(buckets):
     assert np.array_equal(pairs[:, 0], keys[pairs[:, 1]])
 
 
+def _partition_local(keys, buckets):
+    from paper_2101_08878_b200 import native
+
+    n = len(keys)
+    vals = np.arange(n, dtype=np.int64)
+    lib = native.lib()
+    k_d, v_d = native.DeviceBuffer(0, n * 8), native.DeviceBuffer(0, n * 8)
+    native.memcpy(k_d.ptr, keys.ctypes.data, n * 8)
+    native.memcpy(v_d.ptr, vals.ctypes.data, n * 8)
+    out = native.DeviceBuffer(0, n * 16)
+    bounds = native.DeviceBuffer(0, (buckets + 1) * 8)
+    nbytes = lib.m4d_partition_scratch_bytes(n, buckets)
+    scratch = native.DeviceBuffer(0, nbytes)
+    native.check(lib.m4d_partition(k_d.ptr, v_d.ptr, n, 0, buckets, out.ptr, bounds.ptr, scratch.ptr, nbytes, None))
+    native.check(lib.m4d_device_sync(0))
+    got_b = np.frombuffer(native.to_host(bounds.ptr, (buckets + 1) * 8), dtype=np.int64)
+    pairs = np.frombuffer(native.to_host(out.ptr, n * 16), dtype=np.int64).reshape(n, 2)
+    h = oracle.splitmix64_np(keys.view(np.uint64))
+    bucket = ((h & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - int(np.log2(buckets)))).astype(np.int64)
+    want_b = np.concatenate([[0], np.cumsum(np.bincount(bucket, minlength=buckets))])
+    assert np.array_equal(got_b, want_b)
+    assert np.array_equal(np.sort(pairs[:, 1]), vals)  # a permutation of the rows
+    assert np.all(np.diff(bucket[pairs[:, 1]]) >= 0)  # grouped by bucket, in bucket order
+    assert np.array_equal(pairs[:, 0], keys[pairs[:, 1]])
+
+
+@pytest.mark.parametrize("buckets", [512, 1024, 8192])
+@pytest.mark.parametrize("n", [1, 777, 3_000_000])
+def test_speculative_pass1_uniform_keys(buckets, n):
+    """Two-pass LOCAL partition with the speculative pass 1 (regions sized from the
+    mean, no histogram pass): bounds and the row permutation match numpy, including
+    inputs smaller than one tile and one-row inputs."""
+    rng = np.random.default_rng(n + buckets)
+    _partition_local(rng.integers(-(1 << 62), 1 << 62, n).astype(np.int64), buckets)
+
+
+@pytest.mark.parametrize("buckets", [1024, 8192])
+@pytest.mark.parametrize("hot", [1, 3, 40])
+def test_speculative_pass1_overflow_takes_the_exact_fallback(buckets, hot):
+    """Duplicate-heavy keys overflow the speculative regions (one key far above a
+    region's mean + 6 sigma); the gated exact fallback must still give exact bounds and
+    a permutation grouped by partition."""
+    n = 2_000_000
+    rng = np.random.default_rng(hot)
+    keys = rng.integers(0, 1 << 40, n).astype(np.int64)
+    hot_keys = rng.integers(0, 1 << 40, hot)
+    keys[: n // 2] = hot_keys[rng.integers(0, hot, n // 2)]
+    rng.shuffle(keys)
+    _partition_local(keys, buckets)
+
+
 @pytest.mark.parametrize("world,coarse", [(3, 64), (8, 32), (2, 1)])
 def test_owner_coarse_partition_matches_numpy(world, coarse):
     """m4d_partition_owner_coarse: bucket = owner * C + top log2 C bits of the local id."""
@@ -290,6 +341,7 @@ print(list(got))
     {"M4D_JOIN": "small"},
     {"M4D_JOIN": "small", "M4D_JOIN_PART_ROWS": "12400"},  # two build chunks per partition
     {"M4D_JOIN_PERSIST": "1", "M4D_JOIN_PART_ROWS": "500"},  # more partitions than one wave
+    {"M4D_PASS1": "hist"},  # histogram pass before pass 1 instead of the speculative regions
 ])
 def test_tuning_knobs_keep_the_digest(env):
     """Every join knob (read once per process, so each runs in its own interpreter) gives
