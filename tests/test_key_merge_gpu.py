@@ -120,11 +120,13 @@ def test_full_scale_digest_against_the_oracle():
     assert got == oracle.join_mt_c(lk, lv, rk, rv, len(os.sched_getaffinity(0)))
 
 
-@pytest.mark.parametrize("buckets", [32768, 65536])
+@pytest.mark.parametrize("buckets", [1024, 8192, 32768, 65536])
 def test_partition_bounds_under_extreme_skew(buckets):
     """One key fills whole CTAs (>= 65536 equal rows each): the 16-bit shared histogram
-    overflows and the CTA falls back to exact global counting; bounds and the pair
-    permutation still match a numpy recount of the same bucket function."""
+    overflows and the CTA falls back to exact global counting (32768 / 65536), or the
+    speculative pass 1 overflows its regions and takes the exact fallback while its
+    16-bit full-id counters are flushed before they wrap (1024 / 8192); bounds and the
+    pair permutation still match a numpy recount of the same bucket function."""
     from paper_2101_08878_b200 import native
 
     n = 3 * 65536
