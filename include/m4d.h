@@ -302,7 +302,9 @@ size_t m4d_partition_scratch_bytes(int64_t n, int buckets);
  * receives the bucket start rows.  Input: SoA columns (keys, vals), or pairs
  * (keys = pairs, vals = NULL).  n < 2^32.  The hash shuffle of SPEC.md:425.
  * LOCAL with more than 256 buckets (power of two, <= 65536) runs as two
- * L2-friendly scatter passes; RANK allows up to 16384 buckets. */
+ * L2-friendly scatter passes; up to 8192 buckets the first pass needs no
+ * histogram pass (fixed per-CTA regions, exact on-device fallback when one
+ * overflows; M4D_PASS1=hist disables it).  RANK allows up to 16384 buckets. */
 m4d_status m4d_partition(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
                          int64_t* out_pairs, int64_t* bounds, void* scratch, size_t scratch_bytes,
                          void* stream);
