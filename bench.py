@@ -987,6 +987,14 @@ def main(argv=None) -> int:
             emit(reference_p2p(args))
         return 0
 
+    # Watchdog: a run that hangs (e.g. a rank waiting on a peer that died) dumps every
+    # thread's Python stack to stderr and exits instead of sitting until the launcher's
+    # timeout (M4D_BENCH_WATCHDOG_S, default 1500 s; 0 disables).
+    watchdog = float(os.environ.get("M4D_BENCH_WATCHDOG_S", "1500"))
+    if watchdog > 0:
+        import faulthandler
+
+        faulthandler.dump_traceback_later(watchdog, exit=True)
     dist = Dist()
     peaks = load_peaks()
     runner = {"transpose_sum": bench_transpose_sum, "key_merge": bench_key_merge, "p2p": bench_p2p,

@@ -1294,6 +1294,13 @@ static bool tile_bulk(bool push) {
     return mode < 0 ? push : mode == 1;
 }
 
+// The speculative pass 1 (see SpecArgs) stores runs with TMA bulk copies unless
+// M4D_TILE_STORE=rows: N=1 merge step 4.21 vs 4.32 ms (profiles/r2_spec_align.txt).
+static bool tile_bulk_spec() {
+    const char* v = getenv("M4D_TILE_STORE");
+    return !(v && strcmp(v, "rows") == 0);
+}
+
 // Threads per push-scatter CTA (M4D_PUSH_TILE_THREADS, default 1024): longer
 // runs per bucket per tile make NVLink stores efficient (N=2 / N=4 at 128
 // push buckets: 8.08 / 9.99 ms with 256 threads, 7.72 / 9.39 ms with 1024).
@@ -1385,8 +1392,8 @@ static cudaError_t launch_tile_scatter_k(int ctas, cudaStream_t s, const int64_t
                                          int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
                                          longlong2* out, const PushTargets* push, const SpecArgs& spec, bool speculative) {
     static const PushTargets none{};
-    if (speculative)
-        return tile_bulk(false) ? launch_tile_scatter_t<kT, false, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec)
+    if (speculative)  // TMA bulk run stores unless M4D_TILE_STORE=rows (4.21 vs 4.32 ms per merge step)
+        return tile_bulk_spec() ? launch_tile_scatter_t<kT, false, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec)
                                 : launch_tile_scatter_t<kT, false, false, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec);
     if (tile_bulk(push != nullptr))
         return push ? launch_tile_scatter_t<kT, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push, spec)

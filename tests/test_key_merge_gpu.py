@@ -192,6 +192,37 @@ def test_speculative_pass1_uniform_keys(buckets, n):
     _partition_local(rng.integers(-(1 << 62), 1 << 62, n).astype(np.int64), buckets)
 
 
+_SPEC_STORE_SCRIPT = """
+import sys
+sys.path[:0] = [{root!r}, {tests!r}]
+import numpy as np
+from test_key_merge_gpu import _partition_local
+rng = np.random.default_rng(7)
+_partition_local(rng.integers(-(1 << 62), 1 << 62, 3_000_000).astype(np.int64), 8192)
+keys = rng.integers(0, 1 << 40, 2_000_000).astype(np.int64)
+keys[:1_000_000] = 42
+_partition_local(keys, 1024)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("store", ["rows", "bulk"])
+def test_speculative_pass1_store_modes(store):
+    """The speculative pass 1 with row-by-row stores and with TMA bulk run stores
+    (M4D_TILE_STORE, read once per process: one interpreter each), uniform keys and an
+    overflowing hot key."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = _SPEC_STORE_SCRIPT.format(root=root, tests=os.path.join(root, "tests"))
+    out = subprocess.run([sys.executable, "-c", code], env={**os.environ, "M4D_TILE_STORE": store}, cwd=root,
+                         capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().endswith("ok")
+
+
 @pytest.mark.parametrize("buckets", [1024, 8192])
 @pytest.mark.parametrize("hot", [1, 3, 40])
 def test_speculative_pass1_overflow_takes_the_exact_fallback(buckets, hot):
