@@ -386,21 +386,25 @@ __device__ __forceinline__ void load_and_rank(const int64_t* __restrict__ keys, 
 // Full-id counts of the speculative pass 1 (kSpec): 16-bit shared counters, two per
 // word; the increment that takes one to 0x8000 moves 0x8000 to the global count.
 struct FullCounts {
-    uint32_t* smem;                 // (1 << log2full) / 2 words
-    unsigned long long* global;     // this CTA's group row of the per-group full-id histogram
-    int shift;                      // 32 - log2full
+    uint32_t* smem;                 // ids / 2 words
+    unsigned long long* global;     // this CTA's group row of the per-group full-id histogram, or
+    uint32_t* global32;             // (push) the sender's per-(owner, local partition) counts
+    int shift;                      // 32 - log2 of the local partition count
 };
 
-__device__ __forceinline__ void count_full(const FullCounts& fc, uint32_t low) {
-    const uint32_t id = low >> fc.shift, sh = (id & 1u) * 16u;
+__device__ __forceinline__ void count_id(const FullCounts& fc, uint32_t id) {
+    const uint32_t sh = (id & 1u) * 16u;
     const uint32_t old = atomicAdd(&fc.smem[id >> 1], 1u << sh);
     if (((old >> sh) & 0xffffu) == 0x7fffu) {
         atomicSub(&fc.smem[id >> 1], 0x8000u << sh);
-        atomicAdd(fc.global + id, 0x8000ull);
+        if (fc.global32) atomicAdd(fc.global32 + id, 0x8000u);
+        else atomicAdd(fc.global + id, 0x8000ull);
     }
 }
 
-template <bool kFull, bool kSpec = false>
+__device__ __forceinline__ void count_full(const FullCounts& fc, uint32_t low) { count_id(fc, low >> fc.shift); }
+
+template <bool kFull, bool kSpec = false, bool kFine = false>
 __device__ __forceinline__ void load_and_rank_atomic(const int64_t* __restrict__ keys, const int64_t* __restrict__ vals,
                                                      int64_t tile, int rem, int w, int lane, int mode, int buckets,
                                                      int log2b, uint16_t* wb, longlong2 (&row)[kRowsPerThread],
@@ -427,6 +431,12 @@ __device__ __forceinline__ void load_and_rank_atomic(const int64_t* __restrict__
             const uint32_t low = live ? static_cast<uint32_t>(m4d_splitmix64(static_cast<uint64_t>(row[u].x))) : 0u;
             bk[u] = live ? low >> (32 - log2b) : 0xffffffffu;
             if (live) count_full(fc, low);
+        } else if (kFine) {  // mode OWNER_COARSE (bucket_of), and the (owner, local partition) id
+            const uint64_t h = live ? m4d_splitmix64(static_cast<uint64_t>(row[u].x)) : 0ull;
+            const uint32_t low = static_cast<uint32_t>(h);
+            const uint32_t owner = __umulhi(static_cast<uint32_t>(h >> 32), static_cast<uint32_t>(buckets >> log2b));
+            bk[u] = live ? owner << log2b | (log2b ? low >> (32 - log2b) : 0u) : 0xffffffffu;
+            if (live) count_id(fc, owner << (32 - fc.shift) | low >> fc.shift);
         } else {
             bk[u] = live ? bucket_of(row[u].x, mode, buckets, log2b) : 0xffffffffu;
         }
@@ -481,9 +491,11 @@ struct SpecArgs {
     uint32_t* counts = nullptr;              // [buckets][ctas]
     int* overflow = nullptr;
     const int* gate = nullptr;
+    uint32_t* fine_out = nullptr;  // kFine (push): [world][1 << log2full] counts of this sender's rows
+    int fine_ids = 0;              // world << log2full
 };
 
-template <int kT, bool kPush, bool kBulk, bool kSpec = false>
+template <int kT, bool kPush, bool kBulk, bool kSpec = false, bool kFine = false>
 __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile_scatter_kernel(const int64_t* __restrict__ keys,
                                                                        const int64_t* __restrict__ vals, int64_t n,
                                                                        int64_t run, int mode, int buckets, int log2b,
@@ -514,6 +526,12 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         fc.shift = 32 - spec.log2full;
         for (int i = threadIdx.x; i < (1 << spec.log2full) / 2; i += blockDim.x) fc.smem[i] = 0;
     }
+    if (kFine) {  // the push also counts its rows per (owner, local partition): the owners' split needs no histogram
+        fc.smem = reinterpret_cast<uint32_t*>(wbase + kW * kTileBuckets);
+        fc.global32 = spec.fine_out;
+        fc.shift = 32 - spec.log2full;
+        for (int i = threadIdx.x; i < spec.fine_ids / 2; i += blockDim.x) fc.smem[i] = 0;
+    }
     for (int b = threadIdx.x; b < kTileBuckets; b += blockDim.x) {
         if (kSpec) {
             const uint32_t r0 = static_cast<uint32_t>((static_cast<int64_t>(b) * gridDim.x + blockIdx.x) * spec.cap);
@@ -523,7 +541,7 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
             gcur[b] = b < buckets ? static_cast<uint32_t>(offsets[static_cast<int64_t>(b) * gridDim.x + blockIdx.x]) : 0u;
         }
     }
-    if (kSpec) __syncthreads();  // full-id counters zeroed before any rank
+    if (kSpec || kFine) __syncthreads();  // full-id counters zeroed before any rank
     // kPush: bucket b = (owner d, coarse c) writes row j of the local order to
     // seg[d] + (j - start of d's segment), so each owner's rows land contiguous
     // in its receive buffer, C coarse runs in order.  (Shared only when used.)
@@ -553,7 +571,12 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         for (int b = lane; b < kTileBuckets; b += 32) wb[b] = 0;
         __syncwarp();
         const int rem = hi - tile < kTileRows ? static_cast<int>(hi - tile) : kTileRows;
-        if (kSpec) {  // (atomic ranking only)
+        if (kFine) {  // (atomic ranking only)
+            if (rem == kTileRows)
+                load_and_rank_atomic<true, false, true>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, wb, row, bk, off, fc);
+            else
+                load_and_rank_atomic<false, false, true>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, wb, row, bk, off, fc);
+        } else if (kSpec) {  // (atomic ranking only)
             if (rem == kTileRows)
                 load_and_rank_atomic<true, true>(keys, vals, tile, rem, w, lane, mode, buckets, log2b, wb, row, bk, off, fc);
             else
@@ -657,6 +680,13 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         for (int i = threadIdx.x; i < (1 << spec.log2full); i += blockDim.x) {
             const uint32_t c = (fc.smem[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
             if (c) atomicAdd(fc.global + i, static_cast<unsigned long long>(c));
+        }
+    }
+    if (kFine) {
+        __syncthreads();  // every rank's count_id is done
+        for (int i = threadIdx.x; i < spec.fine_ids; i += blockDim.x) {
+            const uint32_t c = (fc.smem[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
+            if (c) atomicAdd(fc.global32 + i, c);
         }
     }
 }
@@ -1374,15 +1404,16 @@ static int l2_pf() {
     return a;
 }
 
-template <int kT, bool kPush, bool kBulk, bool kSpec = false>
+template <int kT, bool kPush, bool kBulk, bool kSpec = false, bool kFine = false>
 static cudaError_t launch_tile_scatter_t(int ctas, cudaStream_t s, const int64_t* keys, const int64_t* vals, int64_t n,
                                          int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
                                          longlong2* out, const PushTargets& push, const SpecArgs& spec) {
-    const size_t smem = tile_smem<kT>() + (kSpec ? (size_t(1) << spec.log2full) / 2 * sizeof(uint32_t) : 0);
-    const cudaError_t e = cudaFuncSetAttribute(tile_scatter_kernel<kT, kPush, kBulk, kSpec>,
+    const size_t smem = tile_smem<kT>() + (kSpec ? (size_t(1) << spec.log2full) / 2 * sizeof(uint32_t) : 0) +
+                        (kFine ? static_cast<size_t>(spec.fine_ids) / 2 * sizeof(uint32_t) : 0);
+    const cudaError_t e = cudaFuncSetAttribute(tile_scatter_kernel<kT, kPush, kBulk, kSpec, kFine>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
-    tile_scatter_kernel<kT, kPush, kBulk, kSpec><<<ctas, kT, smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
+    tile_scatter_kernel<kT, kPush, kBulk, kSpec, kFine><<<ctas, kT, smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
                                                                         out, push, tile_rank_atomic(), l2_pf(), spec);
     return cudaGetLastError();
 }
@@ -1392,6 +1423,8 @@ static cudaError_t launch_tile_scatter_k(int ctas, cudaStream_t s, const int64_t
                                          int64_t run, int mode, int buckets, int log2b, const int64_t* offs,
                                          longlong2* out, const PushTargets* push, const SpecArgs& spec, bool speculative) {
     static const PushTargets none{};
+    if (push && spec.fine_out)  // the push with fused (owner, local partition) counts (bulk run stores)
+        return launch_tile_scatter_t<kT, true, true, false, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, *push, spec);
     if (speculative)  // TMA bulk run stores unless M4D_TILE_STORE=rows (4.21 vs 4.32 ms per merge step)
         return tile_bulk_spec() ? launch_tile_scatter_t<kT, false, true, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec)
                                 : launch_tile_scatter_t<kT, false, false, true>(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs, out, none, spec);
@@ -1455,7 +1488,8 @@ enum { kPlan = 1, kScatter = 2, kPlanAndScatter = 3 };
 static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int64_t n, int mode, int buckets,
                                    int log2b, int64_t* out_pairs, int64_t* bounds, void* scratch,
                                    size_t scratch_bytes, cudaStream_t s, int phases = kPlanAndScatter,
-                                   const PushTargets* push = nullptr, bool push_layout = false) {
+                                   const PushTargets* push = nullptr, bool push_layout = false,
+                                   const SpecArgs& fine = SpecArgs{}) {
     if (scratch_bytes < m4d_partition_scratch_bytes(n, buckets)) return fail(M4D_ERR_USAGE, "partition scratch too small");
     // (the push scatter's plan and scatter calls both size the grid for its CTAs)
     int ctas = push_layout ? partition_ctas(n, push_tile_threads(), push_ctas_per_sm())
@@ -1490,8 +1524,10 @@ static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int
     }
     if (phases & kScatter) {
         if (buckets <= kTileBuckets) {
+            if (fine.fine_out)
+                M4D_CUDA_TRY(cudaMemsetAsync(fine.fine_out, 0, static_cast<size_t>(fine.fine_ids) * sizeof(uint32_t), s));
             M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs,
-                                             reinterpret_cast<longlong2*>(out_pairs), push));
+                                             reinterpret_cast<longlong2*>(out_pairs), push, fine));
         } else {
             M4D_CUDA_TRY(cudaFuncSetAttribute(scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxBuckets * 4));
             scatter_kernel<<<ctas, kHistThreads, cur_smem, s>>>(keys, vals, n, run, mode, buckets, log2b, offs,
@@ -1665,6 +1701,36 @@ m4d_status m4d_partition_owner_push(const int64_t* keys, const int64_t* vals, in
     for (int d = 0; d < world; ++d) push.seg[d] = reinterpret_cast<longlong2*>(seg_dest[d]);
     return partition_single(keys, vals, n, M4D_PART_OWNER_COARSE, world * coarse, cbits, nullptr, nullptr, scratch,
                             scratch_bytes, static_cast<cudaStream_t>(stream), kScatter, &push, true);
+}
+
+size_t m4d_push_fine_smem_limit(void) {
+    // shared memory the push scatter CTA (M4D_PUSH_TILE_THREADS) leaves for 16-bit fine counters
+    const size_t tile = push_tile_threads() == 256 ? tile_smem<256>() : push_tile_threads() == 512 ? tile_smem<512>()
+                                                                                                   : tile_smem<1024>();
+    const size_t cap = 227 * 1024 - 8192;  // (static shared memory of the kernel: cursors, push pointers)
+    return cap > tile ? cap - tile : 0;
+}
+
+m4d_status m4d_partition_owner_push_fine(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
+                                         const uint64_t* seg_dest, int parts, uint32_t* fine_out, void* scratch,
+                                         size_t scratch_bytes, void* stream) {
+    int cbits = 0;
+    const m4d_status st = owner_coarse_check(n, world, coarse, &cbits);
+    if (st != M4D_OK) return st;
+    const int pbits = log2_exact(parts);
+    if (world > kMaxPushOwners) return fail(M4D_ERR_USAGE, "push scatter limited to %d owners", kMaxPushOwners);
+    if (!seg_dest || !fine_out) return fail(M4D_ERR_USAGE, "null push destinations or counts");
+    if (pbits < 1 || static_cast<size_t>(world) * parts * 2 > m4d_push_fine_smem_limit())
+        return fail(M4D_ERR_USAGE, "%d owners x %d partitions of 16-bit counters do not fit the push CTA", world, parts);
+    if (!tile_rank_atomic()) return fail(M4D_ERR_USAGE, "fused fine counts need atomic tile ranking");
+    PushTargets push{};
+    for (int d = 0; d < world; ++d) push.seg[d] = reinterpret_cast<longlong2*>(seg_dest[d]);
+    SpecArgs fine;
+    fine.fine_out = fine_out;
+    fine.fine_ids = world * parts;
+    fine.log2full = pbits;
+    return partition_single(keys, vals, n, M4D_PART_OWNER_COARSE, world * coarse, cbits, nullptr, nullptr, scratch,
+                            scratch_bytes, static_cast<cudaStream_t>(stream), kScatter, &push, true, fine);
 }
 
 // Join variant (M4D_JOIN = big | small, default big): see kSmallThreads.

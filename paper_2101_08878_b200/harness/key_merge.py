@@ -131,8 +131,15 @@ class KeyMerge:
         lib = native.lib()
         self.fine = (world > 1 and (shuffle or _SHUFFLE) == "push" and os.environ.get("M4D_MERGE_FINE", "1") != "0"
                      and self.parts > 1 and world * self.parts * 2 <= lib.m4d_fine_count_smem_limit())
+        # M4D_MERGE_FINE_FUSED=1 (default where the counters fit the push CTA's shared memory,
+        # P <= 4 at 8192 partitions): the push scatter itself counts both sides' rows per
+        # (owner, partition) -- no separate count pass, and both receiver splits are counted
+        self.fine_fused = (self.fine and os.environ.get("M4D_MERGE_FINE_FUSED", "1") != "0"
+                           and world * self.parts * 2 <= lib.m4d_push_fine_smem_limit())
         fine_bytes = world * self.parts * 4 if self.fine else 0
-        self.recv = [_Pairs(device, slack), _Pairs(device, slack, fine_bytes)] if world > 1 else None
+        # bytes after each receive buffer's rows: the senders' counts (kept when a buffer grows)
+        self._recv_extra = [fine_bytes if self.fine_fused else 0, fine_bytes]
+        self.recv = [_Pairs(device, slack, self._recv_extra[0]), _Pairs(device, slack, self._recv_extra[1])] if world > 1 else None
         if self.fine:
             self.fine_out = native.DeviceBuffer(device, fine_bytes)
             self.fine_done = native.Event()
@@ -276,7 +283,7 @@ class KeyMerge:
         t, P, me = self.transport, self.world, self.rank
         total = sum(incoming)
         if total > self.recv[side].capacity:
-            self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096)
+            self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096, self._recv_extra[side])
         if total > self.parted[side].capacity:
             self.parted[side] = _Pairs(self.device, int(total * 1.1) + 4096)
         reqs, at = [], 0
@@ -319,7 +326,7 @@ class KeyMerge:
         native.set_device(self.device)  # ranks of one process may sit on different GPUs
         scratch, nbytes = (self.scratch, self.scratch_bytes) if side == 0 else self.split_scratch1
         if counted:  # the senders' counts, after the rows
-            fine_in = self.recv[1].ptr + self.recv[1].capacity * 16
+            fine_in = self.recv[side].ptr + self.recv[side].capacity * 16
             native.check(native.lib().m4d_partition_runs_counted(
                 self.recv[side].ptr, total, runs.ctypes.data, C, P, self.parts, fine_in, self.parted[side].ptr,
                 self.bounds[side].ptr, scratch.ptr, nbytes, (stream or self.stream).handle))
@@ -411,7 +418,7 @@ class KeyMerge:
             self.launches += 5
             b = self._read_bounds(self.rank_bounds[side], P * C, plan_streams[side])
             self._tp(f"plan{side}_done", plan_streams[side])
-            if side == 1 and self.fine:
+            if side == 1 and self.fine and not self.fine_fused:
                 # my side-1 rows per (owner, partition), into each owner's receive buffer after
                 # its rows (queued after the plan's read-back, so the run-table exchange below
                 # does not wait for it; it runs beside push 0)
@@ -440,9 +447,18 @@ class KeyMerge:
                 dest[d] = self._peer_recv[side][d] + before * 16
             self._tp(f"push{side}_start")
             native.set_device(self.device)
-            native.check(lib.m4d_partition_owner_push(
-                self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest,
-                self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
+            if self.fine_fused:  # the push counts my rows per (owner, partition) as it moves them
+                parts = self.parts
+                native.check(lib.m4d_partition_owner_push_fine(
+                    self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest, parts,
+                    self.fine_out.ptr, self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
+                for d in range(P):  # owner d's row of counts, after the rows of its receive buffer
+                    dst = self._peer_recv[side][d] + self._peer_cap[side][d] * 16 + me * parts * 4
+                    native.memcpy(dst, self.fine_out.ptr + d * parts * 4, parts * 4, self.stream)
+            else:
+                native.check(lib.m4d_partition_owner_push(
+                    self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest,
+                    self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
             self.pushed[side].record(self.stream)
             self._tp(f"push{side}_end")
         self._mark("owner_plan_push_ms")
@@ -450,13 +466,13 @@ class KeyMerge:
         out = []
         for side in range(2):
             self.pushed[side].synchronize()  # my rows for side `side` are in every owner's buffer
-            if side == 1 and self.fine:
+            if side == 1 and self.fine and not self.fine_fused:
                 self.fine_done.synchronize()  # ... and so are my side-1 counts
             await allgather(t, b"\x01", EXCHANGE_TAG + 6 + side)  # ... and every peer's rows in mine
             self._mark(f"side{side}_push_ms")
             self._tp(f"split{side}_start", self.split_streams[side])
             out.append(self._finish_side(side, runs_in[side], C, self.split_streams[side],
-                                         counted=side == 1 and self.fine))
+                                         counted=self.fine_fused or (side == 1 and self.fine)))
             self._tp(f"split{side}_end", self.split_streams[side])
         for side in range(2):  # the join waits for both splits
             if self.split_streams[side] is not self.stream:
@@ -494,7 +510,7 @@ class KeyMerge:
             incoming = [r[C] for r in runs_in]
             total = sum(incoming)
             if total > self.recv[side].capacity:
-                self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096)
+                self.recv[side] = _Pairs(self.device, int(total * 1.1) + 4096, self._recv_extra[side])
             if total > self.parted[side].capacity:
                 self.parted[side] = _Pairs(self.device, int(total * 1.1) + 4096)
             send_t = _torch_bytes(self.sendbuf[side].ptr, max(1, b[P * C] * 16), self.device)

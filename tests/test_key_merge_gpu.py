@@ -394,10 +394,12 @@ def test_tuning_knobs_keep_the_digest(env):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("fine", ["0", "1"])
+@pytest.mark.parametrize("fine", ["0", "1", "separate"])
 def test_counted_receiver_split_matches_the_oracle(world, fine):
-    """M4D_MERGE_FINE: side 1's receiver split with the senders' per-partition counts (no
-    histogram pass) and without; both equal to the oracle, over two steps."""
+    """M4D_MERGE_FINE: receiver splits with the senders' per-partition counts (no
+    histogram pass) -- counted by the push itself for both sides (default), or by a
+    separate pass for side 1 (M4D_MERGE_FINE_FUSED=0) -- and without; all equal to the
+    oracle, over two steps."""
     import os
     import subprocess
     import sys
@@ -406,9 +408,62 @@ def test_counted_receiver_split_matches_the_oracle(world, fine):
     code = _VARIANT_SCRIPT.format(root=root, tests=os.path.join(root, "tests"), rows=200_000, world=world)
     code = code.replace("run_world(200000, %d, 0.3)" % world, "run_world(200000, %d, 0.3, steps=2)" % world)
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
-                         env=dict(os.environ, M4D_MERGE_FINE=fine))
+                         env=dict(os.environ, M4D_MERGE_FINE="1" if fine == "separate" else fine,
+                                  M4D_MERGE_FINE_FUSED="0" if fine == "separate" else "1"))
     assert out.returncode == 0, out.stderr[-2000:]
     assert eval(out.stdout.strip().splitlines()[-1]) == list(oracle.key_merge_c(200_000, world, 0.3))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_push_fine_counts_exact_under_extreme_skew(world):
+    """m4d_partition_owner_push_fine: the push scatter's own (owner, partition) counts
+    spill their 16-bit shared counters exactly under one key repeated 3M times, equal a
+    numpy recount, and the pushed rows equal m4d_partition_owner_push's."""
+    from paper_2101_08878_b200 import native
+
+    lib = native.lib()
+    n, parts = 4_000_000, 8192
+    coarse = lib.m4d_owner_coarse_count(world)
+    keys = np.full(n, 987654321, dtype=np.int64)
+    keys[3_000_000:] = np.arange(1_000_000, dtype=np.int64) * 104729
+    vals = np.arange(n, dtype=np.int64)
+    k_d, v_d = native.DeviceBuffer(0, n * 8), native.DeviceBuffer(0, n * 8)
+    native.memcpy(k_d.ptr, keys.ctypes.data, n * 8)
+    native.memcpy(v_d.ptr, vals.ctypes.data, n * 8)
+    nb = world * coarse
+    nbytes = lib.m4d_partition_scratch_bytes(n, nb)
+    scratch = native.DeviceBuffer(0, nbytes)
+    bounds = native.DeviceBuffer(0, (nb + 1) * 8)
+    native.check(lib.m4d_partition_owner_plan(k_d.ptr, v_d.ptr, n, world, coarse, bounds.ptr, scratch.ptr, nbytes,
+                                              None))
+    native.check(lib.m4d_device_sync(0))
+    b = np.frombuffer(native.to_host(bounds.ptr, (nb + 1) * 8), dtype=np.int64)
+    seg = [int(b[d * coarse]) for d in range(world)] + [n]
+    outs = []
+    for fused in (False, True):
+        dests = [native.DeviceBuffer(0, max(1, seg[d + 1] - seg[d]) * 16) for d in range(world)]
+        addrs = (ctypes.c_uint64 * world)(*[d.ptr for d in dests])
+        counts = native.DeviceBuffer(0, world * parts * 4)
+        native.memset(counts.ptr, 0xFF, world * parts * 4)  # the call zeroes them
+        if fused:
+            native.check(lib.m4d_partition_owner_push_fine(k_d.ptr, v_d.ptr, n, world, coarse, addrs, parts,
+                                                           counts.ptr, scratch.ptr, nbytes, None))
+        else:
+            native.check(lib.m4d_partition_owner_push(k_d.ptr, v_d.ptr, n, world, coarse, addrs, scratch.ptr,
+                                                      nbytes, None))
+        native.check(lib.m4d_device_sync(0))
+        rows = [np.frombuffer(native.to_host(dests[d].ptr, (seg[d + 1] - seg[d]) * 16), dtype=np.int64)
+                .reshape(-1, 2) for d in range(world)]
+        outs.append([r[np.argsort(r[:, 1], kind="stable")] for r in rows])
+        if fused:
+            got = np.frombuffer(native.to_host(counts.ptr, world * parts * 4), dtype=np.uint32)
+    for a, c in zip(*outs):
+        assert np.array_equal(a, c)
+    h = oracle.splitmix64_np(keys.view(np.uint64))
+    owner = ((h >> np.uint64(32)) * np.uint64(world)) >> np.uint64(32)
+    p = (h & np.uint64(0xFFFFFFFF)) >> np.uint64(32 - 13)
+    want = np.bincount((owner * np.uint64(parts) + p).astype(np.int64), minlength=world * parts)
+    assert np.array_equal(got.astype(np.int64), want)
 
 
 def test_fine_counts_exact_under_extreme_skew():

@@ -1,0 +1,12 @@
+#!/bin/bash
+# Push scatter with fused (owner, partition) counts (M4D_MERGE_FINE_FUSED=1, both receiver splits counted)
+# vs the separate side-1 count pass: tests, then N=2 (and N=4 when present) step times.
+exec > gpurun_out/r2_push_fine.log 2>&1
+timeout 1200 python -m pytest tests/test_key_merge_gpu.py tests/test_multiprocess_gpu.py -x -q 2>&1 | tail -3
+G=$(nvidia-smi -L | wc -l)
+for n in 2 4; do [ $n -le $G ] || continue; for rep in 1 2; do for fused in 1 0; do
+  M4D_MERGE_FINE_FUSED=$fused timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $((29600 + RANDOM % 300)) bench.py --gpus $n --workload key_merge --skip-cpu --skip-e2e --steps 10 > gpurun_out/r2_pf_${n}_${fused}.json 2>gpurun_out/r2_pf_${n}_${fused}.err
+  python -c "
+import json; d=json.loads([l for l in open('gpurun_out/r2_pf_${n}_${fused}.json') if l.startswith('{')][-1]); t=d['roofline']['trace_ms']
+print('N=$n fused=$fused step', round(d['ms_per_step'],3), 'parity', d['parity']['digest_equal'], 'push0_end', t['push0_end'], 'push1_end', t['push1_end'], 'split0_end', t['split0_end'], 'split1', t['split1_start'], t['split1_end'], 'join_end', t['join_end'])"
+done; done; done
