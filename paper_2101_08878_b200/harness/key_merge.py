@@ -131,11 +131,14 @@ class KeyMerge:
         lib = native.lib()
         self.fine = (world > 1 and (shuffle or _SHUFFLE) == "push" and os.environ.get("M4D_MERGE_FINE", "1") != "0"
                      and self.parts > 1 and world * self.parts * 2 <= lib.m4d_fine_count_smem_limit())
-        # M4D_MERGE_FINE_FUSED=1 (default where the counters fit the push CTA's shared memory,
-        # P <= 4 at 8192 partitions): the push scatter itself counts both sides' rows per
-        # (owner, partition) -- no separate count pass, and both receiver splits are counted
-        self.fine_fused = (self.fine and os.environ.get("M4D_MERGE_FINE_FUSED", "1") != "0"
-                           and world * self.parts * 2 <= lib.m4d_push_fine_smem_limit())
+        # M4D_MERGE_FINE_FUSED (default: where the 16-bit counters take <= 32 KB, P = 2 at 8192
+        # partitions): the push scatter itself counts both sides' rows per (owner, partition)
+        # -- no separate count pass, and both receiver splits are counted.  N=2 6.06 -> 5.88 ms;
+        # at N=4 the push CTAs' count flush (4 x 8192 global adds each) ate the gain (7.34-7.54
+        # vs 7.31 ms, profiles/r2_push_fine.txt), so =1 forces it wherever the counters fit.
+        fused = os.environ.get("M4D_MERGE_FINE_FUSED", "")
+        limit = lib.m4d_push_fine_smem_limit() if fused == "1" else min(lib.m4d_push_fine_smem_limit(), 32768)
+        self.fine_fused = self.fine and fused != "0" and world * self.parts * 2 <= limit
         fine_bytes = world * self.parts * 4 if self.fine else 0
         # bytes after each receive buffer's rows: the senders' counts (kept when a buffer grows)
         self._recv_extra = [fine_bytes if self.fine_fused else 0, fine_bytes]
