@@ -319,13 +319,17 @@ m4d_status m4d_partition_fine_counts(const int64_t* keys, const int64_t* vals, i
                                      uint32_t* out_counts, void* stream);
 /* The push scatter (m4d_partition_owner_push) counting its rows per (owner,
  * local partition) in the same pass: out_counts[world][parts] (32-bit, zeroed
- * by the call) is what m4d_partition_fine_counts returns, without another read
- * of the keys.  parts a power of two, world * parts * 2 <=
+ * by the call; the buffer holds world * parts + 1 words, the last one the
+ * kernel's completion counter) is what m4d_partition_fine_counts returns,
+ * without another read of the keys; count_dest (may be NULL): for each owner d
+ * the address (e.g. in its IPC-mapped receive buffer) that receives row d,
+ * written by the kernel's last CTA.  parts a power of two, world * parts * 2 <=
  * m4d_push_fine_smem_limit(); run tables as for m4d_partition_owner_push. */
 size_t m4d_push_fine_smem_limit(void);
 m4d_status m4d_partition_owner_push_fine(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
-                                         const uint64_t* seg_dest, int parts, uint32_t* out_counts, void* scratch,
-                                         size_t scratch_bytes, void* stream);
+                                         const uint64_t* seg_dest, int parts, uint32_t* out_counts,
+                                         const uint64_t* count_dest, void* scratch, size_t scratch_bytes,
+                                         void* stream);
 m4d_status m4d_partition_runs_counted(const int64_t* in_pairs, int64_t n, const int64_t* runs_host, int coarse,
                                       int sources, int buckets, const uint32_t* fine_in, int64_t* out_pairs,
                                       int64_t* bounds, void* scratch, size_t scratch_bytes, void* stream);

@@ -491,8 +491,10 @@ struct SpecArgs {
     uint32_t* counts = nullptr;              // [buckets][ctas]
     int* overflow = nullptr;
     const int* gate = nullptr;
-    uint32_t* fine_out = nullptr;  // kFine (push): [world][1 << log2full] counts of this sender's rows
+    uint32_t* fine_out = nullptr;  // kFine (push): [world][1 << log2full] counts of this sender's rows, + a
+                                   // completion counter word
     int fine_ids = 0;              // world << log2full
+    uint32_t* fine_dst[kMaxPushOwners] = {};  // kFine: where owner d takes this sender's row of counts (or null)
 };
 
 template <int kT, bool kPush, bool kBulk, bool kSpec = false, bool kFine = false>
@@ -687,6 +689,21 @@ __global__ void __launch_bounds__(kT, (kT >= 1024 ? 1 : kT >= 512 ? 2 : 4)) tile
         for (int i = threadIdx.x; i < spec.fine_ids; i += blockDim.x) {
             const uint32_t c = (fc.smem[i >> 1] >> ((i & 1) * 16)) & 0xffffu;
             if (c) atomicAdd(fc.global32 + i, c);
+        }
+        // the last CTA to finish hands every owner its row of counts (peer stores into the
+        // owner's buffer), so no copy follows the kernel
+        __threadfence();
+        __syncthreads();
+        __shared__ int last_cta;
+        if (threadIdx.x == 0) last_cta = atomicAdd(spec.fine_out + spec.fine_ids, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last_cta) {
+            __threadfence();
+            const int parts = 1 << spec.log2full;
+            for (int i = threadIdx.x; i < spec.fine_ids; i += blockDim.x) {
+                uint32_t* dst = spec.fine_dst[i >> spec.log2full];
+                if (dst) dst[i & (parts - 1)] = __ldcg(spec.fine_out + i);
+            }
         }
     }
 }
@@ -1524,8 +1541,8 @@ static m4d_status partition_single(const int64_t* keys, const int64_t* vals, int
     }
     if (phases & kScatter) {
         if (buckets <= kTileBuckets) {
-            if (fine.fine_out)
-                M4D_CUDA_TRY(cudaMemsetAsync(fine.fine_out, 0, static_cast<size_t>(fine.fine_ids) * sizeof(uint32_t), s));
+            if (fine.fine_out)  // counts + the completion counter
+                M4D_CUDA_TRY(cudaMemsetAsync(fine.fine_out, 0, static_cast<size_t>(fine.fine_ids + 1) * sizeof(uint32_t), s));
             M4D_CUDA_TRY(launch_tile_scatter(ctas, s, keys, vals, n, run, mode, buckets, log2b, offs,
                                              reinterpret_cast<longlong2*>(out_pairs), push, fine));
         } else {
@@ -1712,8 +1729,9 @@ size_t m4d_push_fine_smem_limit(void) {
 }
 
 m4d_status m4d_partition_owner_push_fine(const int64_t* keys, const int64_t* vals, int64_t n, int world, int coarse,
-                                         const uint64_t* seg_dest, int parts, uint32_t* fine_out, void* scratch,
-                                         size_t scratch_bytes, void* stream) {
+                                         const uint64_t* seg_dest, int parts, uint32_t* fine_out,
+                                         const uint64_t* count_dest, void* scratch, size_t scratch_bytes,
+                                         void* stream) {
     int cbits = 0;
     const m4d_status st = owner_coarse_check(n, world, coarse, &cbits);
     if (st != M4D_OK) return st;
@@ -1729,6 +1747,7 @@ m4d_status m4d_partition_owner_push_fine(const int64_t* keys, const int64_t* val
     fine.fine_out = fine_out;
     fine.fine_ids = world * parts;
     fine.log2full = pbits;
+    for (int d = 0; d < world && count_dest; ++d) fine.fine_dst[d] = reinterpret_cast<uint32_t*>(count_dest[d]);
     return partition_single(keys, vals, n, M4D_PART_OWNER_COARSE, world * coarse, cbits, nullptr, nullptr, scratch,
                             scratch_bytes, static_cast<cudaStream_t>(stream), kScatter, &push, true, fine);
 }

@@ -133,9 +133,9 @@ class KeyMerge:
                      and self.parts > 1 and world * self.parts * 2 <= lib.m4d_fine_count_smem_limit())
         # M4D_MERGE_FINE_FUSED (default: where the 16-bit counters take <= 32 KB, P = 2 at 8192
         # partitions): the push scatter itself counts both sides' rows per (owner, partition)
-        # -- no separate count pass, and both receiver splits are counted.  N=2 6.06 -> 5.88 ms;
-        # at N=4 the push CTAs' count flush (4 x 8192 global adds each) ate the gain (7.34-7.54
-        # vs 7.31 ms, profiles/r2_push_fine.txt), so =1 forces it wherever the counters fit.
+        # -- no separate count pass, and both receiver splits are counted.  N=2 6.05 -> 5.84 ms;
+        # at N=4 the push CTAs' count flush (4 x 8192 global adds each) ate the gain (7.22-7.28
+        # vs 7.17-7.23 ms, profiles/r2_push_fine.txt), so =1 forces it wherever the counters fit.
         fused = os.environ.get("M4D_MERGE_FINE_FUSED", "")
         limit = lib.m4d_push_fine_smem_limit() if fused == "1" else min(lib.m4d_push_fine_smem_limit(), 32768)
         self.fine_fused = self.fine and fused != "0" and world * self.parts * 2 <= limit
@@ -144,7 +144,7 @@ class KeyMerge:
         self._recv_extra = [fine_bytes if self.fine_fused else 0, fine_bytes]
         self.recv = [_Pairs(device, slack, self._recv_extra[0]), _Pairs(device, slack, self._recv_extra[1])] if world > 1 else None
         if self.fine:
-            self.fine_out = native.DeviceBuffer(device, fine_bytes)
+            self.fine_out = native.DeviceBuffer(device, fine_bytes + 256)  # + the push's completion counter
             self.fine_done = native.Event()
         self.parted = [_Pairs(device, slack), _Pairs(device, slack)]
         self.bounds = [native.DeviceBuffer(device, (max(self.parts, world) + 1) * 8) for _ in range(2)]
@@ -452,12 +452,13 @@ class KeyMerge:
             native.set_device(self.device)
             if self.fine_fused:  # the push counts my rows per (owner, partition) as it moves them
                 parts = self.parts
+                # owner d's row of counts goes after the rows of its receive buffer (written by
+                # the kernel's last CTA)
+                cdst = (ctypes.c_uint64 * P)(*[self._peer_recv[side][d] + self._peer_cap[side][d] * 16 + me * parts * 4
+                                               for d in range(P)])
                 native.check(lib.m4d_partition_owner_push_fine(
                     self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest, parts,
-                    self.fine_out.ptr, self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
-                for d in range(P):  # owner d's row of counts, after the rows of its receive buffer
-                    dst = self._peer_recv[side][d] + self._peer_cap[side][d] * 16 + me * parts * 4
-                    native.memcpy(dst, self.fine_out.ptr + d * parts * 4, parts * 4, self.stream)
+                    self.fine_out.ptr, cdst, self.push_scratch[side].ptr, self.push_scratch_bytes, self.stream.handle))
             else:
                 native.check(lib.m4d_partition_owner_push(
                     self.inputs[side].keys.ptr, self.inputs[side].vals.ptr, self.n, P, C, dest,

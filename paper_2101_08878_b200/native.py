@@ -171,7 +171,7 @@ SIGNATURES: dict[str, tuple] = {
                                                 _c_void_p, _size, _c_void_p]),
     "m4d_push_fine_smem_limit": (_size, []),
     "m4d_partition_owner_push_fine": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,
-                                                     ctypes.c_int, _c_void_p, _c_void_p, _size, _c_void_p]),
+                                                     ctypes.c_int, _c_void_p, _c_void_p, _c_void_p, _size, _c_void_p]),
     "m4d_partition_launches": (ctypes.c_int, [ctypes.c_int]),
     "m4d_fine_count_smem_limit": (_size, []),
     "m4d_partition_fine_counts": (ctypes.c_int, [_c_void_p, _c_void_p, _i64, ctypes.c_int, ctypes.c_int, _c_void_p,

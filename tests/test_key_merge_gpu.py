@@ -443,11 +443,14 @@ def test_push_fine_counts_exact_under_extreme_skew(world):
     for fused in (False, True):
         dests = [native.DeviceBuffer(0, max(1, seg[d + 1] - seg[d]) * 16) for d in range(world)]
         addrs = (ctypes.c_uint64 * world)(*[d.ptr for d in dests])
-        counts = native.DeviceBuffer(0, world * parts * 4)
-        native.memset(counts.ptr, 0xFF, world * parts * 4)  # the call zeroes them
+        counts = native.DeviceBuffer(0, world * parts * 4 + 4)
+        native.memset(counts.ptr, 0xFF, world * parts * 4 + 4)  # the call zeroes them
+        handed = native.DeviceBuffer(0, world * parts * 4)  # where each owner takes its row
+        native.memset(handed.ptr, 0xFF, world * parts * 4)
+        cdst = (ctypes.c_uint64 * world)(*[handed.ptr + d * parts * 4 for d in range(world)])
         if fused:
             native.check(lib.m4d_partition_owner_push_fine(k_d.ptr, v_d.ptr, n, world, coarse, addrs, parts,
-                                                           counts.ptr, scratch.ptr, nbytes, None))
+                                                           counts.ptr, cdst, scratch.ptr, nbytes, None))
         else:
             native.check(lib.m4d_partition_owner_push(k_d.ptr, v_d.ptr, n, world, coarse, addrs, scratch.ptr,
                                                       nbytes, None))
@@ -457,6 +460,7 @@ def test_push_fine_counts_exact_under_extreme_skew(world):
         outs.append([r[np.argsort(r[:, 1], kind="stable")] for r in rows])
         if fused:
             got = np.frombuffer(native.to_host(counts.ptr, world * parts * 4), dtype=np.uint32)
+            assert np.array_equal(np.frombuffer(native.to_host(handed.ptr, world * parts * 4), dtype=np.uint32), got)
     for a, c in zip(*outs):
         assert np.array_equal(a, c)
     h = oracle.splitmix64_np(keys.view(np.uint64))
