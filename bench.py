@@ -621,6 +621,33 @@ def p2p_config(args) -> dict:
     return {"workload": "p2p", "sizes": f"1 B - {args.max_size} B, x4 steps", "window": 64}
 
 
+def bench_p2p_brief(args, dist: Dist) -> dict | None:
+    """p2p sub-record of the default line at N >= 2 (the p2p half of BASELINE.json's
+    metric, so it reaches the driver's multi-GPU records): ranks 0 and 1 over the
+    transport, device frames, osu_bw at 4 / 16 MiB (window 64, distinct buffers) and
+    1 B latency (the eager device protocol, rendezvous, host frames).  The full sweep
+    and the reference socket stack: --workload p2p."""
+    from paper_2101_08878_b200.harness import p2p
+
+    t = open_transport(dist, dist.device)  # every rank (already open after key_merge)
+    out = None
+    if dist.rank < 2:
+        peer = 1 - dist.rank
+        bw = {}
+        for n in (4 << 20, 16 << 20):
+            p2p.verify_once(t, peer, n, True)
+            bw[n] = p2p.osu_bw(t, peer, n, 64, 4, True)
+        eager = p2p.osu_latency(t, peer, 1, 1000, True, eager=True) if getattr(t, "eager_device_max", 0) else None
+        rdv = p2p.osu_latency(t, peer, 1, 1000, True)
+        host = p2p.osu_latency(t, peer, 1, 2000, False)
+        out = {"metric": "p2p GB/s (osu_bw, >= 4 MiB)", "value": max(bw.values()), "unit": "GB/s",
+               "osu_bw_GBps": {"4MiB": bw[4 << 20], "16MiB": bw[16 << 20]},
+               "latency_1B_us": {"device_eager": eager, "device_rendezvous": rdv, "host": host},
+               "ranks": "0 <-> 1", "frames": "device, distinct buffers per message, verified once per size"}
+    dist.barrier()
+    return out if dist.rank == 0 else None
+
+
 def bench_p2p(args, dist: Dist, peaks: dict) -> dict | None:
     from paper_2101_08878_b200.harness import p2p
 
@@ -960,6 +987,7 @@ def main(argv=None) -> int:
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--no-merge", action="store_true", help="default run without the key_merge sub-record")
+    ap.add_argument("--skip-p2p", action="store_true", help="default run at N >= 2 without the p2p sub-record")
     ap.add_argument("--traffic", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture (reported as roofline.traffic)")
     args = ap.parse_args(argv)
@@ -1011,6 +1039,10 @@ def main(argv=None) -> int:
                                                         "scaling", "dtype", "config", "gpu_launches", "roofline",
                                                         "e2e", "cpu_baseline", "parity", "clocks", "wall_ms_per_step",
                                                         "partitions", "digest")}
+            if dist.world >= 2 and not args.skip_p2p:
+                p2 = bench_p2p_brief(args, dist)
+                if line is not None and p2 is not None:
+                    line["p2p"] = p2
     finally:
         if getattr(dist, "transport", None) is not None:
             dist.barrier()
